@@ -248,23 +248,31 @@ def _compositions(total, caps):
             yield [v] + rest
 
 
-def plan_bruteforce(h, f, grid, c):
-    """Exhaustive search (tiny N, nK <= 4): lexicographic min of (D exact, sum x dK^2) (R2, R7).
+D_TIE_REL = 1e-9   # D totals closer than this (relative) are equal: c is a real-valued
+                   # loss given as doubles, so 0.006*1 + 0.006*3 vs 0.006*4 must tie (R7)
 
-    Costs are summed exactly in rationals.  Returns (x, n_optimal_plans_with_equal_key).
+
+def plan_bruteforce(h, f, grid, c):
+    """Exhaustive search (tiny N, nK <= 4): lexicographic min of (D, sum x dK^2) (R2, R7).
+
+    D totals are summed exactly in rationals of the given doubles and compared with the
+    relative tolerance D_TIE_REL; sum x dK^2 is an exact integer.
+    Returns (x, number of plans sharing the optimal key).
     """
     nK = len(grid)
     Dfr = [[Fraction(0) if grid[j] <= grid[i] else Fraction(float(c[grid[j] - grid[i]]))
             for j in range(nK)] for i in range(nK)]
-    best, best_key, ties = None, None, 0
+    plans = []
     for x in _plans([int(v) for v in h], [int(v) for v in f]):
-        key = (sum(x[i][j] * Dfr[i][j] for i in range(nK) for j in range(nK)),
-               sum(x[i][j] * (grid[j] - grid[i]) ** 2 for i in range(nK) for j in range(nK)))
-        if best_key is None or key < best_key:
-            best, best_key, ties = x, key, 1
-        elif key == best_key:
-            ties += 1
-    return np.array(best, dtype=np.int64), ties
+        D = sum(x[i][j] * Dfr[i][j] for i in range(nK) for j in range(nK))
+        Q = sum(x[i][j] * (grid[j] - grid[i]) ** 2 for i in range(nK) for j in range(nK))
+        plans.append((D, Q, x))
+    dmin = min(p[0] for p in plans)
+    tol = Fraction(D_TIE_REL) * max(Fraction(1), dmin)
+    near = [p for p in plans if p[0] - dmin <= tol]
+    qmin = min(p[1] for p in near)
+    best = [p for p in near if p[1] == qmin]
+    return np.array(best[0][2], dtype=np.int64), len(best)
 
 
 def plan_lp(h, f, grid, c):
@@ -295,7 +303,7 @@ def plan_lp(h, f, grid, c):
     if r1.status != 0:
         raise RuntimeError(f"phase-1 LP failed: {r1.message}")
     dstar = float(r1.fun)
-    r2 = linprog(Q, A_ub=D[None, :], b_ub=[dstar + 1e-9 * max(1.0, abs(dstar))],
+    r2 = linprog(Q, A_ub=D[None, :], b_ub=[dstar + D_TIE_REL * max(1.0, abs(dstar))],
                  A_eq=A_eq, b_eq=b_eq, bounds=(0, None), method="highs")
     if r2.status != 0:
         raise RuntimeError(f"phase-2 LP failed: {r2.message}")

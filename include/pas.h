@@ -1,0 +1,211 @@
+/*
+ * pas.h -- C-ABI of libpas, the B200-native prompt-routing hot path of
+ *          "Prompt-Aware Scheduling for Efficient Text-to-Image Inferencing System"
+ *          (arxiv 2502.06798; /root/reference/PAPER.md, cited as P:<line>).
+ *
+ * One call, pas_route_batch, runs the paper's per-batch Query Dispatcher path for N prompts:
+ *   a1 normalise + quantise the prompt embeddings            ("closeness")
+ *   a3 cosine similarity vs the approximate-cache store with a fused running top-k
+ *                                                            ("retrieves the nearest cache")
+ *   a4 merge of per-range / per-GPU candidates
+ *   a5 best similarity -> optimal-K, H_K histogram
+ *   a6 targets f from F(K), Eq. 1 K->K' route plan, D_Q      (P:88-P:96, Eq. 1)
+ *   a7 redirection sampling (Philox, reproducible)           ("K-to-K' Router")
+ *   a8 route-and-batch (greedy / uniform) into per-instance FIFO batches
+ * Readings of silent or garbled passages are R1..R20 in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns pas_status; nothing throws across the ABI.  Arguments are
+ *     validated before anything is enqueued, so a validation error writes nothing.
+ *     pas_last_error(ctx) returns a per-context message for the last failure.
+ *   - A CUDA or NCCL failure is sticky: the context is poisoned (every later call returns
+ *     PAS_ERR_STATE) and must be destroyed.
+ *   - Pointers named *_dev are device pointers on cfg.device; *_host are host pointers.
+ *     Device work is enqueued on the caller's stream (stream-ordered, no host sync) unless
+ *     the function says it synchronises.
+ *   - One context per stream; calls on one context are not re-entrant.
+ *   - Sizes are element counts unless stated.  Layouts are row-major, C order.
+ */
+#ifndef PAS_H_
+#define PAS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pas_ctx pas_ctx;          /* opaque, library-owned */
+typedef struct CUstream_st* pas_stream;  /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  PAS_OK = 0,
+  PAS_ERR_ARG = -1,          /* bad pointer / size / value */
+  PAS_ERR_STATE = -2,        /* call order violated, or context poisoned */
+  PAS_ERR_FRACTIONS = -3,    /* F(K) invalid (F >= 0, sum F = 1 +- 1e-9) */
+  PAS_ERR_NO_INSTANCE = -4,  /* F_j > 0 but no serving instance at level j */
+  PAS_ERR_BANDS = -5,        /* K grid / thresholds invalid */
+  PAS_ERR_DEGRADATION = -6,  /* c(dK) not c[0]=0, non-decreasing, convex (R6) */
+  PAS_ERR_CAPACITY = -7,     /* store or batch capacity exceeded */
+  PAS_ERR_CUDA = -8,
+  PAS_ERR_NCCL = -9,
+  PAS_ERR_INVALID_ROWS = -10 /* pas_cache_load: a row is non-finite or has zero norm (R16) */
+} pas_status;
+
+typedef enum { PAS_F32 = 0, PAS_BF16 = 1 } pas_dtype;
+typedef enum { PAS_GREEDY = 0, PAS_UNIFORM = 1 } pas_mode;  /* P:104 high / low load */
+
+#define PAS_MAX_LEVELS 16        /* nK <= 16 (configs use 6 and 10) */
+#define PAS_MAX_INSTANCES 64     /* W <= 64 serving instances */
+#define PAS_T_TOTAL 50           /* total denoising steps */
+#define PAS_MAX_TOPK 16
+#define PAS_NCCL_ID_BYTES 128
+
+/* Flags per prompt (pas_route_out.flags), informational; the oracle grades with its own. */
+#define PAS_FLAG_INVALID 1        /* non-finite or zero-norm embedding -> treated as cold (R16) */
+#define PAS_FLAG_COLD 2           /* empty cache -> K = 0 */
+#define PAS_FLAG_NEAR_TOP1 4      /* GPU s1 - s2 < 2e-2 (north_star near-tie margin) */
+#define PAS_FLAG_NEAR_THRESHOLD 8 /* GPU |s1 - t_m| < 2e-2 for some threshold t_m */
+
+typedef struct {
+  int d;                       /* embedding width; multiple of 64, 64..4096 (configs: 768) */
+  int topk;                    /* k, 1..PAS_MAX_TOPK (default 8) */
+  int64_t max_batch;           /* largest N accepted by pas_route_batch */
+  int64_t max_rows_per_rank;   /* store capacity of THIS rank's shard, rows */
+  int device;                  /* CUDA device ordinal */
+  int rank, world;             /* router GPUs: 0 <= rank < world; cache gid g lives on rank g % world */
+  const unsigned char* nccl_id;/* PAS_NCCL_ID_BYTES from pas_nccl_unique_id on rank 0, broadcast by the
+                                  caller; required iff world > 1 and pas_route_batch is to be used.
+                                  NULL with world > 1 = "external transport": only the split calls
+                                  pas_route_local / pas_route_from_candidates are available. */
+  uint64_t seed;               /* Philox key of the redirection / uniform-routing streams (R18) */
+} pas_config;
+
+/* Per-prompt outputs, caller-owned DEVICE arrays (SoA).  Required arrays must be non-NULL. */
+typedef struct {
+  int32_t* K;               /* [N] optimal-K value (grid value, not index)                 required */
+  int32_t* K_prime;         /* [N] K' the prompt is served at                              required */
+  int32_t* instance;        /* [N] serving instance id in [0, W) ("gpu" of the north star, R12) required */
+  int32_t* slot;            /* [N] FIFO position within that instance; batch = slot / bstar  required */
+  int32_t* topk_id;         /* [N*topk] global cache ids of the k nearest, -1 padded         optional */
+  float* topk_score;        /* [N*topk] their cosine similarities, -inf padded              optional */
+  uint8_t* flags;           /* [N] PAS_FLAG_* bits                                          optional */
+  int32_t* bucket_offsets;  /* [W+1] exclusive scan of per-instance counts                  optional */
+  int32_t* bucket_prompts;  /* [N] prompt ids grouped by instance, FIFO (slot) order         optional */
+} pas_route_out;
+
+/* Host-side view of the last batch's plan (pas_plan_stats). */
+typedef struct {
+  int nK, W;
+  int64_t N;
+  int64_t h[PAS_MAX_LEVELS];                    /* H_K counts (R4) */
+  int64_t f[PAS_MAX_LEVELS];                    /* integer targets from F (R3) */
+  int64_t x[PAS_MAX_LEVELS][PAS_MAX_LEVELS];    /* route plan: x[i][j] prompts with optimal level i served at j */
+  double D_Q;                                   /* Eq. 1 on the integer plan, sum_{K_j>K_i} x_ij D_ij / N */
+  double D_Q_LP;                                /* Eq. 1 optimum on unrounded (h/N, F), context only */
+  int64_t n_redirected, n_upgraded, n_downgraded;   /* K'!=K, K'<K (slower/better), K'>K */
+  int64_t n_invalid, n_near_top1, n_near_threshold;
+  int64_t bucket_count[PAS_MAX_INSTANCES];      /* prompts per instance */
+  float stage_ms[8];    /* device ms per stage of the last batch: [0] normalise, [1] similarity+top-k,
+                           [2] merge + collective + optimal-K/H_K, [3] plan, [4] redirect,
+                           [5] route-and-batch, [6] total, [7] unused */
+} pas_stats;
+
+/* Library and build identification ("sm_100a", version). Never fails. */
+const char* pas_version(void);
+
+/* Create a context: allocates the store (max_rows_per_rank x d bf16), the per-batch workspace
+ * and, if world > 1 and nccl_id != NULL, the NCCL communicator (collective over all ranks).
+ * Defaults after create: no bands (pas_set_bands required), c(dK) = 0.006 dK (R6),
+ * batch_seq = 0.  Errors: PAS_ERR_ARG (bad cfg), PAS_ERR_CUDA (allocation), PAS_ERR_NCCL. */
+pas_status pas_create(pas_ctx** ctx, const pas_config* cfg);
+
+/* Destroy a context (also poisoned ones); frees everything it owns.  NULL is a no-op. */
+pas_status pas_destroy(pas_ctx* ctx);
+
+/* NCCL unique id for the world>1 bootstrap (rank 0 calls it, the caller broadcasts the bytes).
+ * out: PAS_NCCL_ID_BYTES host bytes.  Errors: PAS_ERR_NCCL if NCCL cannot be loaded. */
+pas_status pas_nccl_unique_id(unsigned char* out);
+
+/* Append M cache rows (the approximate-cache store).  Every rank passes the SAME rows;
+ * global id g = (rows already loaded) + i; this rank keeps rows with g % world == rank at local row
+ * g / world, normalised and rounded to bf16 at insert (a2: v / |v|_2, norm in fp64, fp32 RN, bf16 RNE).
+ * rows_dev: device [M x d] of dtype.  first_gid (optional, host): receives the first gid.
+ * Synchronises the stream (validity check).  Errors: PAS_ERR_CAPACITY (shard full, nothing appended),
+ * PAS_ERR_INVALID_ROWS (some row non-finite / zero-norm; nothing appended), PAS_ERR_ARG. */
+pas_status pas_cache_load(pas_ctx* ctx, const void* rows_dev, pas_dtype dtype, int64_t M,
+                          int64_t* first_gid, pas_stream stream);
+
+/* Drop every cached row (global count back to 0).  Stream-ordered. */
+pas_status pas_cache_clear(pas_ctx* ctx);
+
+/* Rows in the store: global total (all ranks) and this rank's shard. */
+pas_status pas_cache_size(const pas_ctx* ctx, int64_t* global_rows, int64_t* local_rows);
+
+/* The optimal-K Selector's similarity bands (R8): K_levels[0..nK) strictly increasing,
+ * K_levels[0] == 0, each < PAS_T_TOTAL; thresholds[0..nK-1) strictly increasing and finite.
+ * A prompt with best similarity s1 gets level #{m : s1 >= thresholds[m]} (bands closed below).
+ * Invalidates previously set fractions.  Errors: PAS_ERR_BANDS. */
+pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const float* thresholds);
+
+/* Degradation c(dK) for dK = 0..len-1 (Eq. 1's D(K',K) = c(K'-K) for K' > K, 0 otherwise; R5, R6).
+ * len must be PAS_T_TOTAL.  c[0] == 0, non-decreasing, convex (second differences >= -1e-12).
+ * Errors: PAS_ERR_DEGRADATION. */
+pas_status pas_set_degradation(pas_ctx* ctx, const double* c_of_dK, int len);
+
+/* Controller outputs for the next batches: F[nK] per-level load fractions (sum 1 +- 1e-9,
+ * F >= 0), instance_level[W] the level index each serving instance runs at (1 <= W <= 64),
+ * bstar >= 1 the optimal batch size ("2-4"), mode greedy (high load) / uniform (low load,
+ * requires bstar == 1, "batch size of 1").  Requires pas_set_bands.
+ * Errors: PAS_ERR_STATE, PAS_ERR_FRACTIONS, PAS_ERR_NO_INSTANCE, PAS_ERR_ARG. */
+pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* instance_level, int W,
+                             int bstar, pas_mode mode);
+
+/* Reset the Philox key and the batch sequence number (R18). */
+pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
+
+/* Route one batch (the hot path).  emb_dev: device [N x d] of dtype, the SAME prompts on every rank.
+ * out: device arrays, written in full on every rank.  N == 0 is a no-op; N > max_batch ->
+ * PAS_ERR_CAPACITY.  Requires bands and fractions (PAS_ERR_STATE).  Enqueue-only (no host sync);
+ * batch_seq increments on success.  world > 1 needs the NCCL communicator. */
+pas_status pas_route_batch(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
+                           const pas_route_out* out, pas_stream stream);
+
+/* Same, from HOST buffers: copies emb_host (should be pinned) to the device, routes, copies every
+ * non-NULL array of out_host (host pointers, same shapes as pas_route_out) back, and synchronises.
+ * This is the end-to-end public path (bench.py "e2e"). */
+pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
+                                const pas_route_out* out_host, pas_stream stream);
+
+/* Split form of pas_route_batch for callers with their own transport (and for single-GPU tests of
+ * the sharded path).  pas_route_local runs a1+a3+the intra-GPU part of a4 on this rank's shard and
+ * writes cand_dev: device [N x topk] pairs {float score; int32 gid} (8 bytes each, score desc, gid asc,
+ * padded (-inf, -1)).  pas_route_from_candidates takes S such blocks laid out [S][N][topk]
+ * (e.g. the all-gather over ranks, S == world), merges them and runs a5..a8 for all N prompts,
+ * using the validity flags of this context's last pas_route_local.  batch_seq increments here. */
+pas_status pas_route_local(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
+                           void* cand_dev, pas_stream stream);
+pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, int64_t N,
+                                     const pas_route_out* out, pas_stream stream);
+
+/* Plan and counters of the last routed batch (host struct).  Synchronises the context's last stream. */
+pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out);
+
+/* Last error message of this context ("" if none).  ctx may be NULL (global errors, e.g. create). */
+const char* pas_last_error(const pas_ctx* ctx);
+
+/* Kernel launches the last pas_route_batch / pas_route_batch_host enqueued (for bench.py's
+ * gpu_launches count). */
+int pas_last_launch_count(const pas_ctx* ctx);
+
+/* ---- test hooks (not part of the routing path) ---------------------------------------------- */
+/* Runs a1 and the a3 GEMM with an epilogue that writes every raw score instead of the top-k:
+ * scores_dev: device [N x local_rows] fp32 (local_rows = this rank's shard size).  For the GEMM's
+ * element-wise parity test on small inputs only. */
+pas_status pas_debug_scores(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N, float* scores_dev,
+                            pas_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAS_H_ */

@@ -1,0 +1,100 @@
+// K1 -- normalise + quantise embedding rows (prompts per batch, cache rows at insert).
+//
+// v_hat_i = bf16_RNE( fp32_RN( v_i / sqrt(sum_j v_j^2) ) ), the sum of squares and the division in
+// fp64 (R11).  Cosine "closeness" of two unit rows is then a dot
+// product, which K2 computes on the tensor cores.  A row with a non-finite element or zero norm is
+// invalid (R16): it is written as zeros and flagged (prompts) or counted (cache insert -> rejected).
+//
+// One warp per row, 128-bit loads (4 fp32 / 8 bf16 per lane per step), two passes over the row (the
+// second pass hits L1).  HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
+// Cache insert applies the shard filter of the round-robin partition (gid g lives on rank g % G at
+// local row g / G) and reads only this rank's rows.
+#include "pas_internal.cuh"
+
+namespace pas {
+namespace {
+
+__device__ __forceinline__ void load4(const float* p, float (&v)[4]) {
+  const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&v)[4]) {
+  const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+  v[0] = __uint_as_float(x.x << 16);
+  v[1] = __uint_as_float(x.x & 0xFFFF0000u);
+  v[2] = __uint_as_float(x.y << 16);
+  v[3] = __uint_as_float(x.y & 0xFFFF0000u);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_normalize(const T* __restrict__ in, int64_t rows, int d,
+                                                   __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
+                                                   int64_t first_gid, int G, int rank, int* invalid_count) {
+  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp_global; i < rows; i += nwarps) {
+    const int64_t gid = first_gid + i;
+    if (G > 1 && (gid % G) != rank) continue;
+    const int64_t orow = (G > 1) ? gid / G : gid;
+    const T* src = in + i * (int64_t)d;
+    double ss = 0.0;
+    bool finite = true;
+    for (int c = lane * 4; c < d; c += 128) {
+      float v[4];
+      load4(src + c, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        finite &= isfinite(v[j]);
+        ss += (double)v[j] * (double)v[j];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    finite = __all_sync(0xffffffffu, finite);
+    const double norm = sqrt(ss);
+    const bool valid = finite && norm > 0.0;
+    __nv_bfloat16* dst = out + orow * (int64_t)d;
+    for (int c = lane * 4; c < d; c += 128) {
+      float v[4];
+      load4(src + c, v);
+      __nv_bfloat162 lo, hi;
+      if (valid) {
+        lo = __floats2bfloat162_rn(__double2float_rn((double)v[0] / norm), __double2float_rn((double)v[1] / norm));
+        hi = __floats2bfloat162_rn(__double2float_rn((double)v[2] / norm), __double2float_rn((double)v[3] / norm));
+      } else {
+        lo = __floats2bfloat162_rn(0.f, 0.f);
+        hi = lo;
+      }
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst + c) = pk;
+    }
+    if (lane == 0) {
+      if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
+      if (!valid && invalid_count) atomicAdd(invalid_count, 1);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
+                             uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
+                             cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (rows * 32 + threads - 1) / threads;
+  const int64_t cap = (int64_t)kNumSMs * 16;  // grid-stride beyond 16 CTAs (128 warps) per SM
+  if (blocks > cap) blocks = cap;
+  if (dtype == PAS_F32)
+    k_normalize<float><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const float*>(in), rows, d, out, flags,
+                                                             first_gid, G, rank, invalid_count);
+  else
+    k_normalize<__nv_bfloat16><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows,
+                                                                     d, out, flags, first_gid, G, rank, invalid_count);
+  return cudaGetLastError();
+}
+
+}  // namespace pas

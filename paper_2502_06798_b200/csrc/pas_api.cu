@@ -1,0 +1,713 @@
+// pas_api.cu -- the C-ABI of libpas (include/pas.h): context, validation, workspace, the batch
+// pipeline K1..K7 on the caller's stream, the cache store, and the NCCL all-gather for world > 1.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "pas_internal.cuh"
+
+using namespace pas;
+
+// ----------------------------------------------------------------------------------------------
+// NCCL, loaded lazily (only world > 1 needs it; torch's bundled libnccl.so.2 is reused if loaded)
+// ----------------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+bool nccl_load() {
+  if (g_nccl.ok) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(h, "ncclCommAbort");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.CommDestroy &&
+              g_nccl.CommAbort && g_nccl.GetErrorString;
+  return g_nccl.ok;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+thread_local std::string g_global_err;
+
+int ceil_log2(int64_t v) {
+  int b = 0;
+  while (((int64_t)1 << b) < v) ++b;
+  return b;
+}
+}  // namespace
+
+// ----------------------------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------------------------
+struct pas_ctx {
+  pas_config cfg{};
+  std::string err;
+  bool poisoned = false;
+  int launches = 0;
+  // state
+  bool bands_set = false, fractions_set = false;
+  int nK = 0, W = 0, bstar = 1, mode = 0;
+  int grid[kMaxLevels]{};
+  float thr[kMaxLevels]{};
+  double F[kMaxLevels]{};
+  double c[kTTotal]{};
+  int inst_level[kMaxInst]{};
+  uint64_t seed = 0, batch_seq = 0;
+  int64_t M_total = 0, M_local = 0, cap_rows = 0, q_rows = 0, cand_cap = 0;
+  int64_t last_local_N = -1;
+  int64_t last_N = 0;
+  // device memory
+  __nv_bfloat16* store = nullptr;
+  __nv_bfloat16* qhat = nullptr;
+  uint8_t* pflags = nullptr;
+  Cand* cand_local = nullptr;
+  Cand* cand_rank = nullptr;
+  Cand* cand_all = nullptr;
+  uint8_t* level = nullptr;
+  int* hist = nullptr;
+  int* invalid_count = nullptr;
+  DevPlan* plan = nullptr;
+  RedirectWs rw{};
+  BatchWs bw{};
+  // host-API staging
+  void* stage_emb = nullptr;
+  int32_t *s_K = nullptr, *s_Kp = nullptr, *s_inst = nullptr, *s_slot = nullptr, *s_tid = nullptr,
+          *s_boff = nullptr, *s_bpr = nullptr;
+  float* s_tsc = nullptr;
+  uint8_t* s_flags = nullptr;
+  // tensor maps
+  CUtensorMap tm_q{}, tm_c{};
+  // comm
+  ncclComm_t comm = nullptr;
+  // timing
+  cudaEvent_t ev[8]{};
+  bool ev_valid = false;
+  cudaStream_t last_stream = nullptr;
+};
+
+namespace {
+
+pas_status fail(pas_ctx* ctx, pas_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) {
+    ctx->err = buf;
+    if (st == PAS_ERR_CUDA || st == PAS_ERR_NCCL) ctx->poisoned = true;
+  } else {
+    g_global_err = buf;
+  }
+  return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                         \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess) return fail((ctx), PAS_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+template <typename T>
+cudaError_t dmalloc(T** p, size_t n) {
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T) + 16);
+}
+
+bool encode_map(CUtensorMap* m, void* base, int64_t rows, int d, int box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t local_rows_below(int64_t total, int G, int rank) {
+  return total > rank ? (total - rank + G - 1) / G : 0;
+}
+
+pas_status check_live(pas_ctx* ctx) {
+  if (!ctx) return fail(nullptr, PAS_ERR_ARG, "null context");
+  if (ctx->poisoned) return fail(ctx, PAS_ERR_STATE, "context poisoned by an earlier CUDA/NCCL error: %s",
+                                 ctx->err.c_str());
+  return PAS_OK;
+}
+
+RouteParams make_params(const pas_ctx* ctx, int64_t N) {
+  RouteParams p{};
+  p.nK = ctx->nK;
+  p.W = ctx->W;
+  p.bstar = ctx->bstar;
+  p.mode = ctx->mode;
+  p.topk = ctx->cfg.topk;
+  p.G = ctx->cfg.world;
+  p.rank = ctx->cfg.rank;
+  p.d = ctx->cfg.d;
+  p.N = N;
+  p.M_total = ctx->M_total;
+  p.seed = ctx->seed;
+  p.batch_seq = ctx->batch_seq;
+  int kb = ceil_log2(N > 1 ? N : 1);
+  p.kb = kb > 16 ? 16 : kb;
+  for (int i = 0; i < kMaxLevels; ++i) {
+    p.grid[i] = ctx->grid[i];
+    p.thr[i] = ctx->thr[i];
+    p.F[i] = ctx->F[i];
+  }
+  for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
+  for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
+  return p;
+}
+
+pas_status validate_out(pas_ctx* ctx, const pas_route_out* out) {
+  if (!out) return fail(ctx, PAS_ERR_ARG, "out is NULL");
+  if (!out->K || !out->K_prime || !out->instance || !out->slot)
+    return fail(ctx, PAS_ERR_ARG, "out->K, K_prime, instance and slot are required");
+  return PAS_OK;
+}
+
+pas_status ready(pas_ctx* ctx, int64_t N) {
+  if (!ctx->bands_set || !ctx->fractions_set)
+    return fail(ctx, PAS_ERR_STATE, "pas_set_bands and pas_set_fractions must be called before routing");
+  if (N < 0) return fail(ctx, PAS_ERR_ARG, "N < 0");
+  if (N > ctx->cfg.max_batch)
+    return fail(ctx, PAS_ERR_CAPACITY, "N = %lld exceeds max_batch = %lld", (long long)N,
+                (long long)ctx->cfg.max_batch);
+  return PAS_OK;
+}
+
+// a1 + a3 (+ the intra-GPU part of a4 into `merged` if non-null).  Returns the candidate layout.
+pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cudaStream_t st, const Cand** cand,
+                     int* S, Cand* merged) {
+  const int k = ctx->cfg.topk;
+  CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+  int R = 1;
+  if (ctx->M_local > 0) {
+    R = simtopk_choose_ranges(N, ctx->M_local);
+    if ((int64_t)R * N > ctx->cand_cap) R = 1;
+    SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
+                  ctx->cand_local, nullptr};
+    CUDA_TRY(ctx, launch_simtopk(a, st));
+  } else {
+    CUDA_TRY(ctx, launch_fill_sentinel(ctx->cand_local, N * k, st));
+  }
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+  *cand = ctx->cand_local;
+  *S = R;
+  if (merged) {
+    CUDA_TRY(ctx, launch_merge(ctx->cand_local, R, N, k, merged, st));
+    ctx->launches++;
+    *cand = merged;
+    *S = 1;
+  }
+  ctx->last_local_N = N;
+  return PAS_OK;
+}
+
+// a4 (final merge) .. a8 for all N prompts from S candidate blocks [S][N][k].
+pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
+  RouteParams p = make_params(ctx, N);
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->hist, 0, sizeof(int) * kMaxLevels, st));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->plan, 0, sizeof(DevPlan), st));
+  SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
+  CUDA_TRY(ctx, launch_merge_select(cand, S, ctx->pflags, p, so, st));
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
+  CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+  CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, st, &ctx->launches));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
+  CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, ctx->bw, out->instance, out->slot,
+                                       out->bucket_offsets, out->bucket_prompts, st, &ctx->launches));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[6], st));
+  ctx->ev_valid = true;
+  ctx->last_stream = st;
+  ctx->last_N = N;
+  ctx->batch_seq++;
+  return PAS_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------------------------
+// C-ABI
+// ----------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* pas_version(void) { return "libpas 0.1 (sm_100a, tcgen05 K2, 1-CTA 128x256)"; }
+
+const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
+
+int pas_last_launch_count(const pas_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+pas_status pas_nccl_unique_id(unsigned char* out) {
+  if (!out) return fail(nullptr, PAS_ERR_ARG, "out is NULL");
+  if (!nccl_load()) return fail(nullptr, PAS_ERR_NCCL, "cannot load libnccl.so.2");
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, PAS_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+  memcpy(out, id.internal, PAS_NCCL_ID_BYTES);
+  return PAS_OK;
+}
+
+pas_status pas_destroy(pas_ctx* ctx) {
+  if (!ctx) return PAS_OK;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  if (ctx->comm) {
+    if (ctx->poisoned) g_nccl.CommAbort(ctx->comm);
+    else g_nccl.CommDestroy(ctx->comm);
+  }
+  void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all,
+                  ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
+                  ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.items,     ctx->rw.cls7,   ctx->rw.lvl_prime,
+                  ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->stage_emb, ctx->s_K, ctx->s_Kp,
+                  ctx->s_inst,  ctx->s_slot,    ctx->s_tid,      ctx->s_boff,       ctx->s_bpr,     ctx->s_tsc,
+                  ctx->s_flags};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+  return PAS_OK;
+}
+
+pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
+  if (!out_ctx || !cfg) return fail(nullptr, PAS_ERR_ARG, "null argument");
+  *out_ctx = nullptr;
+  if (cfg->d < 64 || cfg->d > 4096 || cfg->d % 64)
+    return fail(nullptr, PAS_ERR_ARG, "d = %d must be a multiple of 64 in [64, 4096]", cfg->d);
+  if (cfg->topk < 1 || cfg->topk > PAS_MAX_TOPK)
+    return fail(nullptr, PAS_ERR_ARG, "topk = %d outside [1, %d]", cfg->topk, PAS_MAX_TOPK);
+  if (cfg->max_batch < 1 || cfg->max_batch > (1LL << 26))
+    return fail(nullptr, PAS_ERR_ARG, "max_batch outside [1, 2^26]");
+  if (cfg->max_rows_per_rank < 0 || cfg->max_rows_per_rank > (1LL << 31) / 2)
+    return fail(nullptr, PAS_ERR_ARG, "max_rows_per_rank outside [0, 2^30]");
+  if (cfg->world < 1 || cfg->world > 128 || cfg->rank < 0 || cfg->rank >= cfg->world)
+    return fail(nullptr, PAS_ERR_ARG, "rank/world invalid (1 <= world <= 128, 0 <= rank < world)");
+  if ((int64_t)cfg->max_rows_per_rank * cfg->world >= (1LL << 31))
+    return fail(nullptr, PAS_ERR_ARG, "global ids must fit int32 (max_rows_per_rank * world < 2^31)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return fail(nullptr, PAS_ERR_ARG, "CUDA device %d not available", cfg->device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, PAS_ERR_ARG, "libpas needs an sm_100 device (B200); device %d is sm_%d%d", cfg->device,
+                prop.major, prop.minor);
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(nullptr, PAS_ERR_CUDA, "cudaSetDevice failed");
+
+  pas_ctx* ctx = new pas_ctx();
+  ctx->cfg = *cfg;
+  ctx->cfg.nccl_id = nullptr;
+  ctx->seed = cfg->seed;
+  for (int t = 0; t < kTTotal; ++t) ctx->c[t] = 0.006 * t;   // SPEC S:49 default, R6
+  const int64_t mb = cfg->max_batch, k = cfg->topk, d = cfg->d;
+  ctx->q_rows = (mb + 127) / 128 * 128;
+  ctx->cap_rows = cfg->max_rows_per_rank;
+  ctx->cand_cap = mb > 592 * 128 ? mb : 592 * 128;
+  const int64_t nb = (int64_t)kMaxLevels << 16;
+  const int64_t nblk = (mb + 1023) / 1024;
+  cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, n) \
+  if (e == cudaSuccess) e = dmalloc(&(ptr), (size_t)(n))
+  ALLOC(ctx->store, (ctx->cap_rows > 0 ? ctx->cap_rows : 1) * d);
+  ALLOC(ctx->qhat, ctx->q_rows * d);
+  ALLOC(ctx->pflags, mb);
+  ALLOC(ctx->cand_local, ctx->cand_cap * k);
+  ALLOC(ctx->cand_rank, mb * k);
+  if (cfg->world > 1) ALLOC(ctx->cand_all, (int64_t)cfg->world * mb * k);
+  ALLOC(ctx->level, mb);
+  ALLOC(ctx->hist, kMaxLevels);
+  ALLOC(ctx->invalid_count, 1);
+  ALLOC(ctx->plan, 1);
+  ALLOC(ctx->rw.key, mb);
+  ALLOC(ctx->rw.bucket, mb);
+  ALLOC(ctx->rw.bcount, nb);
+  ALLOC(ctx->rw.bstart, nb);
+  ALLOC(ctx->rw.bfill, nb);
+  ALLOC(ctx->rw.items, mb);
+  ALLOC(ctx->rw.cls7, mb);
+  ALLOC(ctx->rw.lvl_prime, mb);
+  ALLOC(ctx->bw.blk_counts, nblk * 64);
+  ALLOC(ctx->bw.blk_off, nblk * 64);
+  ALLOC(ctx->bw.offsets, kMaxInst + 1);
+#undef ALLOC
+  if (e != cudaSuccess) {
+    pas_destroy(ctx);
+    return fail(nullptr, PAS_ERR_CUDA, "device allocation failed: %s", cudaGetErrorString(e));
+  }
+  for (auto& ev : ctx->ev)
+    if (cudaEventCreate(&ev) != cudaSuccess) {
+      pas_destroy(ctx);
+      return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
+    }
+  if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, 128) ||
+      !encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, 256)) {
+    pas_destroy(ctx);
+    return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
+  }
+  if ((e = simtopk_init()) != cudaSuccess) {
+    pas_destroy(ctx);
+    return fail(nullptr, PAS_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(e));
+  }
+  if (cfg->world > 1 && cfg->nccl_id) {
+    if (!nccl_load()) {
+      pas_destroy(ctx);
+      return fail(nullptr, PAS_ERR_NCCL, "cannot load libnccl.so.2");
+    }
+    ncclUniqueId id;
+    memcpy(id.internal, cfg->nccl_id, PAS_NCCL_ID_BYTES);
+    ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      pas_destroy(ctx);
+      return fail(nullptr, PAS_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+    }
+  }
+  *out_ctx = ctx;
+  return PAS_OK;
+}
+
+pas_status pas_cache_clear(pas_ctx* ctx) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  ctx->M_total = 0;
+  ctx->M_local = 0;
+  return PAS_OK;
+}
+
+pas_status pas_cache_size(const pas_ctx* ctx, int64_t* global_rows, int64_t* local_rows) {
+  if (!ctx) return PAS_ERR_ARG;
+  if (global_rows) *global_rows = ctx->M_total;
+  if (local_rows) *local_rows = ctx->M_local;
+  return PAS_OK;
+}
+
+pas_status pas_cache_load(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64_t M, int64_t* first_gid,
+                          pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
+  if (M < 0 || (M > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / M");
+  const int G = ctx->cfg.world, rank = ctx->cfg.rank;
+  const int64_t new_total = ctx->M_total + M;
+  if (new_total >= (1LL << 31)) return fail(ctx, PAS_ERR_CAPACITY, "global ids must stay below 2^31");
+  const int64_t new_local = local_rows_below(new_total, G, rank);
+  if (new_local > ctx->cap_rows)
+    return fail(ctx, PAS_ERR_CAPACITY, "shard capacity %lld rows exceeded (need %lld)", (long long)ctx->cap_rows,
+                (long long)new_local);
+  if (first_gid) *first_gid = ctx->M_total;
+  if (M == 0) return PAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->invalid_count, 0, sizeof(int), st));
+  // rows are written at local row (first_gid + i) / G of the store
+  CUDA_TRY(ctx, launch_normalize(rows, dtype, M, ctx->cfg.d, ctx->store, nullptr, ctx->M_total, G, rank,
+                                 ctx->invalid_count, st));
+  int bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&bad, ctx->invalid_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (bad) return fail(ctx, PAS_ERR_INVALID_ROWS, "%d of the rows are non-finite or have zero norm", bad);
+  ctx->M_total = new_total;
+  ctx->M_local = new_local;
+  return PAS_OK;
+}
+
+pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const float* thresholds) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!K_levels || nK < 1 || nK > kMaxLevels || (nK > 1 && !thresholds))
+    return fail(ctx, PAS_ERR_BANDS, "need 1 <= nK <= %d levels and nK-1 thresholds", kMaxLevels);
+  if (K_levels[0] != 0) return fail(ctx, PAS_ERR_BANDS, "level 0 required (K_levels[0] == 0, S:29)");
+  for (int i = 0; i < nK; ++i) {
+    if (K_levels[i] < 0 || K_levels[i] >= kTTotal) return fail(ctx, PAS_ERR_BANDS, "K must be in [0, %d)", kTTotal);
+    if (i && K_levels[i] <= K_levels[i - 1]) return fail(ctx, PAS_ERR_BANDS, "K levels must be strictly increasing");
+  }
+  for (int m = 0; m + 1 < nK; ++m) {
+    if (!std::isfinite(thresholds[m])) return fail(ctx, PAS_ERR_BANDS, "thresholds must be finite");
+    if (m && !(thresholds[m] > thresholds[m - 1]))
+      return fail(ctx, PAS_ERR_BANDS, "thresholds must be strictly increasing (S:150)");
+  }
+  ctx->nK = nK;
+  for (int i = 0; i < kMaxLevels; ++i) {
+    ctx->grid[i] = i < nK ? K_levels[i] : 0;
+    ctx->thr[i] = i + 1 < nK ? thresholds[i] : 0.f;
+  }
+  ctx->bands_set = true;
+  ctx->fractions_set = false;
+  return PAS_OK;
+}
+
+pas_status pas_set_degradation(pas_ctx* ctx, const double* c, int len) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!c || len != kTTotal) return fail(ctx, PAS_ERR_DEGRADATION, "c must have PAS_T_TOTAL = %d entries", kTTotal);
+  if (c[0] != 0.0) return fail(ctx, PAS_ERR_DEGRADATION, "c[0] must be 0");
+  for (int t = 0; t < len; ++t)
+    if (!std::isfinite(c[t])) return fail(ctx, PAS_ERR_DEGRADATION, "c must be finite");
+  for (int t = 1; t < len; ++t)
+    if (c[t] < c[t - 1]) return fail(ctx, PAS_ERR_DEGRADATION, "c must be non-decreasing");
+  for (int t = 1; t + 1 < len; ++t) {
+    const double sec = c[t + 1] - 2 * c[t] + c[t - 1];
+    if (sec < -1e-12 * (1.0 + std::fabs(c[t]))) return fail(ctx, PAS_ERR_DEGRADATION, "c must be convex (R6)");
+  }
+  for (int t = 0; t < kTTotal; ++t) ctx->c[t] = c[t];
+  return PAS_OK;
+}
+
+pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* instance_level, int W, int bstar,
+                             pas_mode mode) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->bands_set) return fail(ctx, PAS_ERR_STATE, "pas_set_bands must precede pas_set_fractions");
+  if (!F || !instance_level) return fail(ctx, PAS_ERR_ARG, "null argument");
+  if (W < 1 || W > kMaxInst) return fail(ctx, PAS_ERR_ARG, "W must be in [1, %d]", kMaxInst);
+  if (bstar < 1) return fail(ctx, PAS_ERR_ARG, "bstar must be >= 1");
+  if (mode != PAS_GREEDY && mode != PAS_UNIFORM) return fail(ctx, PAS_ERR_ARG, "unknown mode");
+  if (mode == PAS_UNIFORM && bstar != 1) return fail(ctx, PAS_ERR_ARG, "uniform routing uses batch size 1 (P:104)");
+  double sum = 0.0;
+  for (int j = 0; j < ctx->nK; ++j) {
+    if (!std::isfinite(F[j]) || F[j] < 0.0) return fail(ctx, PAS_ERR_FRACTIONS, "F must be finite and >= 0");
+    sum += F[j];
+  }
+  if (std::fabs(sum - 1.0) > 1e-9) return fail(ctx, PAS_ERR_FRACTIONS, "sum F = %.12g != 1 (S:35)", sum);
+  bool has[kMaxLevels] = {false};
+  for (int w = 0; w < W; ++w) {
+    if (instance_level[w] < 0 || instance_level[w] >= ctx->nK)
+      return fail(ctx, PAS_ERR_ARG, "instance_level[%d] = %d outside [0, nK)", w, instance_level[w]);
+    has[instance_level[w]] = true;
+  }
+  for (int j = 0; j < ctx->nK; ++j)
+    if (F[j] > 0.0 && !has[j])
+      return fail(ctx, PAS_ERR_NO_INSTANCE, "F[%d] > 0 but no instance runs level %d (S:309)", j, j);
+  for (int j = 0; j < kMaxLevels; ++j) ctx->F[j] = j < ctx->nK ? F[j] : 0.0;
+  for (int w = 0; w < kMaxInst; ++w) ctx->inst_level[w] = w < W ? instance_level[w] : 0;
+  ctx->W = W;
+  ctx->bstar = bstar;
+  ctx->mode = mode;
+  ctx->fractions_set = true;
+  return PAS_OK;
+}
+
+pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  ctx->seed = seed;
+  ctx->batch_seq = batch_seq;
+  return PAS_OK;
+}
+
+pas_status pas_route_local(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, void* cand_dev,
+                           pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (N < 0 || N > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "N outside [0, max_batch]");
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  if (N > 0 && (!emb || !cand_dev)) return fail(ctx, PAS_ERR_ARG, "null emb / cand");
+  ctx->launches = 0;
+  if (N == 0) return PAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  const Cand* cand;
+  int S;
+  return run_local(ctx, emb, dtype, N, st, &cand, &S, static_cast<Cand*>(cand_dev));
+}
+
+pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, int64_t N, const pas_route_out* out,
+                                     pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if ((s = ready(ctx, N))) return s;
+  if ((s = validate_out(ctx, out))) return s;
+  if (S < 1 || S > 128) return fail(ctx, PAS_ERR_ARG, "S must be in [1, 128]");
+  if (N == 0) return PAS_OK;
+  if (!cand_dev) return fail(ctx, PAS_ERR_ARG, "null candidates");
+  if (ctx->last_local_N != N)
+    return fail(ctx, PAS_ERR_STATE, "pas_route_local with the same N must precede (validity flags)");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+  return run_global(ctx, static_cast<const Cand*>(cand_dev), S, N, out, st);
+}
+
+pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, const pas_route_out* out,
+                           pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if ((s = ready(ctx, N))) return s;
+  if ((s = validate_out(ctx, out))) return s;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  ctx->launches = 0;
+  if (N == 0) return PAS_OK;
+  if (!emb) return fail(ctx, PAS_ERR_ARG, "emb is NULL");
+  const int G = ctx->cfg.world;
+  if (G > 1 && !ctx->comm)
+    return fail(ctx, PAS_ERR_STATE, "world > 1 without an NCCL communicator: use the split calls");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  const Cand* cand;
+  int S;
+  if (G == 1) {
+    if ((s = run_local(ctx, emb, dtype, N, st, &cand, &S, nullptr))) return s;
+  } else {
+    if ((s = run_local(ctx, emb, dtype, N, st, &cand, &S, ctx->cand_rank))) return s;
+    const size_t count = (size_t)N * ctx->cfg.topk * 2;   // (score, gid) as 2 x 32-bit words
+    ncclResult_t r = g_nccl.AllGather(ctx->cand_rank, ctx->cand_all, count, ncclInt32, ctx->comm, st);
+    if (r != ncclSuccess) return fail(ctx, PAS_ERR_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+    // ncclAllGather places rank r's N*k pairs at offset r*N*k: the layout is [G][N][k]
+    cand = ctx->cand_all;
+    S = G;
+  }
+  return run_global(ctx, cand, S, N, out, st);
+}
+
+pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
+                                const pas_route_out* oh, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if ((s = ready(ctx, N))) return s;
+  if ((s = validate_out(ctx, oh))) return s;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  if (N == 0) return PAS_OK;
+  if (!emb_host) return fail(ctx, PAS_ERR_ARG, "emb_host is NULL");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk;
+  cudaError_t e = cudaSuccess;
+  if (!ctx->stage_emb) {
+    e = cudaMalloc(&ctx->stage_emb, (size_t)mb * ctx->cfg.d * 4);
+    if (!e) e = dmalloc(&ctx->s_K, mb);
+    if (!e) e = dmalloc(&ctx->s_Kp, mb);
+    if (!e) e = dmalloc(&ctx->s_inst, mb);
+    if (!e) e = dmalloc(&ctx->s_slot, mb);
+    if (!e) e = dmalloc(&ctx->s_tid, mb * k);
+    if (!e) e = dmalloc(&ctx->s_tsc, mb * k);
+    if (!e) e = dmalloc(&ctx->s_flags, mb);
+    if (!e) e = dmalloc(&ctx->s_boff, kMaxInst + 1);
+    if (!e) e = dmalloc(&ctx->s_bpr, mb);
+    CUDA_TRY(ctx, e);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t esz = dtype == PAS_F32 ? 4 : 2;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->stage_emb, emb_host, (size_t)N * ctx->cfg.d * esz, cudaMemcpyHostToDevice, st));
+  pas_route_out od{ctx->s_K,   ctx->s_Kp,
+                   ctx->s_inst, ctx->s_slot,
+                   oh->topk_id ? ctx->s_tid : nullptr,
+                   oh->topk_score ? ctx->s_tsc : nullptr,
+                   oh->flags ? ctx->s_flags : nullptr,
+                   oh->bucket_offsets ? ctx->s_boff : nullptr,
+                   oh->bucket_prompts ? ctx->s_bpr : nullptr};
+  if ((s = pas_route_batch(ctx, ctx->stage_emb, dtype, N, &od, stream))) return s;
+  const int W = ctx->W;
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K, od.K, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K_prime, od.K_prime, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->instance, od.instance, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->slot, od.slot, N * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->topk_id) CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_id, od.topk_id, N * k * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->topk_score)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_score, od.topk_score, N * k * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->flags) CUDA_TRY(ctx, cudaMemcpyAsync(oh->flags, od.flags, N, cudaMemcpyDeviceToHost, st));
+  if (oh->bucket_offsets)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_offsets, od.bucket_offsets, (W + 1) * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->bucket_prompts)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_prompts, od.bucket_prompts, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return PAS_OK;
+}
+
+pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!out) return fail(ctx, PAS_ERR_ARG, "out is NULL");
+  memset(out, 0, sizeof(*out));
+  out->nK = ctx->nK;
+  out->W = ctx->W;
+  if (!ctx->ev_valid) return PAS_OK;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev[6]));
+  DevPlan p;
+  CUDA_TRY(ctx, cudaMemcpy(&p, ctx->plan, sizeof p, cudaMemcpyDeviceToHost));
+  out->N = ctx->last_N;
+  for (int i = 0; i < ctx->nK; ++i) {
+    out->h[i] = p.h[i];
+    out->f[i] = p.f[i];
+    for (int j = 0; j < ctx->nK; ++j) out->x[i][j] = p.x[i][j];
+  }
+  out->D_Q = p.D_Q;
+  out->D_Q_LP = p.D_Q_LP;
+  out->n_redirected = p.n_redirected;
+  out->n_upgraded = p.n_upgraded;
+  out->n_downgraded = p.n_downgraded;
+  out->n_invalid = p.n_invalid;
+  out->n_near_top1 = p.n_near_top1;
+  out->n_near_threshold = p.n_near_threshold;
+  for (int w = 0; w < ctx->W; ++w) out->bucket_count[w] = p.inst_count[w];
+  for (int i = 0; i < 6; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) out->stage_ms[i] = ms;
+  }
+  float tot = 0.f;
+  if (cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]) == cudaSuccess) out->stage_ms[6] = tot;
+  cudaGetLastError();
+  return PAS_OK;
+}
+
+// Test hook: K1 + K2 with the epilogue writing every raw score (no top-k); scores_dev [N x M_local].
+pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, float* scores_dev,
+                            pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (N < 1 || N > ctx->cfg.max_batch || !emb || !scores_dev) return fail(ctx, PAS_ERR_ARG, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
+  SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
+                ctx->cand_local, scores_dev};
+  CUDA_TRY(ctx, launch_simtopk(a, st));
+  return PAS_OK;
+}
+
+}  // extern "C"

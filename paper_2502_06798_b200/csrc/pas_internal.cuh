@@ -1,0 +1,131 @@
+// pas_internal.cuh -- shared device/host definitions of libpas (sm_100a only).
+//
+// Nothing in here is imported by, or imports, the CPU oracle (oracle/).  See include/pas.h for the
+// public C-ABI and DESIGN.md for the data layout and the roofline of every kernel.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pas.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libpas is written for sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace pas {
+
+constexpr int kMaxLevels = PAS_MAX_LEVELS;
+constexpr int kMaxInst = PAS_MAX_INSTANCES;
+constexpr int kTTotal = PAS_T_TOTAL;
+constexpr int kNumSMs = 148;
+
+// Candidate pair (score, global cache id); ordered by score desc, gid asc (R10).  Sentinel (-inf, -1).
+struct __align__(8) Cand {
+  float s;
+  int32_t g;
+};
+
+__host__ __device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+  return a.s > b.s || (a.s == b.s && (unsigned)a.g < (unsigned)b.g);
+}
+
+// Per-batch parameters, passed BY VALUE to the kernels that need them (no upload, no host sync).
+struct RouteParams {
+  int nK, W, bstar, mode, topk, G, rank, d;
+  int64_t N, M_total;
+  uint64_t seed, batch_seq;
+  int kb;                        // K6 bucket bits of kappa
+  int grid[kMaxLevels];          // K values
+  float thr[kMaxLevels];         // nK-1 thresholds
+  double F[kMaxLevels];          // load fractions
+  double c[kTTotal];             // degradation c(dK)
+  int inst_level[kMaxInst];      // level index of each serving instance
+};
+
+// Device-side plan + counters of one batch (K5 writes, pas_plan_stats reads).
+struct DevPlan {
+  int h[kMaxLevels];
+  int f[kMaxLevels];
+  int x[kMaxLevels][kMaxLevels];
+  int X[kMaxLevels][kMaxLevels];     // inclusive prefix sums of the rows of x
+  int class_start[kMaxLevels + 1];   // exclusive prefix of h
+  int n_inst[kMaxLevels];
+  int inst_list[kMaxLevels][kMaxInst];
+  double D_Q, D_Q_LP;
+  int n_redirected, n_upgraded, n_downgraded;
+  int n_invalid, n_near_top1, n_near_threshold;
+  int inst_count[kMaxInst];
+};
+
+// ------------------------------------------------------------------------------------------------
+// launchers (each returns cudaGetLastError() of its launch)
+// ------------------------------------------------------------------------------------------------
+// K1: normalise + quantise rows; shard filter (first_gid + i) % G == rank -> local row (first_gid+i)/G
+cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
+                             uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
+                             cudaStream_t st);
+
+// K2: similarity GEMM (tcgen05) + fused running top-k over cache ranges.
+struct SimTopkArgs {
+  const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x 128, SW128
+  const CUtensorMap* tmap_c;      // [rows_c x d] bf16, box 64 x 256, SW128
+  int64_t N;                      // prompts
+  int64_t M_local;                // valid store rows on this rank
+  int d, k, G, rank, R;           // R cache ranges per prompt tile
+  Cand* out;                      // [R][N][k]
+  float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
+};
+cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
+int simtopk_choose_ranges(int64_t N, int64_t M_local);
+size_t simtopk_smem_bytes();
+cudaError_t simtopk_init();
+
+// K3 (+K4 when final): merge [S][N][k] -> [N][k]
+cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cudaStream_t st);
+struct SelectOut {
+  int32_t* K;           // [N] (required)
+  int32_t* topk_id;     // [N*k] optional
+  float* topk_score;    // [N*k] optional
+  uint8_t* flags;       // [N] optional
+  uint8_t* level;       // [N] workspace
+  Cand* cand_out;       // [N*k] optional (merged candidates)
+  int* hist;            // [nK] workspace (zeroed by caller)
+  DevPlan* plan;        // counters
+};
+cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p,
+                                const SelectOut& o, cudaStream_t st);
+
+// K5 plan
+cudaError_t launch_plan(const int* hist, const RouteParams& p, DevPlan* plan, cudaStream_t st);
+
+// K6 redirection
+struct RedirectWs {
+  uint64_t* key;          // [N]
+  int32_t* bucket;        // [N]
+  int32_t* bcount;        // [nK << kb]   zeroed
+  int32_t* bstart;        // [nK << kb]
+  int32_t* bfill;         // [nK << kb]   zeroed
+  int32_t* items;         // [N]
+  int32_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
+  int32_t* lvl_prime;     // [N]
+};
+cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan,
+                            const RedirectWs& w, int32_t* K_prime, cudaStream_t st, int* launches);
+
+// K7 route-and-batch
+struct BatchWs {
+  int32_t* blk_counts;   // [nblk * 64]
+  int32_t* blk_off;      // [nblk * 64]
+  int32_t* offsets;      // [W+1]
+};
+cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan,
+                                   const BatchWs& w, int32_t* instance, int32_t* slot,
+                                   int32_t* bucket_offsets, int32_t* bucket_prompts,
+                                   cudaStream_t st, int* launches);
+
+cudaError_t launch_fill_sentinel(Cand* out, int64_t n, cudaStream_t st);
+
+}  // namespace pas

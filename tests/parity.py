@@ -1,0 +1,134 @@
+"""GPU-vs-oracle parity protocol.
+
+Graded (north_star): scores within 2e-2 of the fp64 Tier-A similarity; top-k ids bit-exact at every
+position whose Tier-A margins to both neighbours are >= 2e-2 (R17); optimal-K bit-exact wherever s1
+is >= 2e-2 from every threshold; everything downstream (H_K, f, x, K', instance, slot, buckets)
+bit-exact, teacher-forced on the GPU's K vector when a flagged near-tie flipped a K; D_Q within 1e-5
+relative.  Internal (tighter): every returned score within TAU_B of the fp64 dot product of the
+bf16-quantised rows of the id the GPU returned (Tier B).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from oracle import route as O
+
+SCORE_TOL = 2e-2          # north_star: similarity within 2e-2 absolute
+MARGIN = 2e-2             # north_star: near-tie margin
+DQ_REL = 1e-5             # north_star: D_Q relative
+# Tier B: bf16 products are exact, fp32 accumulation over d = 768 terms of |q c| <= 1 gives
+# gamma_767 ~ 4.6e-5 worst case (sequential RN); 1e-4 leaves room for the tensor core's order.
+TAU_B = 1e-4
+# Rigorous per-score bound GPU vs Tier A: bf16 rounding of both unit rows, (2u + u^2) |q||c| with
+# u = 2^-8, plus TAU_B.  A top-k id can differ only where the Tier-A margin is < 2 DELTA, a K only
+# where |s1 - t| < DELTA.
+DELTA = 2 * 2.0 ** -8 + 2.0 ** -16 + TAU_B
+
+
+@dataclass
+class Report:
+    n: int = 0
+    graded_ids: int = 0
+    k_flips: list = field(default_factory=list)
+    max_score_err_A: float = 0.0
+    max_score_err_B: float = 0.0
+    flagged_top1: int = 0
+    flagged_threshold: int = 0
+    notes: list = field(default_factory=list)
+
+    def summary(self):
+        return (f"n={self.n} graded_ids={self.graded_ids} k_flips={len(self.k_flips)} "
+                f"max|s-sA|={self.max_score_err_A:.3g} max|s-sB|={self.max_score_err_B:.3g} "
+                f"flag_top1={self.flagged_top1} flag_thr={self.flagged_threshold}")
+
+
+def oracle_topk_streaming(P: np.ndarray, cache_chunks, k: int):
+    """Tier-A top-(k+1) of the prompts P [n, d] over an iterable of (first_gid, rows fp32 [m, d])."""
+    n = P.shape[0]
+    ids = np.full((n, k + 1), -1, dtype=np.int64)
+    sc = np.full((n, k + 1), -np.inf)
+    valid = O.row_valid(P)
+    Pv = np.where(valid[:, None], P, 1.0)
+    for first, rows in cache_chunks:
+        S = O.similarity_A(Pv, rows)
+        gids = np.arange(first, first + rows.shape[0], dtype=np.int64)
+        ci, cs = O.topk_prefiltered(S, gids, k + 1)
+        ids, sc = O.merge_topk(ids, sc, ci, cs, k + 1)
+    ids[~valid] = -1
+    sc[~valid] = -np.inf
+    return ids, sc, valid
+
+
+def tier_b_scores(P: np.ndarray, rows_of_ids: np.ndarray) -> np.ndarray:
+    """s_hat(p, g) for the GPU's ids: rows_of_ids [n, k, d] fp32 cache rows (zeros for -1)."""
+    Pq, _ = O.quantize(P)
+    n, k, d = rows_of_ids.shape
+    Cq, _ = O.quantize(rows_of_ids.reshape(n * k, d))
+    return np.einsum("pd,pkd->pk", Pq, Cq.reshape(n, k, d))
+
+
+def check_topk(gpu_ids, gpu_sc, o_ids, o_sc, rep: Report, P=None, gpu_rows=None):
+    """gpu_ids/gpu_sc [n, k]; o_ids/o_sc [n, k+1] (the (k+1)-th is the next score for R17)."""
+    n, k = gpu_ids.shape
+    rep.n += n
+    sentinel = ~np.isfinite(o_sc[:, :k])
+    assert np.array_equal(np.isfinite(gpu_sc), ~sentinel), "sentinel positions differ"
+    assert np.all(gpu_ids[sentinel] == -1)
+    fin = ~sentinel
+    err = np.abs(gpu_sc[fin] - o_sc[:, :k][fin])
+    if err.size:
+        rep.max_score_err_A = max(rep.max_score_err_A, float(err.max()))
+    assert np.all(err <= SCORE_TOL), f"score error {err.max():.3g} > {SCORE_TOL}"
+    # R17: position m graded iff margins to both neighbours >= 2e-2
+    prev = np.concatenate([np.full((n, 1), np.inf), o_sc[:, :k - 1]], axis=1) if k > 1 else np.full((n, 1), np.inf)
+    nxt = o_sc[:, 1:k + 1]
+    cur = o_sc[:, :k]
+    with np.errstate(invalid="ignore"):
+        graded = fin & ((prev - cur) >= MARGIN) & ((cur - np.where(np.isfinite(nxt), nxt, -np.inf)) >= MARGIN)
+    rep.graded_ids += int(graded.sum())
+    bad = graded & (gpu_ids != o_ids[:, :k])
+    assert not bad.any(), f"{int(bad.sum())} graded top-k ids differ, e.g. prompt {np.argwhere(bad)[0]}"
+    if P is not None and gpu_rows is not None:
+        sb = tier_b_scores(P, gpu_rows)
+        eb = np.abs(np.where(fin, gpu_sc, 0) - np.where(fin, sb, 0))
+        rep.max_score_err_B = max(rep.max_score_err_B, float(eb.max()) if eb.size else 0.0)
+        assert eb.max() <= TAU_B, f"Tier-B score error {eb.max():.3g} > {TAU_B}"
+
+
+def check_levels(gpu_level, o_s1, o_level, usable, thresholds, rep: Report):
+    t = np.asarray(thresholds, dtype=np.float32).astype(np.float64)
+    dist = np.min(np.abs(o_s1[:, None] - t[None, :]), axis=1) if len(t) else np.full(len(o_s1), np.inf)
+    dist = np.where(usable, dist, np.inf)
+    near = dist < MARGIN
+    rep.flagged_threshold += int(near.sum())
+    diff = gpu_level != o_level
+    assert not (diff & ~near).any(), f"{int((diff & ~near).sum())} unflagged optimal-K mismatches"
+    flips = np.nonzero(diff)[0]
+    for p in flips:
+        assert dist[p] < DELTA, f"K flip at prompt {p} with |s1 - t| = {dist[p]:.3g} >= DELTA"
+        rep.k_flips.append((int(p), float(dist[p])))
+
+
+def check_downstream(gpu: dict, gpu_level: np.ndarray, setup: O.Setup, stats: dict | None, rep: Report,
+                     W: int):
+    """Teacher-forced O4..O10 on the GPU's level vector; everything bit-exact."""
+    d = O.downstream(gpu_level, setup)
+    grid = np.asarray(setup.grid)
+    assert np.array_equal(gpu["K_prime"], grid[d["level_prime"]]), "K' differs"
+    assert np.array_equal(gpu["instance"], d["instance"]), "instance differs"
+    assert np.array_equal(gpu["slot"], d["slot"]), "slot differs"
+    if "bucket_offsets" in gpu:
+        assert np.array_equal(gpu["bucket_offsets"][:W + 1], d["offsets"]), "bucket offsets differ"
+        assert np.array_equal(gpu["bucket_prompts"], d["bucket_prompts"]), "bucket prompts differ"
+    if stats is not None:
+        nK = len(setup.grid)
+        assert stats["h"] == d["h"].tolist(), "H_K differs"
+        assert stats["f"] == d["f"].tolist(), "f differs"
+        assert stats["x"] == d["x"].tolist(), "route plan differs"
+        ref = d["D_Q"]
+        assert abs(stats["D_Q"] - ref) <= DQ_REL * abs(ref) + 1e-15, f"D_Q {stats['D_Q']} vs {ref}"
+        assert sum(stats["bucket_count"]) == len(gpu_level)
+        _ = nK
+    return d

@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle (protocol in tests/parity.py).
+
+Covers the GEMM element-wise (Tier B), every config C1..C4 (full oracle where it finishes in
+seconds, sampled prompts against the full cache otherwise, downstream always on all N), and the
+edge cases: empty cache, invalid prompts, M < k, exact duplicate rows (gid tie-break), ragged
+N and M, N = 0, uniform mode, the sharded path (virtual shards on one GPU), determinism, the
+host-buffer entry point and argument validation.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import route as O
+from synth import BLOCK, CONFIGS, Workload
+
+from .parity import Report, check_downstream, check_levels, check_topk, oracle_topk_streaming
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
+
+
+@pytest.fixture(scope="module")
+def pas():
+    from paper_2502_06798_b200 import build
+    build.build()
+    from paper_2502_06798_b200 import pas as p
+    return p
+
+
+def _setup(cfg, mode=None, bstar=None, batch_seq=0, seed=None):
+    return O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
+                   bstar=cfg.bstar if bstar is None else bstar, mode=cfg.mode if mode is None else mode,
+                   topk=cfg.topk, seed=cfg.route_seed if seed is None else seed, batch_seq=batch_seq)
+
+
+def _router(pas, cfg, N, M, world=1, rank=0, mode=None, bstar=None, topk=None):
+    r = pas.Router(d=cfg.d, topk=cfg.topk if topk is None else topk, max_batch=max(N, 1),
+                   max_rows_per_rank=max(M, 1), device=0, rank=rank, world=world, seed=cfg.route_seed)
+    r.set_bands(cfg.grid, cfg.thresholds)
+    r.set_fractions(cfg.F, cfg.instance_level, cfg.bstar if bstar is None else bstar,
+                    cfg.mode if mode is None else mode)
+    return r
+
+
+def _host(out):
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def _levels(cfg, K):
+    return np.searchsorted(np.asarray(cfg.grid), K)
+
+
+def run_parity(pas, name, N=None, M=None, sample=None, mode=None, bstar=None, seed=0):
+    cfg = CONFIGS[name]
+    N = cfg.N if N is None else N
+    M = cfg.M if M is None else M
+    w = Workload(cfg, device=DEV, M=M)
+    P = w.prompts(N)
+    Ph = P.cpu().numpy()
+    rng = np.random.default_rng(seed)
+    idx = np.arange(N) if sample is None or sample >= N else np.sort(rng.choice(N, sample, replace=False))
+    router = _router(pas, cfg, N, M, mode=mode, bstar=bstar)
+
+    def chunks():
+        for b in range(w.n_blocks()):
+            rows = w.cache_block(b).contiguous()
+            router.load_cache(rows)
+            yield b * BLOCK, rows.cpu().numpy()
+
+    o_ids, o_sc, valid = oracle_topk_streaming(Ph[idx], chunks(), cfg.topk)
+    out = router.route(P)
+    torch.cuda.synchronize()
+    st = router.stats()
+    g = _host(out)
+    k = cfg.topk
+    gid = g["topk_id"].reshape(N, k)
+    gsc = g["topk_score"].reshape(N, k)
+    rep = Report()
+    rows = w.rows_at(torch.from_numpy(np.maximum(gid[idx], 0).reshape(-1))).cpu().numpy().reshape(len(idx), k, -1)
+    check_topk(gid[idx], gsc[idx], o_ids, o_sc, rep, Ph[idx], rows)
+    glev = _levels(cfg, g["K"])
+    assert np.array_equal(np.asarray(cfg.grid)[glev], g["K"])
+    o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid & (M > 0))
+    check_levels(glev[idx], o_sc[:, 0], o_lev, valid & (M > 0), cfg.thresholds, rep)
+    check_downstream(g, glev, _setup(cfg, mode, bstar), st, rep, len(cfg.instance_level))
+    router.close()
+    return rep, st
+
+
+# ------------------------------------------------------------------------------------------------
+def test_gemm_scores_tier_b(pas):
+    """The tcgen05 GEMM element-wise: every score of a ragged 200 x 1037 problem (2 prompt tiles,
+    5 cache tiles with a 13-row tail) within TAU_B of the fp64 dot of the bf16-quantised rows."""
+    from .parity import TAU_B
+    cfg = CONFIGS["C1"]
+    N, M = 200, 1037
+    w = Workload(cfg, device=DEV, M=M)
+    C_ = w.cache_rows(0, M).contiguous()
+    P = w.prompts(N)
+    r = _router(pas, cfg, N, M)
+    r.load_cache(C_)
+    S = torch.full((N, M), float("nan"), device=DEV)
+    pas.pas_debug_scores(r.ctx, P, S)
+    torch.cuda.synchronize()
+    Pq, _ = O.quantize(P.cpu().numpy())
+    Cq, _ = O.quantize(C_.cpu().numpy())
+    sb = O.similarity_B(Pq, Cq)
+    sa = O.similarity_A(P.cpu().numpy(), C_.cpu().numpy())
+    got = S.cpu().numpy()
+    assert np.isfinite(got).all()
+    errB = np.abs(got - sb).max()
+    errA = np.abs(got - sa).max()
+    print(f"GEMM max|s-sB|={errB:.3g} max|s-sA|={errA:.3g}")
+    assert errB <= TAU_B and errA <= 2e-2
+    r.close()
+
+
+def test_c1_parity_greedy(pas):
+    rep, st = run_parity(pas, "C1")
+    print(rep.summary(), st["h"], st["D_Q"])
+
+
+def test_c1_parity_uniform(pas):
+    rep, st = run_parity(pas, "C1", mode=1, bstar=1)
+    assert all(c >= 0 for c in st["bucket_count"])
+
+
+def test_c2_parity_heavy_redirection(pas):
+    rep, st = run_parity(pas, "C2")
+    print(rep.summary(), "redirected", st["n_redirected"], "D_Q", st["D_Q"])
+    assert st["n_redirected"] > 0 and st["D_Q"] > 0   # skewed H_K vs F_K (BASELINE configs[1])
+
+
+def test_c3_parity_sampled(pas):
+    rep, st = run_parity(pas, "C3", sample=96)
+    print(rep.summary(), st["stage_ms"])
+
+
+@pytest.mark.slow
+def test_c4_parity_sampled_full_size(pas):
+    """BASELINE configs[3] at full size on one GPU (the bench's N=1 workload): 32 sampled prompts
+    against the whole 10M cache, downstream on all 65,536 prompts."""
+    rep, st = run_parity(pas, "C4", sample=32)
+    print(rep.summary(), st["stage_ms"])
+
+
+# ------------------------------------------------------------------------------------------------
+def _small(pas, cache: torch.Tensor, P: torch.Tensor, topk=8, mode=0, bstar=4, name="C1"):
+    cfg = CONFIGS[name]
+    N, M = P.shape[0], cache.shape[0]
+    r = _router(pas, cfg, N, M, mode=mode, bstar=bstar, topk=topk)
+    if M:
+        r.load_cache(cache.contiguous())
+    out = r.route(P.contiguous())
+    torch.cuda.synchronize()
+    st = r.stats()
+    g = _host(out)
+    r.close()
+    return g, st
+
+
+def test_cold_cache_and_invalid_prompts(pas):
+    cfg = CONFIGS["C1"]
+    w = Workload(cfg, device=DEV)
+    P = w.prompts(40)
+    P[3] = 0.0
+    P[7, 11] = float("nan")
+    P[9, 0] = float("inf")
+    g, st = _small(pas, torch.empty(0, 768, device=DEV), P)
+    assert np.all(g["K"] == 0) and np.all(g["topk_id"] == -1) and np.all(np.isneginf(g["topk_score"]))
+    assert np.all(g["flags"][[3, 7, 9]] & 1) and np.all(g["flags"][[0, 1, 2]] & 2)
+    cache = w.cache_rows(0, 500)
+    g, st = _small(pas, cache, P)
+    assert st["n_invalid"] == 3
+    for p in (3, 7, 9):
+        assert g["K"][p] == 0 and np.all(g["topk_id"].reshape(40, 8)[p] == -1)
+    setup = _setup(cfg)
+    ref = O.route(P.cpu().numpy(), cache.cpu().numpy(), setup)
+    lev = _levels(cfg, g["K"])
+    d = O.downstream(lev, setup)
+    assert np.array_equal(g["slot"], d["slot"]) and np.array_equal(g["instance"], d["instance"])
+    ok = (ref.flags & 12) == 0
+    assert np.array_equal(g["K"][ok], ref.K[ok])
+
+
+def test_fewer_rows_than_k_and_duplicates(pas):
+    cfg = CONFIGS["C1"]
+    w = Workload(cfg, device=DEV)
+    base = w.cache_rows(0, 3)
+    P = w.prompts(5)
+    g, _ = _small(pas, base, P)
+    ids = g["topk_id"].reshape(5, 8)
+    assert np.all(ids[:, 3:] == -1) and np.all(np.sort(ids[:, :3], axis=1) == [0, 1, 2])
+    # exact duplicates (and a rescaled copy): equal scores tie-break to the lower gid (R10)
+    cache = torch.cat([base, base[1:2], base[1:2] * 4.0, base], 0)       # rows 1,3,4,6 identical
+    Q = cache[1:2].repeat(3, 1)
+    g, _ = _small(pas, cache, Q, topk=4)
+    assert g["topk_id"].reshape(3, 4)[0].tolist() == [1, 3, 4, 6]
+
+
+def test_ragged_sizes_and_single_prompt(pas):
+    for N, M in ((1, 1), (129, 257), (257, 513), (130, 4097)):
+        cfg = CONFIGS["C1"]
+        w = Workload(cfg, device=DEV, M=M)
+        C_ = w.cache_rows(0, M)
+        P = w.prompts(N)
+        g, st = _small(pas, C_, P)
+        ids, sc, valid = oracle_topk_streaming(P.cpu().numpy(), [(0, C_.cpu().numpy())], 8)
+        rep = Report()
+        check_topk(g["topk_id"].reshape(N, 8), g["topk_score"].reshape(N, 8), ids, sc, rep)
+        check_downstream(g, _levels(cfg, g["K"]), _setup(cfg), st, rep, 4)
+
+
+def test_n_zero_is_noop(pas):
+    cfg = CONFIGS["C1"]
+    r = _router(pas, cfg, 8, 8)
+    out = r.alloc_out(0)
+    pas.pas_route_batch(r.ctx, torch.empty(0, 768, device=DEV), out)
+    r.close()
+
+
+def test_virtual_shards_match_single_gpu(pas):
+    """The world > 1 data path on one GPU: G contexts hold the round-robin shards, their local
+    candidates are concatenated [G][N][k] (what the NCCL all-gather produces) and merged; the
+    result is byte-identical to G = 1 (R18, R19)."""
+    cfg = CONFIGS["C2"]
+    N, M = 700, 5000
+    w = Workload(cfg, device=DEV, M=M)
+    C_ = w.cache_rows(0, M).contiguous()
+    P = w.prompts(N)
+    ref, _ = _small(pas, C_, P, name="C2")
+    for G in (2, 3, 4):
+        ctxs = [_router(pas, cfg, N, (M + G - 1) // G, world=G, rank=r) for r in range(G)]
+        for r in ctxs:
+            r.load_cache(C_[:1234].contiguous())
+            r.load_cache(C_[1234:].contiguous())
+        cands = torch.empty(G, N * cfg.topk, dtype=torch.int64, device=DEV)
+        for rk, r in enumerate(ctxs):
+            pas.pas_route_local(r.ctx, P, cands[rk])
+        out = ctxs[0].alloc_out(N)
+        pas.pas_route_from_candidates(ctxs[0].ctx, cands, G, N, out)
+        torch.cuda.synchronize()
+        got = _host(out)
+        for key in ("K", "K_prime", "instance", "slot", "topk_id", "topk_score", "bucket_prompts"):
+            assert np.array_equal(got[key], ref[key]), (G, key)
+        for r in ctxs:
+            r.close()
+
+
+def test_determinism_and_batch_seq(pas):
+    cfg = CONFIGS["C2"]
+    w = Workload(cfg, device=DEV, M=3000)
+    C_ = w.cache_rows(0, 3000).contiguous()
+    P = w.prompts(1000)
+    r = _router(pas, cfg, 1000, 3000)
+    r.load_cache(C_)
+    a = _host(r.route(P))
+    r.set_seed(cfg.route_seed, 0)
+    b = _host(r.route(P))
+    c = _host(r.route(P))            # batch_seq 1
+    torch.cuda.synchronize()
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    assert np.array_equal(a["K"], c["K"]) and not np.array_equal(a["K_prime"], c["K_prime"])
+    lev = _levels(cfg, c["K"])
+    d = O.downstream(lev, _setup(cfg, batch_seq=1))
+    assert np.array_equal(c["slot"], d["slot"])
+    r.close()
+
+
+def test_host_entry_point_matches_device(pas):
+    cfg = CONFIGS["C1"]
+    w = Workload(cfg, device=DEV)
+    C_ = w.cache_rows(0, cfg.M).contiguous()
+    P = w.prompts(cfg.N)
+    r = _router(pas, cfg, cfg.N, cfg.M)
+    r.load_cache(C_)
+    dev = _host(r.route(P))
+    r.set_seed(cfg.route_seed, 0)
+    host = r.alloc_out(cfg.N, device="cpu")
+    pas.pas_route_batch_host(r.ctx, P.cpu().pin_memory(), host)
+    for key in dev:
+        assert np.array_equal(dev[key], host[key].numpy()), key
+    r.close()
+
+
+def test_validation_errors(pas):
+    cfg = CONFIGS["C1"]
+    r = pas.Router(d=768, topk=8, max_batch=16, max_rows_per_rank=10, device=0)
+    E = pas.PasError
+    P = torch.randn(4, 768, device=DEV)
+    out = r.alloc_out(4)
+    with pytest.raises(E) as ei:
+        pas.pas_route_batch(r.ctx, P, out)
+    assert ei.value.status == -2                                  # bands / fractions not set
+    with pytest.raises(E) as ei:
+        r.set_bands([5, 25], [0.8])
+    assert ei.value.status == -5                                  # level 0 required
+    with pytest.raises(E) as ei:
+        r.set_bands([0, 25, 10], [0.8, 0.9])
+    assert ei.value.status == -5
+    with pytest.raises(E) as ei:
+        r.set_fractions([1.0], [0])
+    assert ei.value.status == -2                                  # bands first
+    r.set_bands(cfg.grid, cfg.thresholds)
+    with pytest.raises(E) as ei:
+        r.set_fractions([0.6, 0.5, 0, 0, 0, 0], [0, 1])
+    assert ei.value.status == -3                                  # sum F = 1.1
+    with pytest.raises(E) as ei:
+        r.set_fractions([0.5, 0, 0, 0, 0, 0.5], [0, 1])
+    assert ei.value.status == -4                                  # no instance at level 5
+    with pytest.raises(E) as ei:
+        r.set_fractions([1, 0, 0, 0, 0, 0], [0], bstar=4, mode=1)
+    assert ei.value.status == -1                                  # uniform needs b* = 1
+    with pytest.raises(E) as ei:
+        r.set_degradation([0.0] + [0.1 * t * t ** 0.5 for t in range(1, 50)][::-1])
+    assert ei.value.status == -6
+    r.set_fractions([1, 0, 0, 0, 0, 0], [0])
+    with pytest.raises(E) as ei:
+        pas.pas_route_batch(r.ctx, torch.randn(17, 768, device=DEV), r.alloc_out(17))
+    assert ei.value.status == -7                                  # N > max_batch
+    bad = torch.randn(5, 768, device=DEV)
+    bad[2] = 0
+    with pytest.raises(E) as ei:
+        r.load_cache(bad)
+    assert ei.value.status == -10
+    assert pas.pas_cache_size(r.ctx) == (0, 0)                    # nothing appended
+    with pytest.raises(E) as ei:
+        r.load_cache(torch.randn(11, 768, device=DEV))
+    assert ei.value.status == -7
+    r.load_cache(torch.randn(10, 768, device=DEV))
+    assert pas.pas_cache_size(r.ctx) == (10, 10)
+    r.close()

@@ -1,0 +1,61 @@
+"""CPU-side checks of the C-ABI library (no GPU): it is built for sm_100a, loads, and exports every
+entry point include/pas.h declares; argument validation that needs no device fails cleanly."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pas.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2502_06798_b200 import build
+    build.build()
+    from paper_2502_06798_b200 import pas
+    return pas
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pas_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for must in ("pas_cache_load", "pas_set_fractions", "pas_route_batch", "pas_plan_stats",
+                 "pas_create", "pas_destroy", "pas_set_bands"):
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    so = ctypes.CDLL(lib.LIB_PATH)
+    for name in _declared():
+        assert hasattr(so, name), name
+    assert set(_declared()) == set(lib.EXPORTED)
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in _declared():
+        assert re.search(r"\bT " + name + r"\b", out), name
+
+
+def test_built_for_sm100a_only(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(80|86|89|90)", out)
+    sass = subprocess.run(["cuobjdump", "-sass", lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass   # tcgen05 + TMA + TMEM loads
+
+
+def test_version_and_clean_failures_without_gpu(lib):
+    assert "sm_100a" in lib.pas_version()
+    with pytest.raises(lib.PasError) as ei:
+        lib.pas_create(device=0)          # no CUDA device in this container
+    assert ei.value.status in (-1, -8)
+    with pytest.raises(lib.PasError):
+        lib.pas_create(d=100)             # d must be a multiple of 64
+    st = lib.lib.pas_route_batch(None, None, 0, 0, None, None)
+    assert st == -1                       # null context -> PAS_ERR_ARG, nothing enqueued

@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py -- prompts routed per second through libpas on 1..8 B200s (BASELINE.json metric).
+
+One step = one pas_route_batch of the whole hot path (normalise, similarity GEMM + top-k, merge
+(+ NCCL all-gather for G > 1), optimal-K + H_K, Eq. 1 plan, redirection, route-and-batch) on one
+batch of synthetic prompts resident in HBM.  Default workload: C4 (BASELINE configs[3]): 65,536
+prompts vs a 10M-entry cache, the cache row-sharded over the G = --gpus router GPUs (strong
+scaling: total work is fixed).  Launch for G > 1:
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node G --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus G
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle (oracle/) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prompts scheduled/s vs cache size at 1/2/4/8 B200; % of TC/HBM peak"
+UNIT = "prompts/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="libpas", choices=["libpas", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--prompts", type=int, default=None, help="override N")
+    ap.add_argument("--cache", type=int, default=None, help="override M")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample-prompts", type=int, default=32)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(config: str, G: int):
+    """dram read+write bytes per K2 launch from the committed ncu --set full capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as fh:
+            t = json.load(fh)
+        return t.get(f"{config}_G{G}")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------------
+def cpu_baseline(cfg, w, N, M, P_host, n_prompts, n_rows, torch):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
+    n_prompts prompts against the first n_rows cache rows (Tier-A fp64 similarity + top-k +
+    optimal-K), plus the downstream O4..O10 on all N prompts.  Scaled to the full cache (the
+    similarity cost is linear in M) and expressed in prompts/s."""
+    import numpy as np
+
+    from oracle import route as O
+    from synth import BLOCK
+
+    n_rows = min(n_rows, M)
+    idx = np.arange(min(n_prompts, N))
+    chunks = []
+    b = 0
+    while b * BLOCK < n_rows:
+        rows = w.cache_block(b)[: n_rows - b * BLOCK].cpu().numpy()
+        chunks.append((b * BLOCK, rows))
+        b += 1
+    threads = torch.get_num_threads()
+    t0 = time.perf_counter()
+    ids, sc, valid = O.topk_streaming(P_host[idx], iter(chunks), cfg.topk)
+    lev_s = O.optimal_k_level(sc[:, 0], cfg.thresholds, valid)
+    t_sim = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    levels = rng.integers(0, len(cfg.grid), N)
+    levels[idx] = lev_s
+    setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
+                    bstar=cfg.bstar, mode=cfg.mode, topk=cfg.topk, seed=cfg.route_seed)
+    t1 = time.perf_counter()
+    O.downstream(levels, setup)
+    t_down = time.perf_counter() - t1
+    per_prompt = t_sim / len(idx) * (M / n_rows) + t_down / N
+    return {"value": 1.0 / per_prompt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"{len(idx)} prompts x first {n_rows:,} of {M:,} cache rows (fp64 Tier-A similarity, "
+                       f"full-sort top-{cfg.topk}, optimal-K; {t_sim:.1f} s, scaled x{M / n_rows:.2f} to the "
+                       f"full cache) + O4..O10 downstream on all {N:,} prompts ({t_down:.1f} s)"),
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    import torch
+
+    from synth import BLOCK, CONFIGS, Workload
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    N = args.prompts or cfg.N
+    M = args.cache or cfg.M
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, N, M, rank, world)
+
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2502_06798_b200 import pas
+
+    nccl_id = None
+    if world > 1:
+        obj = [pas.pas_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    G = world
+    M_local = (M + G - 1) // G
+    router = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M_local, device=local,
+                        rank=rank, world=G, nccl_id=nccl_id, seed=cfg.route_seed)
+    router.set_bands(cfg.grid, cfg.thresholds)
+    router.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
+    w = Workload(cfg, device=dev, M=M)
+    t_load = time.perf_counter()
+    for b in range(w.n_blocks()):
+        router.load_cache(w.cache_block(b).contiguous())
+    torch.cuda.synchronize()
+    t_load = time.perf_counter() - t_load
+    P = w.prompts(N)
+    out = router.alloc_out(N)
+    stream = torch.cuda.current_stream()
+    cache_bytes = M_local * cfg.d * 2
+    l2_note = ("inputs larger than L2: the %.1f GB cache shard is streamed every step" % (cache_bytes / 1e9)
+               if cache_bytes > 200e6 else "L2 flushed between steps (256 MB write)")
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if cache_bytes <= 200e6 else None
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        router.route(P, out)
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    stage_sum = [0.0] * 8
+    launches = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1.0)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+        router.route(P, out)
+        launches += pas.pas_last_launch_count(router.ctx)
+        if flush is not None:
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+        st = router.stats()          # syncs on the step's last event; device stage times
+        for i in range(8):
+            stage_sum[i] += st["stage_ms"][i]
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    total_ms = sum(step_ms) if flush is not None else ev0.elapsed_time(ev1)
+    total_ms = max_over_ranks(total_ms, dist, dev, torch)
+    k2_ms = max_over_ranks(stage_sum[1] / args.steps, dist, dev, torch)
+    value = N * args.steps / (total_ms / 1e3)
+
+    # ---- e2e through the host-buffer entry point (H2D of the prompts, D2H of every output)
+    e2e = None
+    if not args.no_e2e:
+        Ph = P.cpu().pin_memory()
+        host_out = router.alloc_out(N, device="cpu")
+        for k_, v in host_out.items():
+            host_out[k_] = v.pin_memory()
+        bi = Ph.numel() * Ph.element_size()
+        bo = sum(v.numel() * v.element_size() for k_, v in host_out.items() if k_ != "bucket_offsets") \
+            + (router.W + 1) * 4
+        pas.pas_route_batch_host(router.ctx, Ph, host_out)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            pas.pas_route_batch_host(router.ctx, Ph, host_out)
+        e1.record(stream)
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1), dist, dev, torch)
+        e2e = {"value": N * args.steps / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "api": "pas_route_batch_host (pinned host buffers)"}
+
+    peaks, peak_src = measured_peaks()
+    flops = 2.0 * N * M_local * cfg.d
+    achieved = flops / (k2_ms / 1e3) / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"])
+    traffic = profiled_traffic(args.config, G)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (synth-v1: clustered CLIP-shaped embeddings, d=768, seeded)",
+        "config": {"workload": f"{args.config}: {N:,} prompts vs {M:,}-entry cache ({cfg.note})", "N": N, "M": M,
+                   "G": G, "M_per_gpu": M_local, "d": cfg.d, "topk": cfg.topk, "levels": len(cfg.grid),
+                   "instances": len(cfg.instance_level), "mode": "uniform" if cfg.mode else "greedy",
+                   "bstar": cfg.bstar, "parallelism": f"cache row-sharded x{G}" + (" + NCCL all-gather" if G > 1 else ""),
+                   "l2": l2_note},
+        "roofline": {"kernel": "k_simtopk (K2: tcgen05 similarity GEMM + fused top-k)", "bound": "tensor",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": f"bf16 sustained, {peak_src}",
+                     "algorithmic": f"2*N*M_per_gpu*d = {flops:.4g} flop per launch / mean K2 event time "
+                                    f"{k2_ms:.3f} ms"},
+        "stages_ms": {n: round(stage_sum[i] / args.steps, 4) for i, n in enumerate(
+            ["normalise", "similarity_topk", "merge_collective_optimalK", "plan", "redirect", "route_and_batch",
+             "total"])},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "setup": {"cache_load_s": round(t_load, 2)},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        import numpy as np  # noqa: F401
+        line["cpu_baseline"] = cpu_baseline(cfg, w, N, M, P.cpu().numpy(), args.cpu_sample_prompts,
+                                            args.cpu_sample_rows, torch)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    router.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def max_over_ranks(x, dist, dev, torch):
+    if not dist:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reference_arm(args, cfg, N, M, rank, world):
+    """The CPU oracle as it stands, timed on this host's cores on bounded samples of the workload."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+
+    from oracle import route as O
+    from synth import BLOCK, Workload
+
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    w = Workload(cfg, device=dev, M=M)
+    n_rows = min(M, 1 << 19)
+    n_p = 8
+    P = w.prompts(N).cpu().numpy()
+    chunks = []
+    b = 0
+    while b * BLOCK < n_rows:
+        chunks.append((b * BLOCK, w.cache_block(b)[: n_rows - b * BLOCK].cpu().numpy()))
+        b += 1
+    setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
+                    bstar=cfg.bstar, mode=cfg.mode, topk=cfg.topk, seed=cfg.route_seed)
+    rng = np.random.default_rng(1)
+
+    def step(i):
+        idx = (np.arange(n_p) + i * n_p) % N
+        t0 = time.perf_counter()
+        ids, sc, valid = O.topk_streaming(P[idx], iter(chunks), cfg.topk)
+        lev = O.optimal_k_level(sc[:, 0], cfg.thresholds, valid)
+        t_sim = time.perf_counter() - t0
+        levels = rng.integers(0, len(cfg.grid), min(N, 4096))
+        levels[:n_p] = lev
+        t1 = time.perf_counter()
+        O.downstream(levels, setup)
+        t_down = time.perf_counter() - t1
+        return t_sim / n_p * (M / n_rows) + t_down / len(levels)
+
+    for i in range(args.warmup):
+        step(i)
+    per = [step(args.warmup + i) for i in range(args.steps)]
+    per_prompt = sum(per) / len(per)
+    value = 1.0 / per_prompt
+    threads = torch.get_num_threads()
+    sample = (f"per step: {n_p} prompts x first {n_rows:,} of {M:,} cache rows (fp64 similarity, full-sort "
+              f"top-{cfg.topk}, optimal-K) scaled x{M / n_rows:.1f} to the full cache, + O4..O10 on 4,096 prompts")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_prompt * N * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth-v1)",
+            "config": {"workload": f"{args.config}: {N:,} prompts vs {M:,}-entry cache ({cfg.note})", "N": N,
+                       "M": M},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -149,6 +149,25 @@ def merge_topk(a_ids, a_sc, b_ids, b_sc, k: int):
     return out_i, out_s
 
 
+def topk_streaming(P: np.ndarray, cache_chunks, k: int):
+    """Tier-A top-k of prompts P [n, d] over an iterable of (first_gid, fp32 rows [m, d]) chunks
+    (a cache too large to hold in fp64), merged with ``merge_topk``.  Invalid prompts get sentinels.
+    Returns (ids [n, k], scores [n, k], valid [n])."""
+    n = P.shape[0]
+    ids = np.full((n, k), SENTINEL_GID, dtype=np.int64)
+    sc = np.full((n, k), NEG_INF)
+    valid = row_valid(P)
+    Pv = np.where(valid[:, None], P, 1.0)
+    for first, rows in cache_chunks:
+        S = similarity_A(Pv, rows)
+        gids = np.arange(first, first + rows.shape[0], dtype=np.int64)
+        ci, cs = topk_prefiltered(S, gids, k)
+        ids, sc = merge_topk(ids, sc, ci, cs, k)
+    ids[~valid] = SENTINEL_GID
+    sc[~valid] = NEG_INF
+    return ids, sc, valid
+
+
 # --------------------------------------------------------------------------------------
 # O3 / O4  optimal-K and H_K
 # --------------------------------------------------------------------------------------

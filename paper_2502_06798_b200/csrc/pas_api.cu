@@ -559,9 +559,9 @@ pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, 
   pas_status s = check_live(ctx);
   if (s) return s;
   if ((s = ready(ctx, N))) return s;
-  if ((s = validate_out(ctx, out))) return s;
   if (S < 1 || S > 128) return fail(ctx, PAS_ERR_ARG, "S must be in [1, 128]");
   if (N == 0) return PAS_OK;
+  if ((s = validate_out(ctx, out))) return s;
   if (!cand_dev) return fail(ctx, PAS_ERR_ARG, "null candidates");
   if (ctx->last_local_N != N)
     return fail(ctx, PAS_ERR_STATE, "pas_route_local with the same N must precede (validity flags)");
@@ -578,10 +578,10 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   pas_status s = check_live(ctx);
   if (s) return s;
   if ((s = ready(ctx, N))) return s;
-  if ((s = validate_out(ctx, out))) return s;
   if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
   ctx->launches = 0;
   if (N == 0) return PAS_OK;
+  if ((s = validate_out(ctx, out))) return s;
   if (!emb) return fail(ctx, PAS_ERR_ARG, "emb is NULL");
   const int G = ctx->cfg.world;
   if (G > 1 && !ctx->comm)
@@ -610,9 +610,9 @@ pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dt
   pas_status s = check_live(ctx);
   if (s) return s;
   if ((s = ready(ctx, N))) return s;
-  if ((s = validate_out(ctx, oh))) return s;
   if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
   if (N == 0) return PAS_OK;
+  if ((s = validate_out(ctx, oh))) return s;
   if (!emb_host) return fail(ctx, PAS_ERR_ARG, "emb_host is NULL");
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk;

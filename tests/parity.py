@@ -19,8 +19,9 @@ SCORE_TOL = 2e-2          # north_star: similarity within 2e-2 absolute
 MARGIN = 2e-2             # north_star: near-tie margin
 DQ_REL = 1e-5             # north_star: D_Q relative
 # Tier B: bf16 products are exact, fp32 accumulation over d = 768 terms of |q c| <= 1 gives
-# gamma_767 ~ 4.6e-5 worst case (sequential RN); 1e-4 leaves room for the tensor core's order.
-TAU_B = 1e-4
+# gamma_767 ~ 4.6e-5 worst case (sequential RN); the first B200 run measured 1.7e-6 max over
+# C1..C3 (200 x 1037 element-wise and sampled top-k), so TAU_B = 2e-5 (>10x observed).
+TAU_B = 2e-5
 # Rigorous per-score bound GPU vs Tier A: bf16 rounding of both unit rows, (2u + u^2) |q||c| with
 # u = 2^-8, plus TAU_B.  A top-k id can differ only where the Tier-A margin is < 2 DELTA, a K only
 # where |s1 - t| < DELTA.
@@ -45,20 +46,8 @@ class Report:
 
 
 def oracle_topk_streaming(P: np.ndarray, cache_chunks, k: int):
-    """Tier-A top-(k+1) of the prompts P [n, d] over an iterable of (first_gid, rows fp32 [m, d])."""
-    n = P.shape[0]
-    ids = np.full((n, k + 1), -1, dtype=np.int64)
-    sc = np.full((n, k + 1), -np.inf)
-    valid = O.row_valid(P)
-    Pv = np.where(valid[:, None], P, 1.0)
-    for first, rows in cache_chunks:
-        S = O.similarity_A(Pv, rows)
-        gids = np.arange(first, first + rows.shape[0], dtype=np.int64)
-        ci, cs = O.topk_prefiltered(S, gids, k + 1)
-        ids, sc = O.merge_topk(ids, sc, ci, cs, k + 1)
-    ids[~valid] = -1
-    sc[~valid] = -np.inf
-    return ids, sc, valid
+    """Tier-A top-(k+1) (the (k+1)-th score is the next neighbour for R17)."""
+    return O.topk_streaming(P, cache_chunks, k + 1)
 
 
 def tier_b_scores(P: np.ndarray, rows_of_ids: np.ndarray) -> np.ndarray:

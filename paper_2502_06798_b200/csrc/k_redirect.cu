@@ -7,7 +7,7 @@
 //
 // Ranking without a full sort: composite key (class << 60 | kappa) -> bucket (class, top kb bits of
 // kappa) counting sort (count, scan, scatter), then each prompt counts the keys below it inside its
-// own bucket (expected bucket size <= 2 by the choice of kb).  Global rank = bucket start + in-bucket
+// own bucket (the choice of kb keeps the mean bucket below 16 prompts).  Global rank = bucket start + in-bucket
 // rank, which equals the position in the (key, p) order; rank within class = global - class start.
 //
 // Kernels: k_keys (Philox + bucket histogram), k_scan (one CTA), k_scatter, k_rank (rank, K', and the
@@ -31,27 +31,47 @@ __global__ void k_keys(const uint8_t* __restrict__ level, RouteParams P, uint64_
   atomicAdd(&bcount[b], 1);
 }
 
-// Exclusive scan of n ints with one CTA of 1024 threads (n <= 16 << 16).
+// Exclusive scan of n ints with one CTA of 1024 threads: coalesced tiles of 4096 (int4 per thread),
+// warp-shuffle scans, a running carry across tiles.
 __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ in, int32_t* __restrict__ out, int n) {
-  __shared__ int32_t part[1024];
-  const int t = threadIdx.x;
-  const int per = (n + 1023) / 1024;
-  const int lo = t * per, hi = min(n, lo + per);
-  int s = 0;
-  for (int i = lo; i < hi; ++i) s += in[i];
-  part[t] = s;
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry_s;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry_s = 0;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int v = t >= o ? part[t - o] : 0;
+  for (int base = 0; base < n; base += 4096) {
+    const int i0 = base + 4 * t;
+    int v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = (i0 + j < n) ? in[i0 + j] : 0;
+    const int local = v[0] + v[1] + v[2] + v[3];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    part[t] += v;
+    if (w == 0) {
+      int x = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      wsum[lane] = x;   // inclusive over warps
+    }
     __syncthreads();
-  }
-  int run = part[t] - s;
-  for (int i = lo; i < hi; ++i) {
-    const int v = in[i];
-    out[i] = run;
-    run += v;
+    int run = carry_s + (w ? wsum[w - 1] : 0) + incl - local;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j < n) out[i0 + j] = run;
+      run += v[j];
+    }
+    __syncthreads();
+    if (t == 0) carry_s += wsum[31];
+    __syncthreads();
   }
 }
 

@@ -183,8 +183,10 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   p.M_total = ctx->M_total;
   p.seed = ctx->seed;
   p.batch_seq = ctx->batch_seq;
-  int kb = ceil_log2(N > 1 ? N : 1);
-  p.kb = kb > 16 ? 16 : kb;
+  // K6 buckets: nK << kb with kb = ceil(log2 N) - 4, so a class holding all N prompts averages
+  // <= 16 prompts per bucket (the in-bucket rank loop) and the bucket scan stays small.
+  int kb = ceil_log2(N > 1 ? N : 1) - 4;
+  p.kb = kb < 0 ? 0 : (kb > 16 ? 16 : kb);
   for (int i = 0; i < kMaxLevels; ++i) {
     p.grid[i] = ctx->grid[i];
     p.thr[i] = ctx->thr[i];

@@ -281,8 +281,12 @@ def test_host_entry_point_matches_device(pas):
     r.set_seed(cfg.route_seed, 0)
     host = r.alloc_out(cfg.N, device="cpu")
     pas.pas_route_batch_host(r.ctx, P.cpu().pin_memory(), host)
+    W = len(cfg.instance_level)
     for key in dev:
-        assert np.array_equal(dev[key], host[key].numpy()), key
+        a, b = dev[key], host[key].numpy()
+        if key == "bucket_offsets":      # only [0, W] is written
+            a, b = a[:W + 1], b[:W + 1]
+        assert np.array_equal(a, b), key
     r.close()
 
 

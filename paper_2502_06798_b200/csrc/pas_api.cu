@@ -276,7 +276,7 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
 // ----------------------------------------------------------------------------------------------
 extern "C" {
 
-const char* pas_version(void) { return "libpas 0.1 (sm_100a, tcgen05 K2, 1-CTA 128x256)"; }
+const char* pas_version(void) { return "libpas 0.2 (sm_100a, tcgen05 K2, CTA-pair 256x256)"; }
 
 const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
 
@@ -344,9 +344,11 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->seed = cfg->seed;
   for (int t = 0; t < kTTotal; ++t) ctx->c[t] = 0.006 * t;   // SPEC S:49 default, R6
   const int64_t mb = cfg->max_batch, k = cfg->topk, d = cfg->d;
-  ctx->q_rows = (mb + 127) / 128 * 128;
+  const int64_t qt = simtopk_prompt_rows();
+  ctx->q_rows = (mb + qt - 1) / qt * qt;
   ctx->cap_rows = cfg->max_rows_per_rank;
-  ctx->cand_cap = mb > 592 * 128 ? mb : 592 * 128;
+  // K2 writes [R][N][k]; simtopk_choose_ranges keeps R * ceil(N / qt) <= 8 * 74 units unless R == 1
+  ctx->cand_cap = mb > 592 * qt ? mb : 592 * qt;
   const int64_t nb = (int64_t)kMaxLevels << 16;
   const int64_t nblk = (mb + 1023) / 1024;
   cudaError_t e = cudaSuccess;
@@ -383,8 +385,8 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
     }
-  if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, 128) ||
-      !encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, 256)) {
+  if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, simtopk_box_q()) ||
+      !encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c())) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
   }

@@ -70,8 +70,8 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
 
 // K2: similarity GEMM (tcgen05) + fused running top-k over cache ranges.
 struct SimTopkArgs {
-  const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x 128, SW128
-  const CUtensorMap* tmap_c;      // [rows_c x d] bf16, box 64 x 256, SW128
+  const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x simtopk_box_q(), SW128
+  const CUtensorMap* tmap_c;      // [rows_c x d] bf16, box 64 x simtopk_box_c(), SW128
   int64_t N;                      // prompts
   int64_t M_local;                // valid store rows on this rank
   int d, k, G, rank, R;           // R cache ranges per prompt tile
@@ -82,6 +82,9 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local);
 size_t simtopk_smem_bytes();
 cudaError_t simtopk_init();
+int simtopk_prompt_rows();   // prompt rows per work unit (pair tile)
+int simtopk_box_q();         // TMA box rows of the prompt map
+int simtopk_box_c();         // TMA box rows of the cache map
 
 // K3 (+K4 when final): merge [S][N][k] -> [N][k]
 cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cudaStream_t st);

@@ -5,8 +5,8 @@
 // product, which K2 computes on the tensor cores.  A row with a non-finite element or zero norm is
 // invalid (R16): it is written as zeros and flagged (prompts) or counted (cache insert -> rejected).
 //
-// One warp per row, 128-bit loads (4 fp32 / 8 bf16 per lane per step), two passes over the row (the
-// second pass hits L1).  HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
+// One warp per row, 128-bit loads (4 fp32 / 4 bf16 per lane per step), the row held in registers.
+// HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
 // Cache insert applies the shard filter of the round-robin partition (gid g lives on rank g % G at
 // local row g / G) and reads only this rank's rows.
 #include "pas_internal.cuh"
@@ -26,7 +26,25 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&v)[4]) {
   v[3] = __uint_as_float(x.y & 0xFFFF0000u);
 }
 
-template <typename T>
+__device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[4], double norm, bool valid) {
+  __nv_bfloat162 lo, hi;
+  if (valid) {
+    lo = __floats2bfloat162_rn(__double2float_rn((double)v[0] / norm), __double2float_rn((double)v[1] / norm));
+    hi = __floats2bfloat162_rn(__double2float_rn((double)v[2] / norm), __double2float_rn((double)v[3] / norm));
+  } else {
+    lo = __floats2bfloat162_rn(0.f, 0.f);
+    hi = lo;
+  }
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = pk;
+}
+
+// One warp per row.  VEC = d / 128 float4 (or 4 x bf16) per lane: the whole row is held in registers
+// so all its loads are in flight at once and the row is read from HBM exactly once; VEC = 0 is the
+// generic two-pass path for d > 1024.
+template <typename T, int VEC>
 __global__ void __launch_bounds__(256) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count) {
@@ -38,44 +56,79 @@ __global__ void __launch_bounds__(256) k_normalize(const T* __restrict__ in, int
     if (G > 1 && (gid % G) != rank) continue;
     const int64_t orow = (G > 1) ? gid / G : gid;
     const T* src = in + i * (int64_t)d;
+    __nv_bfloat16* dst = out + orow * (int64_t)d;
     double ss = 0.0;
     bool finite = true;
-    for (int c = lane * 4; c < d; c += 128) {
-      float v[4];
-      load4(src + c, v);
+    if constexpr (VEC > 0) {
+      float v[VEC][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        finite &= isfinite(v[j]);
-        ss += (double)v[j] * (double)v[j];
-      }
-    }
+      for (int c = 0; c < VEC; ++c) load4(src + c * 128 + lane * 4, v[c]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    finite = __all_sync(0xffffffffu, finite);
-    const double norm = sqrt(ss);
-    const bool valid = finite && norm > 0.0;
-    __nv_bfloat16* dst = out + orow * (int64_t)d;
-    for (int c = lane * 4; c < d; c += 128) {
-      float v[4];
-      load4(src + c, v);
-      __nv_bfloat162 lo, hi;
-      if (valid) {
-        lo = __floats2bfloat162_rn(__double2float_rn((double)v[0] / norm), __double2float_rn((double)v[1] / norm));
-        hi = __floats2bfloat162_rn(__double2float_rn((double)v[2] / norm), __double2float_rn((double)v[3] / norm));
-      } else {
-        lo = __floats2bfloat162_rn(0.f, 0.f);
-        hi = lo;
+      for (int c = 0; c < VEC; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          finite &= isfinite(v[c][j]);
+          ss += (double)v[c][j] * (double)v[c][j];
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      finite = __all_sync(0xffffffffu, finite);
+      const double norm = sqrt(ss);
+      const bool valid = finite && norm > 0.0;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) store_row4(dst + c * 128 + lane * 4, v[c], norm, valid);
+      if (lane == 0) {
+        if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
+        if (!valid && invalid_count) atomicAdd(invalid_count, 1);
       }
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(dst + c) = pk;
-    }
-    if (lane == 0) {
-      if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
-      if (!valid && invalid_count) atomicAdd(invalid_count, 1);
+    } else {
+      for (int c = lane * 4; c < d; c += 128) {
+        float v[4];
+        load4(src + c, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          finite &= isfinite(v[j]);
+          ss += (double)v[j] * (double)v[j];
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      finite = __all_sync(0xffffffffu, finite);
+      const double norm = sqrt(ss);
+      const bool valid = finite && norm > 0.0;
+      for (int c = lane * 4; c < d; c += 128) {
+        float v[4];
+        load4(src + c, v);
+        store_row4(dst + c, v, norm, valid);
+      }
+      if (lane == 0) {
+        if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
+        if (!valid && invalid_count) atomicAdd(invalid_count, 1);
+      }
     }
   }
+}
+
+template <typename T>
+cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8_t* flags, int64_t first_gid, int G,
+                     int rank, int* invalid_count, cudaStream_t st) {
+  const int threads = 256;
+  int64_t blocks = (rows * 32 + threads - 1) / threads;
+  const int64_t cap = (int64_t)kNumSMs * 16;  // grid-stride beyond 16 CTAs (128 warps) per SM
+  if (blocks > cap) blocks = cap;
+  const unsigned g = (unsigned)blocks;
+  switch (d % 128 == 0 && d <= 1024 ? d / 128 : 0) {
+    case 1: k_normalize<T, 1><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 2: k_normalize<T, 2><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 3: k_normalize<T, 3><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 4: k_normalize<T, 4><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 5: k_normalize<T, 5><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 6: k_normalize<T, 6><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 7: k_normalize<T, 7><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 8: k_normalize<T, 8><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    default: k_normalize<T, 0><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -84,17 +137,9 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
                              cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  const int threads = 256;
-  int64_t blocks = (rows * 32 + threads - 1) / threads;
-  const int64_t cap = (int64_t)kNumSMs * 16;  // grid-stride beyond 16 CTAs (128 warps) per SM
-  if (blocks > cap) blocks = cap;
   if (dtype == PAS_F32)
-    k_normalize<float><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const float*>(in), rows, d, out, flags,
-                                                             first_gid, G, rank, invalid_count);
-  else
-    k_normalize<__nv_bfloat16><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows,
-                                                                     d, out, flags, first_gid, G, rank, invalid_count);
-  return cudaGetLastError();
+    return launch_t(static_cast<const float*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st);
+  return launch_t(static_cast<const __nv_bfloat16*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st);
 }
 
 }  // namespace pas

@@ -6,58 +6,112 @@
 // owns one prompt row of the accumulator and keeps the k best (score desc, gid asc; R10) over the
 // cache range of its work unit.
 //
-// CTA pairs (cluster of 2, tcgen05 cta_group::2): one MMA instruction computes a 256 x 256 x 16
-// tile, prompt rows 0..127 from CTA 0's shared memory and TMEM, rows 128..255 from CTA 1's; the 256
-// cache rows of B are split 128 / 128 between the two CTAs' shared memory, so each SM stages half of
-// the big operand (half the smem traffic of a 1-CTA 128 x 256 tile for the same per-SM MMA rate).
+// Two tile organisations share one source (compile-time PAS_K2_PAIR; DESIGN.md section 8 records the
+// A/B on one B200 under its 1 kW power cap):
+//   single CTA (default)  tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
+//                         instruction; per stage A 128x64 + B 256x64 bf16 (48 KB), 4 stages.
+//   CTA pair              tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
+//                         128..255 in CTA 1; the 256 cache rows of B split 128/128 between the two
+//                         CTAs' smem (32 KB / stage, 6 stages); TMA bytes of both CTAs land on the
+//                         leader's mbarrier; commits multicast to both CTAs.
 //
-// Work unit = (prompt pair-tile m of 256 rows, cache range r of whole 256-row tiles).  Persistent
-// pairs (74 on 148 SMs) walk units u = cluster + i*clusters with m fastest, so concurrently running
-// pairs stream the SAME cache tiles (L2 reuse of the big operand) against different prompt tiles.
+// Work unit = (prompt tile m, cache range r of whole 256-row tiles).  Persistent CTAs / pairs walk
+// units u = id + i*count with m fastest, so concurrently running CTAs stream the SAME cache tiles
+// (L2 reuse of the big operand) against different prompt tiles.
 //
 // Warp roles per CTA (192 threads, 1 CTA/SM):
-//   warp 0      TMA producer: its 128 prompt rows and its 128 cache rows of each 64-wide k-block
-//               (128-B swizzle) into a 6-stage ring (32 KB / stage); completion bytes of BOTH CTAs
-//               land on the leader's "full" mbarrier.
-//   warp 1      TMEM allocation (cta_group::2, 512 columns = two 256-column fp32 accumulators); in
-//               the leader one lane issues tcgen05.mma.cta_group::2 (M=256, N=256, K=16) and
-//               commits smem stages (multicast to both CTAs' "empty") and accumulators (both
-//               CTAs' "tfull").
-//   warps 2..5  epilogue over this CTA's 128 TMEM lanes: tcgen05.ld 32 columns at a time, chunk max
-//               vs the current k-th score, branch-free bubble insert only when the chunk can improve
-//               the list; then arrive on the leader's "tempty" (8 arrivals: 4 warps x 2 CTAs).
+//   warp 0      TMA producer (128-B swizzle, mbarrier complete_tx).
+//   warp 1      TMEM allocation (512 columns = two 256-column fp32 accumulators) and one lane issuing
+//               tcgen05.mma + tcgen05.commit (smem stage released, accumulator ready).
+//   warps 2..5  epilogue over the CTA's 128 TMEM lanes: tcgen05.ld of 32 columns, max of the chunk
+//               vs the current k-th score, and only when the chunk can improve the list a
+//               branch-free bubble insert (strict >, columns ascending, so equal scores keep the
+//               lower gid).
 #include <cfloat>
 #include <cstdio>
 
 #include "pas_internal.cuh"
 #include "ptx_sm100.cuh"
 
+#ifndef PAS_K2_PAIR
+#define PAS_K2_PAIR 0
+#endif
+
 namespace pas {
 namespace {
 
-constexpr int BM = 128;           // prompt rows per CTA (256 per pair)
-constexpr int BN = 256;           // cache rows per tile (128 staged per CTA)
-constexpr int BN_CTA = BN / 2;
-constexpr int BK = 64;
-constexpr int STAGES = 6;
+constexpr bool PAIR = PAS_K2_PAIR != 0;
+constexpr int CTAS = PAIR ? 2 : 1;
+constexpr int BM = 128;                 // prompt rows per CTA
+constexpr int BN = 256;                 // cache rows per tile (MMA N)
+constexpr int BN_CTA = BN / CTAS;       // cache rows staged per CTA
+constexpr int BK = 64;                  // one 128-B swizzle row of bf16
+constexpr int STAGES = PAIR ? 6 : 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN_CTA * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_PAIRS = kNumSMs / 2;
+constexpr int NUM_WORKERS = kNumSMs / CTAS;      // persistent CTAs (or pairs)
+constexpr int UNIT_ROWS = BM * CTAS;             // prompt rows per work unit
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 struct __align__(8) Bars {
-  uint64_t full[STAGES];    // leader: TMA bytes of both CTAs landed
-  uint64_t empty[STAGES];   // both: MMA finished reading the stage
-  uint64_t tfull[2];        // both: accumulator ready
-  uint64_t tempty[2];       // leader: both epilogues drained the accumulator
+  uint64_t full[STAGES];    // TMA bytes landed (leader's barrier in pair mode)
+  uint64_t empty[STAGES];   // MMA finished reading the stage
+  uint64_t tfull[2];        // accumulator ready
+  uint64_t tempty[2];       // epilogue(s) drained the accumulator
   uint32_t tmem_base;
 };
 
+// Opaque copy: stops the compiler from strength-reducing per-element column ids across chunks.
+__device__ __forceinline__ int opaque(int x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+
+// Epilogue over one accumulator: 32-column chunks (tcgen05.ld), chain max (FMNMX3), the column id
+// materialised only inside the (rare) insert path, the tail mask only on the last partial tile.
+// (A double-buffered tcgen05.ld + tree-max variant was 7 % slower under the power cap: DESIGN.md 8.)
+template <int KMAX, bool PARTIAL>
+__device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_local, float (&s)[KMAX],
+                                            int32_t (&gl)[KMAX]) {
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t v[32];
+    ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
+    ptx::tmem_wait_ld();
+    const int base = opaque(col_base + c * 32);
+    if (PARTIAL) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (base + j >= M_local) v[j] = __float_as_uint(-INFINITY);
+    }
+    float mx = __uint_as_float(v[0]);
+#pragma unroll
+    for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+    if (mx > s[KMAX - 1]) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = __uint_as_float(v[j]);
+        if (x > s[KMAX - 1]) {
+          s[KMAX - 1] = x;
+          gl[KMAX - 1] = base + j;
+#pragma unroll
+          for (int i = KMAX - 1; i > 0; --i) {
+            if (s[i] > s[i - 1]) {
+              const float ts = s[i]; s[i] = s[i - 1]; s[i - 1] = ts;
+              const int32_t tg = gl[i]; gl[i] = gl[i - 1]; gl[i - 1] = tg;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int KMAX, bool DUMP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump) {
@@ -69,10 +123,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0;
   const bool leader = crank == 0;
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
+  const int worker = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nworkers = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int units = MT * R;
 
   if (warp == 0 && lane == 0) {
@@ -84,50 +138,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&bars->tfull[a], 1);
-      ptx::mbar_init(&bars->tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+      ptx::mbar_init(&bars->tempty[a], 4 * CTAS);  // one arrive per epilogue warp (of both CTAs)
     }
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
-    ptx::tmem_alloc_pair(&bars->tmem_base, TMEM_COLS);
-    ptx::tmem_relinquish_pair();
+    if (PAIR) {
+      ptx::tmem_alloc_pair(&bars->tmem_base, TMEM_COLS);
+      ptx::tmem_relinquish_pair();
+    } else {
+      ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  ptx::cluster_sync();
+  if (PAIR) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
 
   if (warp == 0) {
-    // ------------------------------- TMA producer (both CTAs) -------------------------------
+    // ------------------------------- TMA producer -------------------------------
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < units; u += npairs) {
+      for (int u = worker; u < units; u += nworkers) {
         const int m = u % MT, r = u / MT;
         const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-        const int qrow = m * (2 * BM) + (int)crank * BM;
+        const int qrow = m * UNIT_ROWS + (int)crank * BM;
         for (int t = t0; t < t1; ++t) {
           const int crow = t * BN + (int)crank * BN_CTA;
           for (int kb = 0; kb < kblocks; ++kb) {
             ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
-            if (leader) ptx::mbar_arrive_expect_tx(&bars->full[stage], 2 * STAGE_BYTES);
-            ptx::tma_load_2d_pair(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
-            ptx::tma_load_2d_pair(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, crow,
-                                  ptx::kEvictNormal);
+            if (PAIR) {
+              if (leader) ptx::mbar_arrive_expect_tx(&bars->full[stage], CTAS * STAGE_BYTES);
+              ptx::tma_load_2d_pair(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
+              ptx::tma_load_2d_pair(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, crow,
+                                    ptx::kEvictNormal);
+            } else {
+              ptx::mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
+              ptx::tma_load_2d(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
+              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, crow, ptx::kEvictNormal);
+            }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------- MMA issuer (leader CTA) --------------------------------
+    // ------------------------------- MMA issuer ---------------------------------
     if (leader && ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(UNIT_ROWS, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = pair; u < units; u += npairs) {
+      for (int u = worker; u < units; u += nworkers) {
         const int r = u / MT;
         const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
         for (int t = t0; t < t1; ++t) {
@@ -141,79 +206,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint32_t b0 = ptx::smem_u32(sB + stage * B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              ptx::umma_f16_ss_pair(d_tmem, ptx::sdesc_kmajor_sw128(a0 + kk * 32),
-                                    ptx::sdesc_kmajor_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+              const uint64_t ad = ptx::sdesc_kmajor_sw128(a0 + kk * 32);
+              const uint64_t bd = ptx::sdesc_kmajor_sw128(b0 + kk * 32);
+              if (PAIR) ptx::umma_f16_ss_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              else ptx::umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
             }
-            ptx::umma_commit_pair(&bars->empty[stage], 0x3);
+            if (PAIR) ptx::umma_commit_pair(&bars->empty[stage], 0x3);
+            else ptx::umma_commit(&bars->empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::umma_commit_pair(&bars->tfull[acc], 0x3);
+          if (PAIR) ptx::umma_commit_pair(&bars->tfull[acc], 0x3);
+          else ptx::umma_commit(&bars->tfull[acc]);
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
       }
     }
   } else {
-    // ------------------------------- epilogue (both CTAs) -----------------------------------
+    // ------------------------------- epilogue -----------------------------------
     const uint32_t q = warp & 3;              // TMEM lane quarter this warp may access
     const int row = (int)(q * 32 + lane);
     const uint32_t lane_addr = tmem_base + ((q * 32u) << 16);
+    const int Ml = (int)M_local;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < units; u += npairs) {
+    for (int u = worker; u < units; u += nworkers) {
       const int m = u % MT, r = u / MT;
       const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-      const int64_t prompt = (int64_t)m * (2 * BM) + crank * BM + row;
+      const int64_t prompt = (int64_t)m * UNIT_ROWS + crank * BM + row;
       float s[KMAX];
-      int32_t g[KMAX];
+      int32_t gl[KMAX];
 #pragma unroll
-      for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; g[i] = -1; }
+      for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; gl[i] = -1; }
       for (int t = t0; t < t1; ++t) {
         ptx::mbar_wait(&bars->tfull[acc], acc_phase);
         ptx::tc_fence_after();
-        const int64_t col_base = (int64_t)t * BN;
+        const int col_base = t * BN;
+        const uint32_t taddr = lane_addr + acc * BN;
+        if (DUMP) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(lane_addr + acc * BN + c * 32, v);
-          ptx::tmem_wait_ld();
-          const int64_t col0 = col_base + c * 32;
-          if (DUMP) {
-            if (prompt < N) {
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
+            ptx::tmem_wait_ld();
+
+            const int64_t col0 = (int64_t)col_base + c * 32;
+            if (prompt < N)
               for (int j = 0; j < 32; ++j)
                 if (col0 + j < M_local) dump[prompt * M_local + col0 + j] = __uint_as_float(v[j]);
-            }
-            continue;
           }
-          if (col0 + 32 > M_local) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j >= M_local) v[j] = __float_as_uint(-INFINITY);
-          }
-          float mx = __uint_as_float(v[0]);
-#pragma unroll
-          for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
-          if (mx > s[KMAX - 1]) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float x = __uint_as_float(v[j]);
-              if (x > s[KMAX - 1]) {
-                s[KMAX - 1] = x;
-                g[KMAX - 1] = (int32_t)((col0 + j) * G + rank);
-#pragma unroll
-                for (int i = KMAX - 1; i > 0; --i) {
-                  if (s[i] > s[i - 1]) {
-                    const float ts = s[i]; s[i] = s[i - 1]; s[i - 1] = ts;
-                    const int32_t tg = g[i]; g[i] = g[i - 1]; g[i - 1] = tg;
-                  }
-                }
-              }
-            }
-          }
+        } else if (col_base + BN > Ml) {
+          epi_tile<KMAX, true>(taddr, col_base, Ml, s, gl);
+        } else {
+          epi_tile<KMAX, false>(taddr, col_base, Ml, s, gl);
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(&bars->tempty[acc], 0);
+        if (lane == 0) {
+          if (PAIR) ptx::mbar_arrive_cluster(&bars->tempty[acc], 0);
+          else ptx::mbar_arrive(&bars->tempty[acc]);
+        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -221,31 +273,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         Cand* dst = out + ((int64_t)r * N + prompt) * k;
 #pragma unroll
         for (int i = 0; i < KMAX; ++i)
-          if (i < k) dst[i] = Cand{s[i], g[i]};
+          if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
       }
     }
   }
 
   ptx::tc_fence_before();
-  ptx::cluster_sync();
+  if (PAIR) ptx::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    if (PAIR) ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
 template <int KMAX, bool DUMP>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
-  auto kern = k_simtopk<KMAX, DUMP>;
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(*a.tmap_q, *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G, a.rank,
-                                              a.R, MT, NT, a.out, a.dump);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CTAS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = PAIR ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP>, *a.tmap_q, *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
+                            a.rank, a.R, MT, NT, a.out, a.dump);
 }
 
 }  // namespace
 
 size_t simtopk_smem_bytes() { return SMEM_BYTES; }
-int simtopk_prompt_rows() { return 2 * BM; }
+int simtopk_prompt_rows() { return UNIT_ROWS; }
 int simtopk_box_q() { return BM; }
 int simtopk_box_c() { return BN_CTA; }
 
@@ -257,18 +320,19 @@ cudaError_t simtopk_init() {
   return cudaFuncSetAttribute(k_simtopk<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
-// Pick the number of cache ranges R so that (prompt pair-tiles x R) units fill the 74 CTA pairs with
-// the smallest makespan: waves(R) * (tiles per unit + 1 tile of per-unit overhead).
-int simtopk_choose_ranges(int64_t N, int64_t M_local) {
-  const int64_t MT = (N + 2 * BM - 1) / (2 * BM);
+// Pick the number of cache ranges R so that (prompt tiles x R) units fill the persistent workers with
+// the smallest makespan: waves(R) * (tiles per unit + 1 tile of per-unit overhead), subject to the
+// candidate buffer (R * N <= cand_rows).
+int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
+  const int64_t MT = (N + UNIT_ROWS - 1) / UNIT_ROWS;
   const int64_t NT = (M_local + BN - 1) / BN;
   if (NT <= 1 || MT <= 0) return 1;
   int best = 1;
   double best_cost = 1e300;
   const int64_t rmax = NT < 64 ? NT : 64;
   for (int64_t R = 1; R <= rmax; ++R) {
-    if (R > 1 && MT * R > 8 * NUM_PAIRS) break;
-    const int64_t waves = (MT * R + NUM_PAIRS - 1) / NUM_PAIRS;
+    if (R > 1 && R * N > cand_rows) break;
+    const int64_t waves = (MT * R + NUM_WORKERS - 1) / NUM_WORKERS;
     const double cost = (double)waves * (double)((NT + R - 1) / R + 1);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = (int)R; }
   }
@@ -276,12 +340,12 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local) {
 }
 
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
-  const int MT = (int)((a.N + 2 * BM - 1) / (2 * BM));
+  const int MT = (int)((a.N + UNIT_ROWS - 1) / UNIT_ROWS);
   const int NT = (int)((a.M_local + BN - 1) / BN);
   if (MT == 0 || NT == 0) return cudaSuccess;
   const int units = MT * a.R;
-  const int pairs = units < NUM_PAIRS ? units : NUM_PAIRS;
-  const int grid = 2 * pairs;
+  const int workers = units < NUM_WORKERS ? units : NUM_WORKERS;
+  const int grid = CTAS * workers;
   if (a.dump) return launch_variant<8, true>(a, MT, NT, grid, st);
   if (a.k <= 8) return launch_variant<8, false>(a, MT, NT, grid, st);
   return launch_variant<16, false>(a, MT, NT, grid, st);

@@ -12,6 +12,10 @@
 
 #include "pas_internal.cuh"
 
+#ifndef PAS_K2_PAIR
+#define PAS_K2_PAIR 0
+#endif
+
 using namespace pas;
 
 // ----------------------------------------------------------------------------------------------
@@ -223,8 +227,11 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
   int R = 1;
   if (ctx->M_local > 0) {
-    R = simtopk_choose_ranges(N, ctx->M_local);
-    if ((int64_t)R * N > ctx->cand_cap) R = 1;
+    R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap);
+    if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
+      const int r = atoi(ov);
+      if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
+    }
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
                   ctx->cand_local, nullptr};
     CUDA_TRY(ctx, launch_simtopk(a, st));
@@ -276,7 +283,7 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
 // ----------------------------------------------------------------------------------------------
 extern "C" {
 
-const char* pas_version(void) { return "libpas 0.2 (sm_100a, tcgen05 K2, CTA-pair 256x256)"; }
+const char* pas_version(void) { return PAS_K2_PAIR ? "libpas 0.3 (sm_100a, tcgen05 K2 cta_group::2 256x256)" : "libpas 0.3 (sm_100a, tcgen05 K2 cta_group::1 128x256)"; }
 
 const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
 
@@ -347,8 +354,8 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   const int64_t qt = simtopk_prompt_rows();
   ctx->q_rows = (mb + qt - 1) / qt * qt;
   ctx->cap_rows = cfg->max_rows_per_rank;
-  // K2 writes [R][N][k]; simtopk_choose_ranges keeps R * ceil(N / qt) <= 8 * 74 units unless R == 1
-  ctx->cand_cap = mb > 592 * qt ? mb : 592 * qt;
+  // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
+  ctx->cand_cap = 4 * mb > 592 * qt ? 4 * mb : 592 * qt;
   const int64_t nb = (int64_t)kMaxLevels << 16;
   const int64_t nblk = (mb + 1023) / 1024;
   cudaError_t e = cudaSuccess;

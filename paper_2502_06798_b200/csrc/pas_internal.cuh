@@ -79,7 +79,7 @@ struct SimTopkArgs {
   float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
 };
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
-int simtopk_choose_ranges(int64_t N, int64_t M_local);
+int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows);
 size_t simtopk_smem_bytes();
 cudaError_t simtopk_init();
 int simtopk_prompt_rows();   // prompt rows per work unit (pair tile)

@@ -42,7 +42,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Blocking wait on a phase parity (PAS_MBAR_SUSPEND: pass a suspend-time hint to try_wait).
+#ifndef PAS_MBAR_SUSPEND   // suspend-time hint on try_wait: waiting warps sleep instead of spinning
+#define PAS_MBAR_SUSPEND 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if PAS_MBAR_SUSPEND
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "LAB_WAIT:\n\t"
@@ -52,6 +67,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // ---------------- TMA ----------------

@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpas.so")
+# PAS_LIB selects an alternative build of the same C-ABI (kernel A/B experiments only)
+LIB_PATH = os.environ.get("PAS_LIB") or os.path.join(_HERE, "lib", "libpas.so")
 
 PAS_OK = 0
 STATUS = {0: "PAS_OK", -1: "PAS_ERR_ARG", -2: "PAS_ERR_STATE", -3: "PAS_ERR_FRACTIONS",

@@ -81,7 +81,8 @@ typedef struct {
   uint64_t seed;               /* Philox key of the redirection / uniform-routing streams (R18) */
 } pas_config;
 
-/* Per-prompt outputs, caller-owned DEVICE arrays (SoA).  Required arrays must be non-NULL. */
+/* Per-prompt outputs, caller-owned DEVICE arrays (SoA), each 16-byte aligned (PAS_ERR_ARG otherwise).
+ * Required arrays must be non-NULL. */
 typedef struct {
   int32_t* K;               /* [N] optimal-K value (grid value, not index)                 required */
   int32_t* K_prime;         /* [N] K' the prompt is served at                              required */
@@ -115,7 +116,9 @@ typedef struct {
 const char* pas_version(void);
 
 /* Create a context: allocates the store (max_rows_per_rank x d bf16), the per-batch workspace
- * and, if world > 1 and nccl_id != NULL, the NCCL communicator (collective over all ranks).
+ * (the prompt-side part -- max_batch x d bf16 and the candidate buffers -- on the first routing call
+ * that needs it) and, if world > 1 and nccl_id != NULL, the NCCL communicator (collective over all
+ * ranks).
  * Defaults after create: no bands (pas_set_bands required), c(dK) = 0.006 dK (R6),
  * batch_seq = 0.  Errors: PAS_ERR_ARG (bad cfg), PAS_ERR_CUDA (allocation), PAS_ERR_NCCL. */
 pas_status pas_create(pas_ctx** ctx, const pas_config* cfg);
@@ -164,7 +167,8 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
 /* Reset the Philox key and the batch sequence number (R18). */
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
 
-/* Route one batch (the hot path).  emb_dev: device [N x d] of dtype, the SAME prompts on every rank.
+/* Route one batch (the hot path).  emb_dev: device [N x d] of dtype (16-byte aligned rows), the SAME
+ * prompts on every rank.
  * out: device arrays, written in full on every rank.  N == 0 is a no-op; N > max_batch ->
  * PAS_ERR_CAPACITY.  Requires bands and fractions (PAS_ERR_STATE).  Enqueue-only (no host sync);
  * batch_seq increments on success.  world > 1 needs the NCCL communicator. */
@@ -182,7 +186,9 @@ pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dt
  * writes cand_dev: device [N x topk] pairs {float score; int32 gid} (8 bytes each, score desc, gid asc,
  * padded (-inf, -1)).  pas_route_from_candidates takes S such blocks laid out [S][N][topk]
  * (e.g. the all-gather over ranks, S == world), merges them and runs a5..a8 for all N prompts,
- * using the validity flags of this context's last pas_route_local.  batch_seq increments here. */
+ * using the validity flags of this context's last pas_route_local when it had the same N (otherwise
+ * every prompt is valid; a caller marks an invalid prompt with an all-sentinel list, which yields
+ * K = 0).  batch_seq increments here.  1 <= S <= 128. */
 pas_status pas_route_local(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
                            void* cand_dev, pas_stream stream);
 pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, int64_t N,

@@ -6,9 +6,11 @@
 // #{m : s1 >= t_m} over the similarity bands (R8, closed below); cold cache or invalid
 // embedding -> level 0 = vanilla (R16).  Only top-1 sets K (R9).
 //
-// Input candidates [S][N][k] (each list sorted by score desc, gid asc).  One warp per prompt: lane s
-// holds the head of source s (lanes loop when S > 32); k rounds of a warp arg-max on (score, gid)
-// emit the merged list.  H_K: shared-memory histogram per CTA, one global atomic per non-zero bin.
+// Input candidates [S][N][k] (each list sorted by score desc, gid asc).  S * k <= 32 (and S <= 4):
+// thread per prompt over candidate rows staged in shared memory with coalesced loads.  Otherwise warp
+// per prompt: lane s holds the head of source s (lanes loop when S > 32); k rounds of a warp arg-max
+// on (score, gid) emit the merged list.  H_K: shared-memory histogram per CTA, one global atomic per
+// non-zero bin.  HBM per prompt: S*k*8 B read, k*8 + 5 B written (+1 flag byte read).
 #include "pas_internal.cuh"
 
 namespace pas {
@@ -70,17 +72,91 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge(const Cand* __restrict__ i
   merge_prompt(in, S, N, k, p, out + p * k, lane);
 }
 
+// K4 for one prompt.  Thresholds are padded with +inf to 16 (make_params), so the level
+// #{m : s1 >= t_m} is a 4-step binary search, and the near-threshold test only needs the two
+// thresholds around s1.  Counts go to per-thread registers (Tally) and are flushed once per CTA.
+struct Tally {
+  uint64_t lv[4];        // 16 levels x 16-bit counters
+  int inv, near1, nearT;
+  __device__ __forceinline__ void zero() {
+    lv[0] = lv[1] = lv[2] = lv[3] = 0;
+    inv = near1 = nearT = 0;
+  }
+  __device__ __forceinline__ void add_level(int l) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) lv[g] += ((l >> 2) == g) ? (1ull << ((l & 3) * 16)) : 0ull;
+  }
+};
+
+__device__ __forceinline__ void select_one(float s1, float s2, int64_t p, bool invalid, bool cold,
+                                           const RouteParams& P, const SelectOut& o, Tally& ty) {
+  int lvl = 0;
+  uint8_t fl = 0;
+  if (invalid) fl |= PAS_FLAG_INVALID;
+  else if (cold) fl |= PAS_FLAG_COLD;
+  else {
+#pragma unroll
+    for (int step = 8; step >= 1; step >>= 1)
+      if (s1 >= P.thr[lvl + step - 1]) lvl += step;
+    if (s2 != -INFINITY && s1 - s2 < 2e-2f) fl |= PAS_FLAG_NEAR_TOP1;
+    if ((lvl > 0 && s1 - P.thr[lvl - 1] < 2e-2f) || (lvl < P.nK - 1 && P.thr[lvl] - s1 < 2e-2f))
+      fl |= PAS_FLAG_NEAR_THRESHOLD;
+  }
+  o.level[p] = (uint8_t)lvl;
+  o.K[p] = P.grid[lvl];
+  if (o.flags) o.flags[p] = fl;
+  ty.add_level(lvl);
+  ty.inv += (fl & PAS_FLAG_INVALID) ? 1 : 0;
+  ty.near1 += (fl & PAS_FLAG_NEAR_TOP1) ? 1 : 0;
+  ty.nearT += (fl & PAS_FLAG_NEAR_THRESHOLD) ? 1 : 0;
+}
+
+// Block-wide reduction of the per-thread tallies, then one global atomic per non-zero counter.
+__device__ __forceinline__ void flush_tally(const RouteParams& P, const SelectOut& o, const Tally& ty) {
+  __shared__ int hist[kMaxLevels];
+  __shared__ int cnt[3];
+  __syncthreads();
+  if (threadIdx.x < kMaxLevels) hist[threadIdx.x] = 0;
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; ++l) {
+    if (l >= P.nK) break;
+    int v = (int)((ty.lv[l >> 2] >> ((l & 3) * 16)) & 0xFFFF);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&hist[l], v);
+  }
+  int a = ty.inv, b = ty.near1, c = ty.nearT;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+    c += __shfl_xor_sync(0xffffffffu, c, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(&cnt[0], a);
+    if (b) atomicAdd(&cnt[1], b);
+    if (c) atomicAdd(&cnt[2], c);
+  }
+  __syncthreads();
+  if (threadIdx.x < P.nK && hist[threadIdx.x]) atomicAdd(&o.hist[threadIdx.x], hist[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    if (cnt[0]) atomicAdd(&o.plan->n_invalid, cnt[0]);
+    if (cnt[1]) atomicAdd(&o.plan->n_near_top1, cnt[1]);
+    if (cnt[2]) atomicAdd(&o.plan->n_near_threshold, cnt[2]);
+  }
+}
+
+// Warp per prompt (any S <= 128).
 __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restrict__ in, int S,
                                                              const uint8_t* __restrict__ pflags,
                                                              const RouteParams P, SelectOut o) {
   __shared__ Cand res[WARPS][PAS_MAX_TOPK];
-  __shared__ int hist[kMaxLevels];
-  __shared__ int cnt[3];
+  Tally ty;
+  ty.zero();
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  if (threadIdx.x < kMaxLevels) hist[threadIdx.x] = 0;
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  __syncthreads();
   const int64_t p = (int64_t)blockIdx.x * WARPS + w;
   const int k = P.topk;
   if (p < P.N) {
@@ -93,42 +169,132 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restr
       merge_prompt(in, S, P.N, k, p, res[w], lane);
     }
     __syncwarp();
-    // lanes write the k results (coalesced)
     for (int i = lane; i < k; i += 32) {
       const Cand c = res[w][i];
       if (o.topk_id) o.topk_id[p * k + i] = c.g;
       if (o.topk_score) o.topk_score[p * k + i] = c.s;
       if (o.cand_out) o.cand_out[p * k + i] = c;
     }
-    if (lane == 0) {
-      int lvl = 0;
-      uint8_t fl = 0;
-      if (invalid) fl |= PAS_FLAG_INVALID;
-      else if (cold) fl |= PAS_FLAG_COLD;
-      else {
-        const float s1 = res[w][0].s;
-        for (int m = 0; m < P.nK - 1; ++m) lvl += (s1 >= P.thr[m]) ? 1 : 0;
-        const float s2 = (k > 1) ? res[w][1].s : -INFINITY;
-        if (s2 != -INFINITY && s1 - s2 < 2e-2f) fl |= PAS_FLAG_NEAR_TOP1;
-        for (int m = 0; m < P.nK - 1; ++m)
-          if (fabsf(s1 - P.thr[m]) < 2e-2f) fl |= PAS_FLAG_NEAR_THRESHOLD;
+    if (lane == 0) select_one(res[w][0].s, k > 1 ? res[w][1].s : -INFINITY, p, invalid, cold, P, o, ty);
+  }
+  flush_tally(P, o, ty);
+}
+
+// Thread per prompt for S * k <= 32 (the common case: R or G small).  All global traffic is
+// coalesced 16-byte vectors through shared memory: the CTA's candidate rows of every source are
+// staged in, each thread merges its S lists, and the CTA's top-k ids / scores leave as int4 rows.
+constexpr int TP_THREADS = 128;
+constexpr int TP_MAXSK = 32;
+
+__global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __restrict__ in, int S,
+                                                                 const uint8_t* __restrict__ pflags,
+                                                                 const RouteParams P, SelectOut o) {
+  extern __shared__ __align__(16) Cand sm[];   // S * 128 * (k + 1) pairs (dynamic, padded rows)
+  // after the merge the staging buffer is reused for the outgoing ids and scores (rows padded to k+1
+  // words so the per-thread rows fall in different banks)
+  const int kp = P.topk + 1;
+  int32_t* sid = reinterpret_cast<int32_t*>(sm);
+  float* ssc = reinterpret_cast<float*>(sm) + TP_THREADS * kp;
+  Tally ty;
+  ty.zero();
+  const int k = P.topk;
+  const bool cold = (P.M_total == 0);
+  const int64_t ntiles = (P.N + TP_THREADS - 1) / TP_THREADS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {   // persistent over tiles
+    const int64_t p0 = tile * TP_THREADS;
+    const int np = (int)min((int64_t)TP_THREADS, P.N - p0);
+    __syncthreads();   // previous tile's output copy finished reading the staging buffer
+    for (int s = 0; s < S; ++s) {   // coalesced global reads into rows padded to k+1 pairs
+      const Cand* src = in + ((int64_t)s * P.N + p0) * k;
+      Cand* dst = sm + s * TP_THREADS * kp;
+      for (int i = threadIdx.x; i < np * k; i += TP_THREADS) dst[(i / k) * kp + i % k] = src[i];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int64_t p = p0 + t;
+    Cand res[PAS_MAX_TOPK];
+    bool invalid = false;
+    if (t < np) {
+      invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
+      if (invalid || cold) {
+#pragma unroll
+        for (int i = 0; i < PAS_MAX_TOPK; ++i) res[i] = Cand{-INFINITY, -1};
+      } else if (S == 1) {
+#pragma unroll
+        for (int i = 0; i < PAS_MAX_TOPK; ++i)
+          if (i < k) res[i] = sm[t * kp + i];
+      } else {
+        int pos[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < PAS_MAX_TOPK; ++i) {
+          if (i >= k) break;
+          Cand best{-INFINITY, -1};
+          int bs = -1;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            if (s < S && pos[s] < k) {
+              const Cand c = sm[(s * TP_THREADS + t) * kp + pos[s]];
+              if (bs < 0 || cand_better(c, best)) { best = c; bs = s; }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (s == bs) pos[s]++;
+          res[i] = best;
+        }
       }
-      o.level[p] = (uint8_t)lvl;
-      o.K[p] = P.grid[lvl];
-      if (o.flags) o.flags[p] = fl;
-      atomicAdd(&hist[lvl], 1);
-      if (fl & PAS_FLAG_INVALID) atomicAdd(&cnt[0], 1);
-      if (fl & PAS_FLAG_NEAR_TOP1) atomicAdd(&cnt[1], 1);
-      if (fl & PAS_FLAG_NEAR_THRESHOLD) atomicAdd(&cnt[2], 1);
+    }
+    __syncthreads();   // every thread has read its candidates: the staging buffer becomes sid / ssc
+    if (t < np) {
+#pragma unroll
+      for (int i = 0; i < PAS_MAX_TOPK; ++i) {
+        if (i >= k) break;
+        sid[t * kp + i] = res[i].g;
+        ssc[t * kp + i] = res[i].s;
+      }
+      select_one(res[0].s, k > 1 ? res[1].s : -INFINITY, p, invalid, cold, P, o, ty);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < np * k; i += TP_THREADS) {   // coalesced global writes
+      const int j = (i / k) * kp + i % k;
+      if (o.topk_id) o.topk_id[p0 * k + i] = sid[j];
+      if (o.topk_score) o.topk_score[p0 * k + i] = ssc[j];
+      if (o.cand_out) o.cand_out[p0 * k + i] = Cand{ssc[j], sid[j]};
     }
   }
-  __syncthreads();
-  if (threadIdx.x < P.nK && hist[threadIdx.x]) atomicAdd(&o.hist[threadIdx.x], hist[threadIdx.x]);
-  if (threadIdx.x == 0) {
-    if (cnt[0]) atomicAdd(&o.plan->n_invalid, cnt[0]);
-    if (cnt[1]) atomicAdd(&o.plan->n_near_top1, cnt[1]);
-    if (cnt[2]) atomicAdd(&o.plan->n_near_threshold, cnt[2]);
+  flush_tally(P, o, ty);
+}
+
+// S == 1 (lists already merged, e.g. one cache range on one GPU): pure streaming.  Thread e owns the
+// pair of candidates 2e, 2e+1 (one 16-byte load, two 8-byte stores, all coalesced); the thread that
+// owns a prompt's first pair also does K4 for it.  Requires even k.
+constexpr int S1_THREADS = 256;
+template <int HALF>
+__global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict__ in,
+                                                          const uint8_t* __restrict__ pflags, const RouteParams P,
+                                                          SelectOut o) {
+  Tally ty;
+  ty.zero();
+  constexpr uint32_t half = HALF;
+  const bool cold = (P.M_total == 0);
+  const uint32_t total = (uint32_t)P.N * half;                    // <= 2^30
+  // persistent grid-stride loop: one smem histogram flush per CTA (global atomics stay O(grid))
+  for (uint32_t e = blockIdx.x * S1_THREADS + threadIdx.x; e < total; e += gridDim.x * S1_THREADS) {
+    const uint32_t p = e / half;
+    const int4 v = __ldg(in + e);
+    Cand c0{__int_as_float(v.x), v.y}, c1{__int_as_float(v.z), v.w};
+    const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
+    if (invalid || cold) {
+      c0 = Cand{-INFINITY, -1};
+      c1 = c0;
+    }
+    if (o.topk_id) reinterpret_cast<int2*>(o.topk_id)[e] = make_int2(c0.g, c1.g);
+    if (o.topk_score) reinterpret_cast<float2*>(o.topk_score)[e] = make_float2(c0.s, c1.s);
+    if (o.cand_out) reinterpret_cast<int4*>(o.cand_out)[e] = make_int4(__float_as_int(c0.s), c0.g,
+                                                                       __float_as_int(c1.s), c1.g);
+    if (e == p * half) select_one(c0.s, c1.s, p, invalid, cold, P, o, ty);
   }
+  flush_tally(P, o, ty);
 }
 
 __global__ void k_fill_sentinel(Cand* out, int64_t n) {
@@ -148,8 +314,32 @@ cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cud
 cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p,
                                 const SelectOut& o, cudaStream_t st) {
   if (p.N <= 0) return cudaSuccess;
-  const int64_t blocks = (p.N + WARPS - 1) / WARPS;
-  k_merge_select<<<(unsigned)blocks, WARPS * 32, 0, st>>>(in, S, pflags, p, o);
+  if (S == 1 && (p.topk & 1) == 0) {
+    const int64_t threads = p.N * (p.topk >> 1);
+    int64_t blocks = (threads + S1_THREADS - 1) / S1_THREADS;
+    if (blocks > (int64_t)kNumSMs * 8) blocks = (int64_t)kNumSMs * 8;   // one resident wave
+    const unsigned g = (unsigned)blocks;
+    const int4* in4 = reinterpret_cast<const int4*>(in);
+    switch (p.topk >> 1) {
+      case 1: k_select_s1<1><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 2: k_select_s1<2><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 3: k_select_s1<3><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 4: k_select_s1<4><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 5: k_select_s1<5><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 6: k_select_s1<6><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 7: k_select_s1<7><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      default: k_select_s1<8><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+    }
+  } else if (S <= 4 && S * p.topk <= TP_MAXSK) {
+    int64_t blocks = (p.N + TP_THREADS - 1) / TP_THREADS;
+    if (blocks > (int64_t)kNumSMs * 8) blocks = (int64_t)kNumSMs * 8;   // persistent CTAs
+    // staging for S lists in, and ids + scores (= 1 list of pairs) out, rows padded to k+1 pairs
+    const size_t smem = (size_t)(S > 1 ? S : 1) * TP_THREADS * (p.topk + 1) * sizeof(Cand);
+    k_merge_select_thr<<<(unsigned)blocks, TP_THREADS, smem, st>>>(in, S, pflags, p, o);
+  } else {
+    const int64_t blocks = (p.N + WARPS - 1) / WARPS;
+    k_merge_select<<<(unsigned)blocks, WARPS * 32, 0, st>>>(in, S, pflags, p, o);
+  }
   return cudaGetLastError();
 }
 

@@ -26,11 +26,24 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&v)[4]) {
   v[3] = __uint_as_float(x.y & 0xFFFF0000u);
 }
 
+// fp32_RN(v / norm) without a per-element fp64 division: q = v * RN(1 / norm) is within 2 ulp (fp64)
+// of v / norm, so fp32_RN(q) == fp32_RN(v / norm) unless v / norm lies within a few fp64 ulp of an
+// fp32 rounding midpoint -- recognisable from the 29 bits of q below the fp32 mantissa being
+// ~0x10000000 -- in which case (probability ~2^-25) the exact fp64 division decides.  One DMUL per
+// element instead of a division sequence keeps K1 off the fp64 pipe's limit and on the HBM roofline.
+__device__ __forceinline__ float div_rn(float v, double norm, double inv) {
+  const double q = (double)v * inv;
+  const long long low = __double_as_longlong(q) & 0x1FFFFFFFLL;
+  if (llabs(low - 0x10000000LL) <= 16) return __double2float_rn((double)v / norm);
+  return __double2float_rn(q);
+}
+
 __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[4], double norm, bool valid) {
   __nv_bfloat162 lo, hi;
   if (valid) {
-    lo = __floats2bfloat162_rn(__double2float_rn((double)v[0] / norm), __double2float_rn((double)v[1] / norm));
-    hi = __floats2bfloat162_rn(__double2float_rn((double)v[2] / norm), __double2float_rn((double)v[3] / norm));
+    const double inv = 1.0 / norm;
+    lo = __floats2bfloat162_rn(div_rn(v[0], norm, inv), div_rn(v[1], norm, inv));
+    hi = __floats2bfloat162_rn(div_rn(v[2], norm, inv), div_rn(v[3], norm, inv));
   } else {
     lo = __floats2bfloat162_rn(0.f, 0.f);
     hi = lo;
@@ -45,7 +58,7 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
 // so all its loads are in flight at once and the row is read from HBM exactly once; VEC = 0 is the
 // generic two-pass path for d > 1024.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(256) k_normalize(const T* __restrict__ in, int64_t rows, int d,
+__global__ void __launch_bounds__(256, 3) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count) {
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -113,11 +126,13 @@ template <typename T>
 cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8_t* flags, int64_t first_gid, int G,
                      int rank, int* invalid_count, cudaStream_t st) {
   const int threads = 256;
+  const int vec = d % 128 == 0 && d <= 1024 ? d / 128 : 0;
+  // grid = exactly the resident CTAs (3 per SM by the launch bounds): one wave, grid-stride rows
   int64_t blocks = (rows * 32 + threads - 1) / threads;
-  const int64_t cap = (int64_t)kNumSMs * 16;  // grid-stride beyond 16 CTAs (128 warps) per SM
+  const int64_t cap = (int64_t)kNumSMs * 3;
   if (blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
-  switch (d % 128 == 0 && d <= 1024 ? d / 128 : 0) {
+  switch (vec) {
     case 1: k_normalize<T, 1><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
     case 2: k_normalize<T, 2><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
     case 3: k_normalize<T, 3><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;

@@ -116,6 +116,10 @@ __global__ void k_plan(const int* __restrict__ hist, const RouteParams P, DevPla
     const int j = P.inst_level[w];
     plan->inst_list[j][plan->n_inst[j]++] = w;
   }
+  for (int j = 0; j < nK; ++j) {
+    const uint64_t d = plan->n_inst[j] > 0 ? (uint64_t)plan->n_inst[j] : 1;
+    plan->n_inst_magic[j] = ((1ull << 32) + d - 1) / d;
+  }
 }
 
 }  // namespace

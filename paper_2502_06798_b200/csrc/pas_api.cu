@@ -66,6 +66,8 @@ EncodeTiledFn get_encode_fn() {
 
 thread_local std::string g_global_err;
 
+constexpr int kMaxKb = 20;   // K6 buckets <= 16 << 20
+
 int ceil_log2(int64_t v) {
   int b = 0;
   while (((int64_t)1 << b) < v) ++b;
@@ -178,6 +180,9 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   p.nK = ctx->nK;
   p.W = ctx->W;
   p.bstar = ctx->bstar;
+  p.bstar_shift = -1;
+  for (int b = 0; b < 31; ++b)
+    if (ctx->bstar == (1 << b)) p.bstar_shift = b;
   p.mode = ctx->mode;
   p.topk = ctx->cfg.topk;
   p.G = ctx->cfg.world;
@@ -190,10 +195,10 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   // K6 buckets: nK << kb with kb = ceil(log2 N) - 4, so a class holding all N prompts averages
   // <= 16 prompts per bucket (the in-bucket rank loop) and the bucket scan stays small.
   int kb = ceil_log2(N > 1 ? N : 1) - 4;
-  p.kb = kb < 0 ? 0 : (kb > 16 ? 16 : kb);
+  p.kb = kb < 0 ? 0 : (kb > kMaxKb ? kMaxKb : kb);
   for (int i = 0; i < kMaxLevels; ++i) {
     p.grid[i] = ctx->grid[i];
-    p.thr[i] = ctx->thr[i];
+    p.thr[i] = i + 1 < ctx->nK ? ctx->thr[i] : INFINITY;   // +inf padding: level by binary search
     p.F[i] = ctx->F[i];
   }
   for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
@@ -201,10 +206,17 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   return p;
 }
 
-pas_status validate_out(pas_ctx* ctx, const pas_route_out* out) {
+pas_status validate_out(pas_ctx* ctx, const pas_route_out* out, bool device = true) {
   if (!out) return fail(ctx, PAS_ERR_ARG, "out is NULL");
   if (!out->K || !out->K_prime || !out->instance || !out->slot)
     return fail(ctx, PAS_ERR_ARG, "out->K, K_prime, instance and slot are required");
+  if (device) {
+    const void* ptrs[] = {out->K, out->K_prime, out->instance, out->slot, out->topk_id, out->topk_score,
+                          out->flags, out->bucket_offsets, out->bucket_prompts};
+    for (const void* q : ptrs)
+      if (reinterpret_cast<uintptr_t>(q) & 15)
+        return fail(ctx, PAS_ERR_ARG, "output arrays must be 16-byte aligned (vectorised stores)");
+  }
   return PAS_OK;
 }
 
@@ -218,10 +230,28 @@ pas_status ready(pas_ctx* ctx, int64_t N) {
   return PAS_OK;
 }
 
+// Prompt-side workspace (Q_hat, validity flags, K2 candidates, NCCL buffers), allocated on the first
+// call that runs a1 + a3, so a context used only through pas_route_from_candidates never holds it.
+pas_status ensure_prompt_ws(pas_ctx* ctx) {
+  if (ctx->qhat) return PAS_OK;
+  const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk, d = ctx->cfg.d;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = dmalloc(&ctx->qhat, (size_t)(ctx->q_rows * d));
+  if (e == cudaSuccess) e = dmalloc(&ctx->pflags, (size_t)mb);
+  if (e == cudaSuccess) e = dmalloc(&ctx->cand_local, (size_t)(ctx->cand_cap * k));
+  if (e == cudaSuccess) e = dmalloc(&ctx->cand_rank, (size_t)(mb * k));
+  if (e == cudaSuccess && ctx->cfg.world > 1) e = dmalloc(&ctx->cand_all, (size_t)((int64_t)ctx->cfg.world * mb * k));
+  if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "prompt workspace allocation failed: %s", cudaGetErrorString(e));
+  if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, simtopk_box_q()))
+    return fail(ctx, PAS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the prompt map");
+  return PAS_OK;
+}
+
 // a1 + a3 (+ the intra-GPU part of a4 into `merged` if non-null).  Returns the candidate layout.
 pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cudaStream_t st, const Cand** cand,
                      int* S, Cand* merged) {
   const int k = ctx->cfg.topk;
+  if (pas_status s = ensure_prompt_ws(ctx)) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   ctx->launches++;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
@@ -258,7 +288,8 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->hist, 0, sizeof(int) * kMaxLevels, st));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->plan, 0, sizeof(DevPlan), st));
   SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
-  CUDA_TRY(ctx, launch_merge_select(cand, S, ctx->pflags, p, so, st));
+  const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;   // else: all prompts valid
+  CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
   CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
@@ -309,8 +340,9 @@ pas_status pas_destroy(pas_ctx* ctx) {
   }
   void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all,
                   ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
-                  ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.items,     ctx->rw.cls7,   ctx->rw.lvl_prime,
-                  ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->stage_emb, ctx->s_K, ctx->s_Kp,
+                  ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.sorted,    ctx->rw.cls7,
+                  ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp, ctx->rw.scan_tmp,
+                  ctx->stage_emb, ctx->s_K, ctx->s_Kp,
                   ctx->s_inst,  ctx->s_slot,    ctx->s_tid,      ctx->s_boff,       ctx->s_bpr,     ctx->s_tsc,
                   ctx->s_flags};
   for (void* p : ptrs)
@@ -356,17 +388,14 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->cap_rows = cfg->max_rows_per_rank;
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
   ctx->cand_cap = 4 * mb > 592 * qt ? 4 * mb : 592 * qt;
-  const int64_t nb = (int64_t)kMaxLevels << 16;
-  const int64_t nblk = (mb + 1023) / 1024;
+  int kbm = ceil_log2(mb > 1 ? mb : 1) - 4;
+  kbm = kbm < 0 ? 0 : (kbm > kMaxKb ? kMaxKb : kbm);
+  const int64_t nb = (int64_t)kMaxLevels << kbm;
+  const int64_t ncls = 64 * (int64_t)batch_tiles(mb);
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, n) \
   if (e == cudaSuccess) e = dmalloc(&(ptr), (size_t)(n))
   ALLOC(ctx->store, (ctx->cap_rows > 0 ? ctx->cap_rows : 1) * d);
-  ALLOC(ctx->qhat, ctx->q_rows * d);
-  ALLOC(ctx->pflags, mb);
-  ALLOC(ctx->cand_local, ctx->cand_cap * k);
-  ALLOC(ctx->cand_rank, mb * k);
-  if (cfg->world > 1) ALLOC(ctx->cand_all, (int64_t)cfg->world * mb * k);
   ALLOC(ctx->level, mb);
   ALLOC(ctx->hist, kMaxLevels);
   ALLOC(ctx->invalid_count, 1);
@@ -376,12 +405,13 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ALLOC(ctx->rw.bcount, nb);
   ALLOC(ctx->rw.bstart, nb);
   ALLOC(ctx->rw.bfill, nb);
-  ALLOC(ctx->rw.items, mb);
+  ALLOC(ctx->rw.sorted, mb);
   ALLOC(ctx->rw.cls7, mb);
-  ALLOC(ctx->rw.lvl_prime, mb);
-  ALLOC(ctx->bw.blk_counts, nblk * 64);
-  ALLOC(ctx->bw.blk_off, nblk * 64);
+  ALLOC(ctx->rw.scan_tmp, scan_tmp_ints(nb));
+  ALLOC(ctx->bw.blk_counts, ncls);
+  ALLOC(ctx->bw.blk_off, ncls);
   ALLOC(ctx->bw.offsets, kMaxInst + 1);
+  ALLOC(ctx->bw.scan_tmp, scan_tmp_ints(ncls));
 #undef ALLOC
   if (e != cudaSuccess) {
     pas_destroy(ctx);
@@ -392,8 +422,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
     }
-  if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, simtopk_box_q()) ||
-      !encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c())) {
+  if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c())) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
   }
@@ -574,8 +603,6 @@ pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, 
   if (N == 0) return PAS_OK;
   if ((s = validate_out(ctx, out))) return s;
   if (!cand_dev) return fail(ctx, PAS_ERR_ARG, "null candidates");
-  if (ctx->last_local_N != N)
-    return fail(ctx, PAS_ERR_STATE, "pas_route_local with the same N must precede (validity flags)");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
@@ -623,7 +650,7 @@ pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dt
   if ((s = ready(ctx, N))) return s;
   if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
   if (N == 0) return PAS_OK;
-  if ((s = validate_out(ctx, oh))) return s;
+  if ((s = validate_out(ctx, oh, false))) return s;
   if (!emb_host) return fail(ctx, PAS_ERR_ARG, "emb_host is NULL");
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk;
@@ -714,6 +741,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   if (N < 1 || N > ctx->cfg.max_batch || !emb || !scores_dev) return fail(ctx, PAS_ERR_ARG, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
                 ctx->cand_local, scores_dev};

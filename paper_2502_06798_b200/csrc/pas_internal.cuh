@@ -38,6 +38,7 @@ struct RouteParams {
   int64_t N, M_total;
   uint64_t seed, batch_seq;
   int kb;                        // K6 bucket bits of kappa
+  int bstar_shift;               // log2(bstar) if bstar is a power of two, else -1
   int grid[kMaxLevels];          // K values
   float thr[kMaxLevels];         // nK-1 thresholds
   double F[kMaxLevels];          // load fractions
@@ -53,6 +54,7 @@ struct DevPlan {
   int X[kMaxLevels][kMaxLevels];     // inclusive prefix sums of the rows of x
   int class_start[kMaxLevels + 1];   // exclusive prefix of h
   int n_inst[kMaxLevels];
+  uint64_t n_inst_magic[kMaxLevels];   // ceil(2^32 / n_j): x / n_j == (x * magic) >> 32 for x < 2^26
   int inst_list[kMaxLevels][kMaxInst];
   double D_Q, D_Q_LP;
   int n_redirected, n_upgraded, n_downgraded;
@@ -105,30 +107,42 @@ cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, co
 cudaError_t launch_plan(const int* hist, const RouteParams& p, DevPlan* plan, cudaStream_t st);
 
 // K6 redirection
+struct __align__(16) KeyEntry {
+  uint64_t key;           // (class << 60) | kappa
+  int32_t p;              // prompt index
+  int32_t pad;
+};
 struct RedirectWs {
   uint64_t* key;          // [N]
   int32_t* bucket;        // [N]
   int32_t* bcount;        // [nK << kb]   zeroed
   int32_t* bstart;        // [nK << kb]
   int32_t* bfill;         // [nK << kb]   zeroed
-  int32_t* items;         // [N]
+  KeyEntry* sorted;       // [N] bucket order
   int32_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
-  int32_t* lvl_prime;     // [N]
+  int32_t* scan_tmp;      // scan_tmp_ints(nK << kb)
 };
 cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan,
                             const RedirectWs& w, int32_t* K_prime, cudaStream_t st, int* launches);
 
 // K7 route-and-batch
 struct BatchWs {
-  int32_t* blk_counts;   // [nblk * 64]
-  int32_t* blk_off;      // [nblk * 64]
+  int32_t* blk_counts;   // [64 * batch_tiles(N)], class-major
+  int32_t* blk_off;      // [64 * batch_tiles(N)]
   int32_t* offsets;      // [W+1]
+  int32_t* scan_tmp;     // scan_tmp_ints(64 * batch_tiles(N))
 };
+int batch_tiles(int64_t N);
 cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan,
                                    const BatchWs& w, int32_t* instance, int32_t* slot,
                                    int32_t* bucket_offsets, int32_t* bucket_prompts,
                                    cudaStream_t st, int* launches);
 
 cudaError_t launch_fill_sentinel(Cand* out, int64_t n, cudaStream_t st);
+
+// device-wide exclusive scan of n int32 (tmp: scan_tmp_ints(n) ints)
+int scan_tmp_ints(int64_t n);
+cudaError_t launch_exclusive_scan(const int32_t* in, int32_t* out, int n, int32_t* tmp, cudaStream_t st,
+                                  int* launches);
 
 }  // namespace pas

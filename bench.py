@@ -189,15 +189,12 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2502_06798_b200 import dist as pdist
     from paper_2502_06798_b200 import pas
 
-    nccl_id = None
-    if world > 1:
-        obj = [pas.pas_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    nccl_id = pdist.bootstrap_nccl_id(rank) if world > 1 else None
     G = world
-    M_local = (M + G - 1) // G
+    M_local = max(1, pdist.shard_rows(M, G, rank))
     router = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M_local, device=local,
                         rank=rank, world=G, nccl_id=nccl_id, seed=cfg.route_seed)
     router.set_bands(cfg.grid, cfg.thresholds)
@@ -322,11 +319,8 @@ def main():
 
 
 def max_over_ranks(x, dist, dev, torch):
-    if not dist:
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2502_06798_b200 import dist as pdist
+    return pdist.max_over_ranks(x, dev) if dist else x
 
 
 def reference_arm(args, cfg, N, M, rank, world):

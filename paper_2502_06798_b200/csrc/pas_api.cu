@@ -588,6 +588,7 @@ pas_status pas_route_local(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   if (N == 0) return PAS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
   const Cand* cand;
   int S;
@@ -626,6 +627,7 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
     return fail(ctx, PAS_ERR_STATE, "world > 1 without an NCCL communicator: use the split calls");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;   // first call only: outside the timed stages
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
   const Cand* cand;
   int S;

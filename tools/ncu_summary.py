@@ -32,6 +32,8 @@ def launches(path, steps=None):
     rows = list(csv.DictReader(io.StringIO(txt[start:])))
     per = {}
     for r in rows:
+        if r.get("Metric Name", "gpu__time_duration.sum") != "gpu__time_duration.sum":
+            continue
         name = re.sub(r"\(.*", "", r["Kernel Name"]).split("::")[-1]
         v = float(r["Metric Value"].replace(",", ""))
         scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r["Metric Unit"], 1e-3)

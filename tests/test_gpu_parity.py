@@ -337,3 +337,63 @@ def test_validation_errors(pas):
     r.load_cache(torch.randn(10, 768, device=DEV))
     assert pas.pas_cache_size(r.ctx) == (10, 10)
     r.close()
+
+
+# ------------------------------------------------------------------------------------------------
+def _full_parity(pas, cfg, N, M, topk=8, mode=None, bstar=None, d=None, instance_level=None, F=None,
+                 dtype=torch.float32, seed=0):
+    """Full-oracle parity on a small problem with overridable k, d, instances, F and input dtype."""
+    import dataclasses
+    cfg = dataclasses.replace(cfg, topk=topk, d=d or cfg.d,
+                              instance_level=instance_level or cfg.instance_level, F=F or cfg.F)
+    w = Workload(cfg, device=DEV, M=M, d=cfg.d)
+    C_ = w.cache_rows(0, M).contiguous()
+    P = w.prompts(N).to(dtype).contiguous()
+    r = pas.Router(d=cfg.d, topk=topk, max_batch=N, max_rows_per_rank=M, device=0, seed=cfg.route_seed)
+    r.set_bands(cfg.grid, cfg.thresholds)
+    r.set_fractions(cfg.F, cfg.instance_level, cfg.bstar if bstar is None else bstar,
+                    cfg.mode if mode is None else mode)
+    r.load_cache(C_)
+    g = _host(r.route(P))
+    torch.cuda.synchronize()
+    st = r.stats()
+    r.close()
+    Ph = P.float().cpu().numpy()
+    o_ids, o_sc, valid = oracle_topk_streaming(Ph, [(0, C_.cpu().numpy())], topk)
+    rep = Report()
+    check_topk(g["topk_id"].reshape(N, topk), g["topk_score"].reshape(N, topk), o_ids, o_sc, rep)
+    glev = _levels(cfg, g["K"])
+    o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid)
+    check_levels(glev, o_sc[:, 0], o_lev, valid, cfg.thresholds, rep)
+    check_downstream(g, glev, _setup(cfg, mode, bstar), st, rep, len(cfg.instance_level))
+    return rep, st
+
+
+@pytest.mark.parametrize("topk", [1, 3, 16])
+def test_topk_widths(pas, topk):
+    """k = 1 (K from top-1 only), odd k (thread-per-prompt select), k = 16 (the KMAX = 16 epilogue)."""
+    _full_parity(pas, CONFIGS["C2"], N=300, M=3001, topk=topk)
+
+
+@pytest.mark.parametrize("d", [320, 1024])
+def test_embedding_widths(pas, d):
+    """d = 320 (d % 128 != 0: the generic K1 path, 5 k-blocks) and d = 1024 (16 k-blocks)."""
+    _full_parity(pas, CONFIGS["C1"], N=200, M=2000, d=d)
+
+
+def test_bf16_embeddings(pas):
+    _full_parity(pas, CONFIGS["C1"], N=150, M=1500, dtype=torch.bfloat16)
+
+
+def test_many_ranges_warp_merge(pas):
+    """Few prompts against a large cache: R > 4 ranges, so the warp-per-prompt S-way merge runs."""
+    rep, st = _full_parity(pas, CONFIGS["C1"], N=100, M=150_000)
+    assert st["stage_ms"][1] > 0
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_many_instances(pas, mode):
+    """W = 40 serving instances (several per level; in uniform mode > 32 classes for K7)."""
+    cfg = CONFIGS["C2"]
+    inst = [i % 6 for i in range(40)]
+    _full_parity(pas, cfg, N=2000, M=5000, instance_level=inst, mode=mode, bstar=1 if mode else 3)

@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -59,3 +60,12 @@ def test_version_and_clean_failures_without_gpu(lib):
         lib.pas_create(d=100)             # d must be a multiple of 64
     st = lib.lib.pas_route_batch(None, None, 0, 0, None, None)
     assert st == -1                       # null context -> PAS_ERR_ARG, nothing enqueued
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """No silent CPU fallback: importing the binding with no library raises ImportError."""
+    code = ("import os, sys; os.environ['PAS_LIB'] = %r; sys.path.insert(0, %r)\n"
+            "try:\n    import paper_2502_06798_b200.pas\nexcept ImportError as e:\n    print('raised', e)\n")
+    out = subprocess.run([sys.executable, "-c", code % (str(tmp_path / "missing.so"), ROOT)],
+                         capture_output=True, text=True)
+    assert "raised" in out.stdout, out.stdout + out.stderr

@@ -19,14 +19,15 @@
 // units u = id + i*count with m fastest, so concurrently running CTAs stream the SAME cache tiles
 // (L2 reuse of the big operand) against different prompt tiles.
 //
-// Warp roles per CTA (192 threads, 1 CTA/SM):
+// Warp roles per CTA (320 threads, 1 CTA/SM):
 //   warp 0      TMA producer (128-B swizzle, mbarrier complete_tx).
 //   warp 1      TMEM allocation (512 columns = two 256-column fp32 accumulators) and one lane issuing
 //               tcgen05.mma + tcgen05.commit (smem stage released, accumulator ready).
-//   warps 2..5  epilogue over the CTA's 128 TMEM lanes: tcgen05.ld of 32 columns, max of the chunk
-//               vs the current k-th score, and only when the chunk can improve the list a
-//               branch-free bubble insert (strict >, columns ascending, so equal scores keep the
-//               lower gid).
+//   warps 2..9  epilogue over the CTA's 128 TMEM lanes, two warps per lane quarter (column halves
+//               0..127 / 128..255 of every tile, each with its own top-k list, merged by a bitonic
+//               network at the end of the unit): tcgen05.ld of 32 columns, max of the chunk vs the
+//               current k-th score, and only when the chunk can improve the list a branch-free
+//               bubble insert (strict >, columns ascending, so equal scores keep the lower column).
 #include <cfloat>
 #include <cstdio>
 
@@ -50,11 +51,14 @@ constexpr int STAGES = PAIR ? 6 : 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN_CTA * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
-constexpr int NUM_THREADS = 192;
+constexpr int EPI_WARPS = 8;                     // 2 per TMEM lane quarter: column halves
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_WORKERS = kNumSMs / CTAS;      // persistent CTAs (or pairs)
 constexpr int UNIT_ROWS = BM * CTAS;             // prompt rows per work unit
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int LIST_BYTES = BM * 16 * 8;             // hand-over of the upper half's lists (KMAX <= 16)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + LIST_BYTES;
+constexpr int WARMUP_TILES = 24;
 
 struct __align__(8) Bars {
   uint64_t full[STAGES];    // TMA bytes landed (leader's barrier in pair mode)
@@ -77,7 +81,7 @@ template <int KMAX, bool PARTIAL>
 __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_local, float (&s)[KMAX],
                                             int32_t (&gl)[KMAX]) {
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < BN / 64; ++c) {   // this warp's half of the tile: 4 chunks of 32 columns
     uint32_t v[32];
     ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
     ptx::tmem_wait_ld();
@@ -110,6 +114,38 @@ __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_loc
   }
 }
 
+// Top-KMAX of two sorted lists (score desc, column asc): bitonic half-cleaner against the reversed
+// partner list, then a bitonic sort of the KMAX winners -- static indexing only.
+__device__ __forceinline__ bool better(float sa, int ga, float sb, int gb) {
+  return sa > sb || (sa == sb && (unsigned)ga < (unsigned)gb);
+}
+template <int KMAX>
+__device__ __forceinline__ void merge_lists(float (&s)[KMAX], int32_t (&gl)[KMAX], const float* ps, const int32_t* pg) {
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    const float bs = ps[KMAX - 1 - i];
+    const int32_t bg = pg[KMAX - 1 - i];
+    if (!better(s[i], gl[i], bs, bg)) { s[i] = bs; gl[i] = bg; }
+  }
+#pragma unroll
+  for (int len = KMAX / 2; len >= 1; len >>= 1) {
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      if ((i & len) == 0) {
+        const int j = i + len;
+        if (!better(s[i], gl[i], s[j], gl[j])) {
+          const float ts = s[i]; s[i] = s[j]; s[j] = ts;
+          const int32_t tg = gl[i]; gl[i] = gl[j]; gl[j] = tg;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+}
+
 template <int KMAX, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
@@ -120,6 +156,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  float* list_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [BM][KMAX]
+  int32_t* list_g = reinterpret_cast<int32_t*>(list_s + BM * KMAX);            // [BM][KMAX]
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -138,7 +176,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&bars->tfull[a], 1);
-      ptx::mbar_init(&bars->tempty[a], 4 * CTAS);  // one arrive per epilogue warp (of both CTAs)
+      ptx::mbar_init(&bars->tempty[a], EPI_WARPS * CTAS);  // one arrive per epilogue warp (of both CTAs)
     }
     ptx::fence_mbar_init();
   }
@@ -225,8 +263,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ------------------------------- epilogue -----------------------------------
     const uint32_t q = warp & 3;              // TMEM lane quarter this warp may access
+    const int half = (int)(warp - 2) >> 2;    // 0: columns 0..127 of each tile, 1: 128..255
     const int row = (int)(q * 32 + lane);
-    const uint32_t lane_addr = tmem_base + ((q * 32u) << 16);
+    const uint32_t lane_addr = tmem_base + ((q * 32u) << 16) + half * (BN / 2);
     const int Ml = (int)M_local;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -241,11 +280,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t0; t < t1; ++t) {
         ptx::mbar_wait(&bars->tfull[acc], acc_phase);
         ptx::tc_fence_after();
-        const int col_base = t * BN;
+        const int col_base = t * BN + half * (BN / 2);
         const uint32_t taddr = lane_addr + acc * BN;
         if (DUMP) {
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = 0; c < BN / 64; ++c) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
             ptx::tmem_wait_ld();
@@ -255,7 +294,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 32; ++j)
                 if (col0 + j < M_local) dump[prompt * M_local + col0 + j] = __uint_as_float(v[j]);
           }
-        } else if (col_base + BN > Ml) {
+        } else if (col_base + BN / 2 > Ml) {
           epi_tile<KMAX, true>(taddr, col_base, Ml, s, gl);
         } else {
           epi_tile<KMAX, false>(taddr, col_base, Ml, s, gl);
@@ -269,11 +308,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
-      if (!DUMP && prompt < N) {
-        Cand* dst = out + ((int64_t)r * N + prompt) * k;
+      if (!DUMP) {
+        // the upper-half warps hand their lists over; the lower half merges and writes
+        if (half == 1) {
 #pragma unroll
-        for (int i = 0; i < KMAX; ++i)
-          if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
+          for (int i = 0; i < KMAX; ++i) {
+            list_s[row * KMAX + i] = s[i];
+            list_g[row * KMAX + i] = gl[i];
+          }
+        }
+        epi_barrier();
+        if (half == 0) {
+          merge_lists<KMAX>(s, gl, list_s + row * KMAX, list_g + row * KMAX);
+          if (prompt < N) {
+            Cand* dst = out + ((int64_t)r * N + prompt) * k;
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i)
+              if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
+          }
+        }
+        epi_barrier();
       }
     }
   }
@@ -321,8 +375,10 @@ cudaError_t simtopk_init() {
 }
 
 // Pick the number of cache ranges R so that (prompt tiles x R) units fill the persistent workers with
-// the smallest makespan: waves(R) * (tiles per unit + 1 tile of per-unit overhead), subject to the
-// candidate buffer (R * N <= cand_rows).
+// the smallest makespan: waves(R) * (tiles per unit + WARMUP_TILES), subject to the candidate buffer
+// (R * N <= cand_rows).  WARMUP_TILES prices a unit's start: while a fresh top-k list is filling,
+// nearly every 32-column chunk of some lane takes the insert path (P(insert) ~ 32 k / columns seen),
+// which makes the first ~8k columns of a unit epilogue-bound rather than MMA-bound.
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
   const int64_t MT = (N + UNIT_ROWS - 1) / UNIT_ROWS;
   const int64_t NT = (M_local + BN - 1) / BN;
@@ -333,7 +389,7 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
   for (int64_t R = 1; R <= rmax; ++R) {
     if (R > 1 && R * N > cand_rows) break;
     const int64_t waves = (MT * R + NUM_WORKERS - 1) / NUM_WORKERS;
-    const double cost = (double)waves * (double)((NT + R - 1) / R + 1);
+    const double cost = (double)waves * (double)((NT + R - 1) / R + WARMUP_TILES);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = (int)R; }
   }
   return best;

@@ -385,7 +385,7 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
   if (NT <= 1 || MT <= 0) return 1;
   int best = 1;
   double best_cost = 1e300;
-  const int64_t rmax = NT < 64 ? NT : 64;
+  const int64_t rmax = NT < 128 ? NT : 128;   // the S-way merge takes S <= 128 sources
   for (int64_t R = 1; R <= rmax; ++R) {
     if (R > 1 && R * N > cand_rows) break;
     const int64_t waves = (MT * R + NUM_WORKERS - 1) / NUM_WORKERS;

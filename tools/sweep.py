@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Sweeps behind BASELINE's metric "prompts scheduled/s vs cache size" on one B200.
+
+  --kind cache   N = 16,384 prompts vs M in {1k, 100k, 1M, 10M, 50M} (SURVEY 8(d) "sweep" row)
+  --kind load    C5: N = 256 .. 131,072 (x2) vs a 50M-entry cache, F(K) recomputed before every
+                 batch from the previous batch's H_K (F_b = (1 - l_b) h_{b-1} / N_{b-1} + l_b e_{K=25},
+                 l_b = log2(N_b / 256) / 9), the pas_set_fractions call timed
+                 with the batch.
+
+Device time with CUDA events per batch (median of --steps), stage split from pas_plan_stats.  One
+JSON object per line.  The cache is generated on the GPU block by block (synth-v1).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", choices=["cache", "load"], default="cache")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--max-cache", type=int, default=50_000_000)
+    ap.add_argument("--ns", type=str, default="", help="comma-separated N values for --kind load")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2502_06798_b200 import pas
+    from synth import CONFIGS, Workload
+
+    dev = torch.device("cuda", 0)
+    if args.kind == "cache":
+        cfg = CONFIGS["C4"]
+        N = 16384
+        sizes = [m for m in (1_000, 100_000, 1_000_000, 10_000_000, 50_000_000) if m <= args.max_cache]
+        for M in sizes:
+            w = Workload(cfg, device=dev, M=M)
+            r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M, device=0, seed=cfg.route_seed)
+            r.set_bands(cfg.grid, cfg.thresholds)
+            r.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
+            t0 = time.perf_counter()
+            for b in range(w.n_blocks()):
+                r.load_cache(w.cache_block(b).contiguous())
+            load_s = time.perf_counter() - t0
+            P = w.prompts(N)
+            out = r.alloc_out(N)
+            ms = []
+            k2 = []
+            for i in range(args.warmup + args.steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r.route(P, out)
+                e1.record()
+                e1.synchronize()
+                if i >= args.warmup:
+                    ms.append(e0.elapsed_time(e1))
+                    k2.append(r.stats()["stage_ms"][1])
+            med = statistics.median(ms)
+            tf = 2.0 * N * M * cfg.d / (statistics.median(k2) / 1e3) / 1e12
+            print(json.dumps({"kind": "cache", "N": N, "M": M, "prompts_per_s": N / (med / 1e3), "ms_median": med,
+                              "ms_p10": sorted(ms)[max(0, len(ms) // 10)], "ms_p90": sorted(ms)[min(len(ms) - 1, (9 * len(ms)) // 10)],
+                              "k2_tflops": tf, "cache_load_s": round(load_s, 2)}), flush=True)
+            r.close()
+            del w, P, out
+            torch.cuda.empty_cache()
+    else:
+        cfg = CONFIGS["C5"]
+        M = min(cfg.M, args.max_cache)
+        Ns = [int(x) for x in args.ns.split(",")] if args.ns else [256 << i for i in range(10)]
+        w = Workload(cfg, device=dev, M=M)
+        r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=Ns[-1], max_rows_per_rank=M, device=0, seed=cfg.route_seed)
+        r.set_bands(cfg.grid, cfg.thresholds)
+        nK = len(cfg.grid)
+        F = [1.0 / nK] * nK
+        r.set_fractions(F, cfg.instance_level, cfg.bstar, cfg.mode)
+        t0 = time.perf_counter()
+        for b in range(w.n_blocks()):
+            r.load_cache(w.cache_block(b).contiguous())
+        load_s = time.perf_counter() - t0
+        Pall = w.prompts(Ns[-1])
+        prev_h, prev_N = None, None
+        for N in Ns:
+            P = Pall[:N].contiguous()
+            out = r.alloc_out(N)
+            ell = math.log2(N / 256) / 9
+            ms = []
+            for i in range(args.warmup + args.steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                if prev_h is not None:          # controller update from the previous batch's H_K
+                    F = [(1 - ell) * h / prev_N for h in prev_h]
+                    F[-1] += ell
+                    s = sum(F)
+                    F = [f / s for f in F]
+                    r.set_fractions(F, cfg.instance_level, cfg.bstar, cfg.mode)
+                r.route(P, out)
+                e1.record()
+                st = r.stats()                  # syncs; H_K of this batch feeds the next F
+                prev_h, prev_N = st["h"], N
+                if i >= args.warmup:
+                    ms.append(e0.elapsed_time(e1))
+            med = statistics.median(ms)
+            print(json.dumps({"kind": "load", "N": N, "M": M, "prompts_per_s": N / (med / 1e3), "ms_median": med,
+                              "stage_ms": st["stage_ms"][:7], "D_Q": st["D_Q"], "F": [round(f, 4) for f in F],
+                              "h": st["h"], "cache_load_s": round(load_s, 2)}), flush=True)
+        r.close()
+
+
+if __name__ == "__main__":
+    main()

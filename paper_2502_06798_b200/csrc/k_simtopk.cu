@@ -77,11 +77,11 @@ __device__ __forceinline__ int opaque(int x) {
 // Epilogue over one accumulator: 32-column chunks (tcgen05.ld), chain max (FMNMX3), the column id
 // materialised only inside the (rare) insert path, the tail mask only on the last partial tile.
 // (A double-buffered tcgen05.ld + tree-max variant was 7 % slower under the power cap: DESIGN.md 8.)
-template <int KMAX, bool PARTIAL>
+template <int KMAX, bool PARTIAL, int NCH = BN / 64>
 __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_local, float (&s)[KMAX],
                                             int32_t (&gl)[KMAX]) {
 #pragma unroll 1
-  for (int c = 0; c < BN / 64; ++c) {   // this warp's half of the tile: 4 chunks of 32 columns
+  for (int c = 0; c < NCH; ++c) {   // this warp's share of the tile: NCH chunks of 32 columns
     uint32_t v[32];
     ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
     ptx::tmem_wait_ld();
@@ -341,6 +341,220 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// A-in-TMEM variant (d <= 768): the CTA's 128 prompt rows (Q_hat, bf16) are written into tensor
+// memory once per work unit (tcgen05.st by the epilogue warps, K/2 columns of packed bf16 pairs per
+// lane) and every tcgen05.mma takes A from TMEM ("[a]" operand) and only B from shared memory.
+// Per cache tile only the B k-blocks cross L2 -> SMEM (8 KB stages, 64 cache rows), cutting the L2
+// and SMEM traffic per flop by a third against the SS tile.  TMEM: A in columns [0, d/2), two
+// 64-column fp32 accumulators at 384 and 448.  MMA M = 128, N = 64, K = 16 (32 cycles each).
+// ------------------------------------------------------------------------------------------------
+constexpr int TA_BN = 64;
+constexpr int TA_STAGES = 12;
+constexpr int TA_B_BYTES = TA_BN * BK * 2;
+constexpr int TA_ACC_COL = 384;
+constexpr int TA_SMEM_BYTES = TA_STAGES * TA_B_BYTES + 1024 /*align*/ + 512 /*barriers*/ + LIST_BYTES;
+
+struct __align__(8) TaBars {
+  uint64_t full[TA_STAGES];
+  uint64_t empty[TA_STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint64_t a_ready;
+  uint32_t tmem_base;
+};
+
+template <int KMAX, bool DUMP>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_simtopk_ta(const __grid_constant__ CUtensorMap tmC, const __nv_bfloat16* __restrict__ qhat, int64_t N,
+                 int64_t M_local, int d, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
+                 float* __restrict__ dump) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;
+  TaBars* bars = reinterpret_cast<TaBars*>(smem + TA_STAGES * TA_B_BYTES);
+  float* list_s = reinterpret_cast<float*>(smem + TA_STAGES * TA_B_BYTES + 512);
+  int32_t* list_g = reinterpret_cast<int32_t*>(list_s + BM * KMAX);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const int units = MT * R;
+  const int kblocks = d / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmC);
+    for (int s = 0; s < TA_STAGES; ++s) {
+      ptx::mbar_init(&bars->full[s], 1);
+      ptx::mbar_init(&bars->empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&bars->tfull[a], 1);
+      ptx::mbar_init(&bars->tempty[a], EPI_WARPS);
+    }
+    ptx::mbar_init(&bars->a_ready, EPI_WARPS);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = bars->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------- TMA producer (B only) ---------------------------
+    if (ptx::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int r = u / MT;
+        const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < kblocks; ++kb) {
+            ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&bars->full[stage], TA_B_BYTES);
+            ptx::tma_load_2d(&tmC, sB + stage * TA_B_BYTES, &bars->full[stage], kb * BK, t * TA_BN,
+                             ptx::kEvictNormal);
+            if (++stage == TA_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------- MMA issuer --------------------------------------
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, TA_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      uint32_t a_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int r = u / MT;
+        const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+        ptx::mbar_wait(&bars->a_ready, a_phase);   // this unit's prompt rows are in TMEM
+        a_phase ^= 1;
+        ptx::tc_fence_after();
+        for (int t = t0; t < t1; ++t) {
+          ptx::mbar_wait(&bars->tempty[acc], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + TA_ACC_COL + acc * TA_BN;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            ptx::mbar_wait(&bars->full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t b0 = ptx::smem_u32(sB + stage * TA_B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              ptx::umma_f16_ts(d_tmem, tmem_base + kb * (BK / 2) + kk * 8, ptx::sdesc_kmajor_sw128(b0 + kk * 32),
+                               idesc, (kb | kk) != 0);
+            ptx::umma_commit(&bars->empty[stage]);
+            if (++stage == TA_STAGES) { stage = 0; phase ^= 1; }
+          }
+          ptx::umma_commit(&bars->tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------- epilogue ----------------------------------------
+    const uint32_t q = warp & 3;
+    const int half = (int)(warp - 2) >> 2;      // chunk of the 64-column tile: columns half*32..+32
+    const int row = (int)(q * 32 + lane);
+    const uint32_t lane_off = (q * 32u) << 16;
+    const int Ml = (int)M_local;
+    const int acols = d / 4;                    // 32-bit A columns written by each half
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int m = u % MT, r = u / MT;
+      const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+      const int64_t prompt = (int64_t)m * BM + row;
+      // A rows -> TMEM (the previous unit's MMAs are complete: this warp consumed its last tile)
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(qhat + prompt * d + half * (d / 2));
+#pragma unroll 1
+        for (int g = 0; g < acols / 16; ++g) {
+          uint32_t v[16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 x = __ldg(src + g * 4 + j);
+            v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+          }
+          ptx::tmem_st_32x32b_x16(tmem_base + lane_off + half * acols + g * 16, v);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars->a_ready);
+      }
+      float s[KMAX];
+      int32_t gl[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; gl[i] = -1; }
+      for (int t = t0; t < t1; ++t) {
+        ptx::mbar_wait(&bars->tfull[acc], acc_phase);
+        ptx::tc_fence_after();
+        const int col_base = t * TA_BN + half * 32;
+        const uint32_t taddr = tmem_base + lane_off + TA_ACC_COL + acc * TA_BN + half * 32;
+        if (DUMP) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(taddr, v);
+          ptx::tmem_wait_ld();
+          if (prompt < N)
+            for (int j = 0; j < 32; ++j)
+              if ((int64_t)col_base + j < M_local) dump[prompt * M_local + col_base + j] = __uint_as_float(v[j]);
+        } else if (col_base + 32 > Ml) {
+          epi_tile<KMAX, true, 1>(taddr, col_base, Ml, s, gl);
+        } else {
+          epi_tile<KMAX, false, 1>(taddr, col_base, Ml, s, gl);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars->tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+      if (!DUMP) {
+        if (half == 1) {
+#pragma unroll
+          for (int i = 0; i < KMAX; ++i) {
+            list_s[row * KMAX + i] = s[i];
+            list_g[row * KMAX + i] = gl[i];
+          }
+        }
+        epi_barrier();
+        if (half == 0) {
+          merge_lists<KMAX>(s, gl, list_s + row * KMAX, list_g + row * KMAX);
+          if (prompt < N) {
+            Cand* dst = out + ((int64_t)r * N + prompt) * k;
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i)
+              if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
+          }
+        }
+        epi_barrier();
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int KMAX, bool DUMP>
+cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
+  k_simtopk_ta<KMAX, DUMP><<<grid, NUM_THREADS, TA_SMEM_BYTES, st>>>(*a.tmap_c, a.qhat, a.N, a.M_local, a.d, a.k, a.G,
+                                                                     a.rank, a.R, MT, NT, a.out, a.dump);
+  return cudaGetLastError();
+}
+
 template <int KMAX, bool DUMP>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
@@ -361,14 +575,22 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaS
 
 }  // namespace
 
+#ifndef PAS_K2_ATMEM   // A-in-TMEM variant: correct, but 29 % slower under the power cap
+#define PAS_K2_ATMEM 0
+#endif
+bool simtopk_uses_tmem_a(int d) { return PAS_K2_ATMEM && !PAIR && d <= 2 * TA_ACC_COL; }
 size_t simtopk_smem_bytes() { return SMEM_BYTES; }
 int simtopk_prompt_rows() { return UNIT_ROWS; }
 int simtopk_box_q() { return BM; }
-int simtopk_box_c() { return BN_CTA; }
+int simtopk_box_c(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : BN_CTA; }
+static int tile_rows(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : BN; }
 
 // Opt the kernel variants into > 48 KB dynamic shared memory on the current device.
 cudaError_t simtopk_init() {
   cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk_ta<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES))) return e;
   return cudaFuncSetAttribute(k_simtopk<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -379,9 +601,10 @@ cudaError_t simtopk_init() {
 // (R * N <= cand_rows).  WARMUP_TILES prices a unit's start: while a fresh top-k list is filling,
 // nearly every 32-column chunk of some lane takes the insert path (P(insert) ~ 32 k / columns seen),
 // which makes the first ~8k columns of a unit epilogue-bound rather than MMA-bound.
-int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
+int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d) {
   const int64_t MT = (N + UNIT_ROWS - 1) / UNIT_ROWS;
-  const int64_t NT = (M_local + BN - 1) / BN;
+  const int64_t NT = (M_local + tile_rows(d) - 1) / tile_rows(d);
+  const double warmup = (double)WARMUP_TILES * BN / tile_rows(d);
   if (NT <= 1 || MT <= 0) return 1;
   int best = 1;
   double best_cost = 1e300;
@@ -389,7 +612,7 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
   for (int64_t R = 1; R <= rmax; ++R) {
     if (R > 1 && R * N > cand_rows) break;
     const int64_t waves = (MT * R + NUM_WORKERS - 1) / NUM_WORKERS;
-    const double cost = (double)waves * (double)((NT + R - 1) / R + WARMUP_TILES);
+    const double cost = (double)waves * ((double)((NT + R - 1) / R) + warmup);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = (int)R; }
   }
   return best;
@@ -397,11 +620,16 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows) {
 
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   const int MT = (int)((a.N + UNIT_ROWS - 1) / UNIT_ROWS);
-  const int NT = (int)((a.M_local + BN - 1) / BN);
+  const int NT = (int)((a.M_local + tile_rows(a.d) - 1) / tile_rows(a.d));
   if (MT == 0 || NT == 0) return cudaSuccess;
   const int units = MT * a.R;
   const int workers = units < NUM_WORKERS ? units : NUM_WORKERS;
   const int grid = CTAS * workers;
+  if (simtopk_uses_tmem_a(a.d)) {
+    if (a.dump) return launch_ta<8, true>(a, MT, NT, grid, st);
+    if (a.k <= 8) return launch_ta<8, false>(a, MT, NT, grid, st);
+    return launch_ta<16, false>(a, MT, NT, grid, st);
+  }
   if (a.dump) return launch_variant<8, true>(a, MT, NT, grid, st);
   if (a.k <= 8) return launch_variant<8, false>(a, MT, NT, grid, st);
   return launch_variant<16, false>(a, MT, NT, grid, st);

@@ -257,13 +257,13 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
   int R = 1;
   if (ctx->M_local > 0) {
-    R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap);
+    R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap, ctx->cfg.d);
     if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
       const int r = atoi(ov);
       if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
     }
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
-                  ctx->cand_local, nullptr};
+                  ctx->qhat, ctx->cand_local, nullptr};
     CUDA_TRY(ctx, launch_simtopk(a, st));
   } else {
     CUDA_TRY(ctx, launch_fill_sentinel(ctx->cand_local, N * k, st));
@@ -422,7 +422,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
     }
-  if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c())) {
+  if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c((int)d))) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
   }
@@ -746,7 +746,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
-                ctx->cand_local, scores_dev};
+                ctx->qhat, ctx->cand_local, scores_dev};
   CUDA_TRY(ctx, launch_simtopk(a, st));
   return PAS_OK;
 }

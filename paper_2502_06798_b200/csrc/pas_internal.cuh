@@ -77,16 +77,18 @@ struct SimTopkArgs {
   int64_t N;                      // prompts
   int64_t M_local;                // valid store rows on this rank
   int d, k, G, rank, R;           // R cache ranges per prompt tile
+  const __nv_bfloat16* qhat;      // [rows_q x d] (A-in-TMEM variant reads the prompt rows directly)
   Cand* out;                      // [R][N][k]
   float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
 };
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
-int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows);
+int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
+bool simtopk_uses_tmem_a(int d);
 size_t simtopk_smem_bytes();
 cudaError_t simtopk_init();
 int simtopk_prompt_rows();   // prompt rows per work unit (pair tile)
 int simtopk_box_q();         // TMA box rows of the prompt map
-int simtopk_box_c();         // TMA box rows of the cache map
+int simtopk_box_c(int d);    // TMA box rows of the cache map
 
 // K3 (+K4 when final): merge [S][N][k] -> [N][k]
 cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cudaStream_t st);

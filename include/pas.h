@@ -77,7 +77,9 @@ typedef struct {
   const unsigned char* nccl_id;/* PAS_NCCL_ID_BYTES from pas_nccl_unique_id on rank 0, broadcast by the
                                   caller; required iff world > 1 and pas_route_batch is to be used.
                                   NULL with world > 1 = "external transport": only the split calls
-                                  pas_route_local / pas_route_from_candidates are available. */
+                                  pas_route_local / pas_route_from_candidates are available.
+                                  Non-NULL with world == 1: a 1-rank communicator, pas_route_batch
+                                  takes the all-gather path (transport self-test). */
   uint64_t seed;               /* Philox key of the redirection / uniform-routing streams (R18) */
 } pas_config;
 

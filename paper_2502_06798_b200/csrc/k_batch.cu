@@ -81,6 +81,7 @@ __device__ __forceinline__ void warp_class_rank(const int (&v)[PER], int nC, int
 
 __global__ void __launch_bounds__(THREADS) k_cls_count(const int32_t* __restrict__ cls, int64_t N, int ntiles,
                                                        int nC, int32_t* __restrict__ counts /*[64][ntiles]*/) {
+  pdl_entry();
   __shared__ int32_t cnt[NCLS];
   if (threadIdx.x < NCLS) cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const int32_t* __restrict_
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       const DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
                                                       int32_t* __restrict__ slot) {
+  pdl_entry();
   __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp class totals, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const int32_t* __restrict_
 // Per-instance counts from the class totals (scan of the class-major counts), then offsets.
 __global__ void k_offsets(const int32_t* __restrict__ scanned, int ntiles, int64_t N, const RouteParams P,
                           DevPlan* __restrict__ plan, int32_t* __restrict__ off, int32_t* __restrict__ user_off) {
+  pdl_entry();
   if (threadIdx.x != 0) return;
   const int nC = P.mode == PAS_UNIFORM ? P.W : P.nK;
   int count[kMaxInst];
@@ -188,6 +191,7 @@ __global__ void k_offsets(const int32_t* __restrict__ scanned, int ntiles, int64
 // 4 prompts per thread (16-byte loads of instance and slot), scattered 4-byte stores.
 __global__ void k_bucket(const int32_t* __restrict__ instance, const int32_t* __restrict__ slot, int64_t N,
                          const int32_t* __restrict__ off, int32_t* __restrict__ prompts) {
+  pdl_entry();
   __shared__ int32_t soff[NCLS + 1];
   if (threadIdx.x <= NCLS) soff[threadIdx.x] = off[threadIdx.x];
   __syncthreads();
@@ -214,16 +218,16 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
   if (p.N <= 0) return cudaSuccess;
   const int ntiles = batch_tiles(p.N);
   const int nclasses = p.mode == PAS_UNIFORM ? p.W : p.nK;
-  k_cls_count<<<ntiles, THREADS, 0, st>>>(r.cls7, p.N, ntiles, nclasses, w.blk_counts);
+  launch_pdl(k_cls_count, ntiles, THREADS, 0, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
   cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, NCLS * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
-  k_cls_rank<<<ntiles, THREADS, 0, st>>>(r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot);
+  launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot);
   *launches += 2;
   if (e != cudaSuccess) return e;
-  k_offsets<<<1, 32, 0, st>>>(w.blk_off, ntiles, p.N, p, plan, w.offsets, bucket_offsets);
+  launch_pdl(k_offsets, 1, 32, 0, st, w.blk_off, ntiles, p.N, p, plan, w.offsets, bucket_offsets);
   *launches += 1;
   if (bucket_prompts) {
-    k_bucket<<<(unsigned)((p.N + 1023) / 1024), 256, 0, st>>>(instance, slot, p.N, w.offsets, bucket_prompts);
+    launch_pdl(k_bucket, (unsigned)((p.N + 1023) / 1024), 256, 0, st, instance, slot, p.N, w.offsets, bucket_prompts);
     *launches += 1;
   }
   return cudaGetLastError();

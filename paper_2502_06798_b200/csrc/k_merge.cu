@@ -66,6 +66,7 @@ __device__ __forceinline__ void merge_prompt(const Cand* __restrict__ in, int S,
 
 __global__ void __launch_bounds__(WARPS * 32) k_merge(const Cand* __restrict__ in, int S, int64_t N, int k,
                                                       Cand* __restrict__ out) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (p >= N) return;
@@ -152,6 +153,7 @@ __device__ __forceinline__ void flush_tally(const RouteParams& P, const SelectOu
 __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restrict__ in, int S,
                                                              const uint8_t* __restrict__ pflags,
                                                              const RouteParams P, SelectOut o) {
+  pdl_entry();
   __shared__ Cand res[WARPS][PAS_MAX_TOPK];
   Tally ty;
   ty.zero();
@@ -189,6 +191,7 @@ constexpr int TP_MAXSK = 32;
 __global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __restrict__ in, int S,
                                                                  const uint8_t* __restrict__ pflags,
                                                                  const RouteParams P, SelectOut o) {
+  pdl_entry();
   extern __shared__ __align__(16) Cand sm[];   // S * 128 * (k + 1) pairs (dynamic, padded rows)
   // after the merge the staging buffer is reused for the outgoing ids and scores (rows padded to k+1
   // words so the per-thread rows fall in different banks)
@@ -273,6 +276,7 @@ template <int HALF>
 __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict__ in,
                                                           const uint8_t* __restrict__ pflags, const RouteParams P,
                                                           SelectOut o) {
+  pdl_entry();
   Tally ty;
   ty.zero();
   constexpr uint32_t half = HALF;
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict
 }
 
 __global__ void k_fill_sentinel(Cand* out, int64_t n) {
+  pdl_entry();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = Cand{-INFINITY, -1};
 }
@@ -307,7 +312,7 @@ __global__ void k_fill_sentinel(Cand* out, int64_t n) {
 cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cudaStream_t st) {
   if (N <= 0) return cudaSuccess;
   const int64_t blocks = (N + WARPS - 1) / WARPS;
-  k_merge<<<(unsigned)blocks, WARPS * 32, 0, st>>>(in, S, N, k, out);
+  launch_pdl(k_merge, (unsigned)blocks, WARPS * 32, 0, st, in, S, N, k, out);
   return cudaGetLastError();
 }
 
@@ -321,24 +326,24 @@ cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, co
     const unsigned g = (unsigned)blocks;
     const int4* in4 = reinterpret_cast<const int4*>(in);
     switch (p.topk >> 1) {
-      case 1: k_select_s1<1><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 2: k_select_s1<2><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 3: k_select_s1<3><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 4: k_select_s1<4><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 5: k_select_s1<5><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 6: k_select_s1<6><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      case 7: k_select_s1<7><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
-      default: k_select_s1<8><<<g, S1_THREADS, 0, st>>>(in4, pflags, p, o); break;
+      case 1: launch_pdl(k_select_s1<1>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 2: launch_pdl(k_select_s1<2>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 3: launch_pdl(k_select_s1<3>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 4: launch_pdl(k_select_s1<4>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 5: launch_pdl(k_select_s1<5>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 6: launch_pdl(k_select_s1<6>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      case 7: launch_pdl(k_select_s1<7>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
+      default: launch_pdl(k_select_s1<8>, g, S1_THREADS, 0, st, in4, pflags, p, o); break;
     }
   } else if (S <= 4 && S * p.topk <= TP_MAXSK) {
     int64_t blocks = (p.N + TP_THREADS - 1) / TP_THREADS;
     if (blocks > (int64_t)kNumSMs * 8) blocks = (int64_t)kNumSMs * 8;   // persistent CTAs
     // staging for S lists in, and ids + scores (= 1 list of pairs) out, rows padded to k+1 pairs
     const size_t smem = (size_t)(S > 1 ? S : 1) * TP_THREADS * (p.topk + 1) * sizeof(Cand);
-    k_merge_select_thr<<<(unsigned)blocks, TP_THREADS, smem, st>>>(in, S, pflags, p, o);
+    launch_pdl(k_merge_select_thr, (unsigned)blocks, TP_THREADS, smem, st, in, S, pflags, p, o);
   } else {
     const int64_t blocks = (p.N + WARPS - 1) / WARPS;
-    k_merge_select<<<(unsigned)blocks, WARPS * 32, 0, st>>>(in, S, pflags, p, o);
+    launch_pdl(k_merge_select, (unsigned)blocks, WARPS * 32, 0, st, in, S, pflags, p, o);
   }
   return cudaGetLastError();
 }
@@ -347,7 +352,7 @@ cudaError_t launch_fill_sentinel(Cand* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4096) blocks = 4096;
-  k_fill_sentinel<<<(unsigned)blocks, 256, 0, st>>>(out, n);
+  launch_pdl(k_fill_sentinel, (unsigned)blocks, 256, 0, st, out, n);
   return cudaGetLastError();
 }
 

@@ -61,6 +61,7 @@ template <typename T, int VEC>
 __global__ void __launch_bounds__(256, 3) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count) {
+  pdl_entry();
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -133,15 +134,15 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
   if (blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
   switch (vec) {
-    case 1: k_normalize<T, 1><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 2: k_normalize<T, 2><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 3: k_normalize<T, 3><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 4: k_normalize<T, 4><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 5: k_normalize<T, 5><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 6: k_normalize<T, 6><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 7: k_normalize<T, 7><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 8: k_normalize<T, 8><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    default: k_normalize<T, 0><<<g, threads, 0, st>>>(in, rows, d, out, flags, first_gid, G, rank, invalid_count);
+    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
+    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count);
   }
   return cudaGetLastError();
 }

@@ -1,4 +1,4 @@
-// K5 -- Eq. 1 K->K' route plan for one batch, solved in one CTA.
+// K5 -- Eq. 1 K->K' route plan for one batch, solved by one warp.
 //
 // Paper (PAPER.md P:88-P:96): the Query Fraction Solver gives F(K); the K-to-K' Route Planner finds
 // redirection probabilities P(K'_j|K_i) minimising
@@ -13,119 +13,127 @@
 // strictly convex tie-break, so NW-corner IS the lexicographic optimum; the oracle checks this
 // against exhaustive search and an LP (tests/test_oracle_plan.py, tests/test_gpu_*).
 //
-// nK <= 16: one thread does the arithmetic (fp64 with explicit _rn intrinsics, no FMA contraction,
-// so f is bit-identical to the CPU).  Also builds the row prefix tables X, the class starts, the
-// per-level instance lists I_j (ascending ids) and the redirect counters.
+// One warp, no serial loops over the plan: the NW-corner coupling has the closed form
+//     x_ij = max(0, min(Hc_i, Fc_j) - max(Hc_{i-1}, Fc_{j-1}))       (Hc, Fc cumulative sums),
+// the overlap of prompt-rank intervals, so each of the nK^2 <= 256 entries is computed independently.
+// Largest remainder: f_j = floor(N F_j) + [rank of frac_j among the levels (desc, ties -> lower
+// index) < R].  fp64 with explicit _rn intrinsics (no FMA contraction): f is bit-identical to the
+// CPU.  Also: row prefix tables X, class starts, the per-level instance lists I_j (ascending ids) with
+// their multiply-high division constants, redirect counters, D_Q and D_Q_LP (fixed reduction order).
 #include "pas_internal.cuh"
 
 namespace pas {
 namespace {
 
-__global__ void k_plan(const int* __restrict__ hist, const RouteParams P, DevPlan* __restrict__ plan) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(32) k_plan(const int* __restrict__ hist, const RouteParams P,
+                                             DevPlan* __restrict__ plan) {
+  pdl_entry();
+  __shared__ int h_s[kMaxLevels], f_s[kMaxLevels], hc[kMaxLevels + 1], fc[kMaxLevels + 1];
+  __shared__ double frac_s[kMaxLevels];
+  const int lane = threadIdx.x;
   const int nK = P.nK;
   const int N = (int)P.N;
-  int h[kMaxLevels], f[kMaxLevels];
-  for (int i = 0; i < nK; ++i) h[i] = hist[i];
   // ---- O5 largest remainder apportionment of N*F
-  double frac[kMaxLevels];
-  int sumf = 0;
-  for (int j = 0; j < nK; ++j) {
-    const double q = __dmul_rn((double)N, P.F[j]);
-    const double fl = floor(q);
-    f[j] = (int)fl;
-    frac[j] = __dsub_rn(q, fl);
-    sumf += f[j];
+  int fl = 0;
+  double frac = -1.0;
+  if (lane < nK) {
+    h_s[lane] = hist[lane];
+    const double q = __dmul_rn((double)N, P.F[lane]);
+    const double f0 = floor(q);
+    fl = (int)f0;
+    frac = __dsub_rn(q, f0);
+    frac_s[lane] = frac;
   }
-  int R = N - sumf;
-  bool used[kMaxLevels];
-  for (int j = 0; j < nK; ++j) used[j] = false;
-  for (int r = 0; r < R; ++r) {
-    int best = -1;
-    for (int j = 0; j < nK; ++j)
-      if (!used[j] && (best < 0 || frac[j] > frac[best])) best = j;   // ties -> lower index
-    used[best] = true;
-    f[best] += 1;
+  const int R = N - warp_sum(lane < nK ? fl : 0);
+  __syncwarp();
+  if (lane < nK) {
+    int rank = 0;
+    for (int j = 0; j < nK; ++j) rank += (frac_s[j] > frac || (frac_s[j] == frac && j < lane)) ? 1 : 0;
+    f_s[lane] = fl + (rank < R ? 1 : 0);
   }
-  // ---- O6 north-west-corner integer transport (monotone coupling)
-  int x[kMaxLevels][kMaxLevels];
-  for (int i = 0; i < nK; ++i)
-    for (int j = 0; j < nK; ++j) x[i][j] = 0;
-  {
-    int rem_r[kMaxLevels], rem_c[kMaxLevels];
-    for (int i = 0; i < nK; ++i) { rem_r[i] = h[i]; rem_c[i] = f[i]; }
-    int i = 0, j = 0;
-    while (i < nK && j < nK) {
-      if (rem_r[i] == 0) { ++i; continue; }
-      if (rem_c[j] == 0) { ++j; continue; }
-      const int t = rem_r[i] < rem_c[j] ? rem_r[i] : rem_c[j];
-      x[i][j] += t;
-      rem_r[i] -= t;
-      rem_c[j] -= t;
+  __syncwarp();
+  if (lane == 0) {   // cumulative sums (<= 16 terms)
+    hc[0] = 0;
+    fc[0] = 0;
+    for (int i = 0; i < nK; ++i) {
+      hc[i + 1] = hc[i] + h_s[i];
+      fc[i + 1] = fc[i] + f_s[i];
     }
   }
-  // ---- O7 D_Q (Eq. 1 on counts), in (i, j) order
-  double dq = 0.0;
+  __syncwarp();
+  // ---- O6 NW-corner coupling in closed form, O7 D_Q and counters
+  double dq = 0.0, lp = 0.0;
   int n_red = 0, n_up = 0, n_down = 0;
-  for (int i = 0; i < nK; ++i)
-    for (int j = 0; j < nK; ++j) {
-      if (j != i) n_red += x[i][j];
-      if (j < i) n_up += x[i][j];
-      if (j > i) {
-        n_down += x[i][j];
-        dq = __dadd_rn(dq, __dmul_rn((double)x[i][j], P.c[P.grid[j] - P.grid[i]]));
-      }
+  const double invN = N > 0 ? __ddiv_rn(1.0, (double)N) : 0.0;
+  for (int e = lane; e < nK * nK; e += 32) {
+    const int i = e / nK, j = e % nK;
+    const int lo = max(hc[i], fc[j]), hi = min(hc[i + 1], fc[j + 1]);
+    const int x = hi > lo ? hi - lo : 0;
+    plan->x[i][j] = x;
+    if (j != i) n_red += x;
+    if (j < i) n_up += x;
+    if (j > i) {
+      n_down += x;
+      dq = __dadd_rn(dq, __dmul_rn((double)x, P.c[P.grid[j] - P.grid[i]]));
     }
-  plan->D_Q = N > 0 ? __ddiv_rn(dq, (double)N) : 0.0;
-  // ---- D_Q_LP: same monotone coupling on the unrounded masses (h/N, F), context only
-  {
-    double rr[kMaxLevels], rc[kMaxLevels];
-    for (int i = 0; i < nK; ++i) { rr[i] = N > 0 ? __ddiv_rn((double)h[i], (double)N) : 0.0; rc[i] = P.F[i]; }
-    int i = 0, j = 0;
-    double lp = 0.0;
-    while (i < nK && j < nK) {
-      if (rr[i] <= 1e-15) { ++i; continue; }
-      if (rc[j] <= 1e-15) { ++j; continue; }
-      const double t = rr[i] < rc[j] ? rr[i] : rc[j];
-      if (j > i) lp = __dadd_rn(lp, __dmul_rn(t, P.c[P.grid[j] - P.grid[i]]));
-      rr[i] = __dsub_rn(rr[i], t);
-      rc[j] = __dsub_rn(rc[j], t);
-    }
-    plan->D_Q_LP = lp;
+    // D_Q_LP: the same monotone coupling on the unrounded masses (h/N, F), context only
+    double hlo = __dmul_rn((double)hc[i], invN), hhi = __dmul_rn((double)hc[i + 1], invN);
+    double flo = 0.0, fhi = 0.0;
+    for (int jj = 0; jj < j; ++jj) flo = __dadd_rn(flo, P.F[jj]);
+    fhi = __dadd_rn(flo, P.F[j]);
+    const double ov = fmin(hhi, fhi) - fmax(hlo, flo);
+    if (j > i && ov > 0) lp = __dadd_rn(lp, __dmul_rn(ov, P.c[P.grid[j] - P.grid[i]]));
   }
-  int cs = 0;
-  for (int i = 0; i < nK; ++i) {
-    plan->h[i] = h[i];
-    plan->f[i] = f[i];
-    plan->class_start[i] = cs;
-    cs += h[i];
+  dq = warp_sum_fixed(dq);
+  lp = warp_sum_fixed(lp);
+  n_red = warp_sum(n_red);
+  n_up = warp_sum(n_up);
+  n_down = warp_sum(n_down);
+  __syncwarp();
+  if (lane < nK) {   // row prefix tables and class starts
+    const int i = lane;
+    plan->h[i] = h_s[i];
+    plan->f[i] = f_s[i];
+    plan->class_start[i] = hc[i];
     int acc = 0;
     for (int j = 0; j < nK; ++j) {
-      plan->x[i][j] = x[i][j];
-      acc += x[i][j];
+      const int lo = max(hc[i], fc[j]), hi = min(hc[i + 1], fc[j + 1]);
+      acc += hi > lo ? hi - lo : 0;
       plan->X[i][j] = acc;
     }
+    // I_j: ascending instance ids at level j, and the multiply-high constant for div n_j
+    int n = 0;
+    for (int w = 0; w < P.W; ++w)
+      if (P.inst_level[w] == i) plan->inst_list[i][n++] = w;
+    plan->n_inst[i] = n;
+    const uint64_t d = n > 0 ? (uint64_t)n : 1;
+    plan->n_inst_magic[i] = ((1ull << 32) + d - 1) / d;
   }
-  plan->class_start[nK] = cs;
-  plan->n_redirected = n_red;
-  plan->n_upgraded = n_up;
-  plan->n_downgraded = n_down;
-  // ---- I_j: ascending instance ids per level
-  for (int j = 0; j < nK; ++j) plan->n_inst[j] = 0;
-  for (int w = 0; w < P.W; ++w) {
-    const int j = P.inst_level[w];
-    plan->inst_list[j][plan->n_inst[j]++] = w;
-  }
-  for (int j = 0; j < nK; ++j) {
-    const uint64_t d = plan->n_inst[j] > 0 ? (uint64_t)plan->n_inst[j] : 1;
-    plan->n_inst_magic[j] = ((1ull << 32) + d - 1) / d;
+  if (lane == 0) {
+    plan->class_start[nK] = hc[nK];
+    plan->D_Q = N > 0 ? __ddiv_rn(dq, (double)N) : 0.0;
+    plan->D_Q_LP = lp;
+    plan->n_redirected = n_red;
+    plan->n_upgraded = n_up;
+    plan->n_downgraded = n_down;
   }
 }
 
 }  // namespace
 
 cudaError_t launch_plan(const int* hist, const RouteParams& p, DevPlan* plan, cudaStream_t st) {
-  k_plan<<<1, 32, 0, st>>>(hist, p, plan);
+  launch_pdl(k_plan, 1, 32, 0, st, hist, p, plan);
   return cudaGetLastError();
 }
 

@@ -21,6 +21,7 @@ namespace {
 
 __global__ void k_keys(const uint8_t* __restrict__ level, RouteParams P, uint64_t* __restrict__ key,
                        int32_t* __restrict__ bucket, int32_t* __restrict__ bcount) {
+  pdl_entry();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P.N) return;
   const uint4 w = philox_stream(P.seed, P.batch_seq, (uint32_t)p, kStreamRedirect);
@@ -36,6 +37,7 @@ __global__ void k_keys(const uint8_t* __restrict__ level, RouteParams P, uint64_
 __global__ void k_scatter(const uint64_t* __restrict__ key, const int32_t* __restrict__ bucket, int64_t N,
                           const int32_t* __restrict__ bstart, int32_t* __restrict__ bfill,
                           KeyEntry* __restrict__ sorted) {
+  pdl_entry();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= N) return;
   const int b = bucket[p];
@@ -47,6 +49,7 @@ __global__ void k_scatter(const uint64_t* __restrict__ key, const int32_t* __res
 __global__ void k_rank(const KeyEntry* __restrict__ sorted, RouteParams P, const DevPlan* __restrict__ plan,
                        const int32_t* __restrict__ bcount, const int32_t* __restrict__ bstart,
                        int32_t* __restrict__ cls7, int32_t* __restrict__ K_prime) {
+  pdl_entry();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.N) return;
   const KeyEntry e = sorted[i];
@@ -79,13 +82,13 @@ cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const De
   if (p.N <= 0) return cudaSuccess;
   const int nb = p.nK << p.kb;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(w.bcount, 0, sizeof(int32_t) * nb, st))) return e;
-  if ((e = cudaMemsetAsync(w.bfill, 0, sizeof(int32_t) * nb, st))) return e;
+  if ((e = launch_zero(w.bcount, nb, w.bfill, nb, nullptr, 0, st))) return e;
+  *launches += 1;
   const unsigned blocks = (unsigned)((p.N + 255) / 256);
-  k_keys<<<blocks, 256, 0, st>>>(level, p, w.key, w.bucket, w.bcount);
+  launch_pdl(k_keys, blocks, 256, 0, st, level, p, w.key, w.bucket, w.bcount);
   if ((e = launch_exclusive_scan(w.bcount, w.bstart, nb, w.scan_tmp, st, launches))) return e;
-  k_scatter<<<blocks, 256, 0, st>>>(w.key, w.bucket, p.N, w.bstart, w.bfill, w.sorted);
-  k_rank<<<blocks, 256, 0, st>>>(w.sorted, p, plan, w.bcount, w.bstart, w.cls7, K_prime);
+  launch_pdl(k_scatter, blocks, 256, 0, st, w.key, w.bucket, p.N, w.bstart, w.bfill, w.sorted);
+  launch_pdl(k_rank, blocks, 256, 0, st, w.sorted, p, plan, w.bcount, w.bstart, w.cls7, K_prime);
   *launches += 3;
   return cudaGetLastError();
 }

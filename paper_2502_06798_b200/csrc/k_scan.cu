@@ -50,6 +50,7 @@ __device__ __forceinline__ void load_tile(const int32_t* in, int n, int i0, int 
 
 __global__ void __launch_bounds__(THREADS) k_scan_small(const int32_t* __restrict__ in, int32_t* __restrict__ out,
                                                         int n) {
+  pdl_entry();
   __shared__ int wsum[32];
   int carry = 0;
   for (int base = 0; base < n; base += TILE) {
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(THREADS) k_scan_small(const int32_t* __restric
 
 __global__ void __launch_bounds__(THREADS) k_tile_sum(const int32_t* __restrict__ in, int n,
                                                       int32_t* __restrict__ sums) {
+  pdl_entry();
   __shared__ int wsum[32];
   const int i0 = blockIdx.x * TILE + 4 * threadIdx.x;
   int v[4];
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sum(const int32_t* __restrict_
 
 __global__ void __launch_bounds__(THREADS) k_tile_scan(const int32_t* __restrict__ in, int n,
                                                        const int32_t* __restrict__ prefix, int32_t* __restrict__ out) {
+  pdl_entry();
   __shared__ int wsum[32];
   const int i0 = blockIdx.x * TILE + 4 * threadIdx.x;
   int v[4];
@@ -93,7 +96,25 @@ __global__ void __launch_bounds__(THREADS) k_tile_scan(const int32_t* __restrict
   }
 }
 
+__global__ void k_zero(int32_t* a, int64_t na, int32_t* b, int64_t nb, int32_t* c, int64_t nc) {
+  pdl_entry();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb + nc; i += stride) {
+    if (i < na) a[i] = 0;
+    else if (i < na + nb) b[i - na] = 0;
+    else c[i - na - nb] = 0;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_zero(int32_t* a, int64_t na, int32_t* b, int64_t nb, int32_t* c, int64_t nc, cudaStream_t st) {
+  const int64_t n = na + nb + nc;
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  return launch_pdl(k_zero, (unsigned)blocks, 256, 0, st, a, na, b, nb, c, nc);
+}
 
 int scan_tmp_ints(int64_t n) { return (int)((n + TILE - 1) / TILE) + 1; }
 
@@ -101,14 +122,14 @@ cudaError_t launch_exclusive_scan(const int32_t* in, int32_t* out, int n, int32_
                                   int* launches) {
   if (n <= 0) return cudaSuccess;
   if (n <= 4 * TILE) {
-    k_scan_small<<<1, THREADS, 0, st>>>(in, out, n);
+    launch_pdl(k_scan_small, 1, THREADS, 0, st, in, out, n);
     *launches += 1;
     return cudaGetLastError();
   }
   const int tiles = (n + TILE - 1) / TILE;
-  k_tile_sum<<<tiles, THREADS, 0, st>>>(in, n, tmp);
-  k_scan_small<<<1, THREADS, 0, st>>>(tmp, tmp, tiles);   // in-place is safe: each element read before written
-  k_tile_scan<<<tiles, THREADS, 0, st>>>(in, n, tmp, out);
+  launch_pdl(k_tile_sum, tiles, THREADS, 0, st, in, n, tmp);
+  launch_pdl(k_scan_small, 1, THREADS, 0, st, tmp, tmp, tiles);   // in-place is safe: each element read before written
+  launch_pdl(k_tile_scan, tiles, THREADS, 0, st, in, n, tmp, out);
   *launches += 3;
   return cudaGetLastError();
 }

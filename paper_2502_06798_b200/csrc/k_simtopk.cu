@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (PAIR) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
+  pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
+  pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
 
   if (warp == 0) {
     // ------------------------------- TMA producer (B only) ---------------------------
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 template <int KMAX, bool DUMP>
 cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
-  k_simtopk_ta<KMAX, DUMP><<<grid, NUM_THREADS, TA_SMEM_BYTES, st>>>(*a.tmap_c, a.qhat, a.N, a.M_local, a.d, a.k, a.G,
+  launch_pdl(k_simtopk_ta<KMAX, DUMP>, grid, NUM_THREADS, TA_SMEM_BYTES, st, *a.tmap_c, a.qhat, a.N, a.M_local, a.d, a.k, a.G,
                                                                      a.rank, a.R, MT, NT, a.out, a.dump);
   return cudaGetLastError();
 }
@@ -562,13 +564,15 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaS
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CTAS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CTAS;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = PAIR ? 1 : 0;
+  cfg.numAttrs = PAIR ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP>, *a.tmap_q, *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
                             a.rank, a.R, MT, NT, a.out, a.dump);
 }

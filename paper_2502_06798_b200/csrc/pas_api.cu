@@ -240,7 +240,8 @@ pas_status ensure_prompt_ws(pas_ctx* ctx) {
   if (e == cudaSuccess) e = dmalloc(&ctx->pflags, (size_t)mb);
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_local, (size_t)(ctx->cand_cap * k));
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_rank, (size_t)(mb * k));
-  if (e == cudaSuccess && ctx->cfg.world > 1) e = dmalloc(&ctx->cand_all, (size_t)((int64_t)ctx->cfg.world * mb * k));
+  if (e == cudaSuccess && (ctx->cfg.world > 1 || ctx->comm))
+    e = dmalloc(&ctx->cand_all, (size_t)((int64_t)ctx->cfg.world * mb * k));
   if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "prompt workspace allocation failed: %s", cudaGetErrorString(e));
   if (!encode_map(&ctx->tm_q, ctx->qhat, ctx->q_rows, (int)d, simtopk_box_q()))
     return fail(ctx, PAS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the prompt map");
@@ -285,8 +286,10 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
 // a4 (final merge) .. a8 for all N prompts from S candidate blocks [S][N][k].
 pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
   RouteParams p = make_params(ctx, N);
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->hist, 0, sizeof(int) * kMaxLevels, st));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->plan, 0, sizeof(DevPlan), st));
+  static_assert(sizeof(DevPlan) % 4 == 0, "DevPlan zeroed as int32 words");
+  CUDA_TRY(ctx, launch_zero(ctx->hist, kMaxLevels, reinterpret_cast<int32_t*>(ctx->plan), sizeof(DevPlan) / 4,
+                            nullptr, 0, st));
+  ctx->launches++;
   SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
   const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;   // else: all prompts valid
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
@@ -382,7 +385,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->cfg.nccl_id = nullptr;
   ctx->seed = cfg->seed;
   for (int t = 0; t < kTTotal; ++t) ctx->c[t] = 0.006 * t;   // SPEC S:49 default, R6
-  const int64_t mb = cfg->max_batch, k = cfg->topk, d = cfg->d;
+  const int64_t mb = cfg->max_batch, d = cfg->d;
   const int64_t qt = simtopk_prompt_rows();
   ctx->q_rows = (mb + qt - 1) / qt * qt;
   ctx->cap_rows = cfg->max_rows_per_rank;
@@ -430,7 +433,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(e));
   }
-  if (cfg->world > 1 && cfg->nccl_id) {
+  if (cfg->nccl_id) {   // world == 1 with an id: a 1-rank communicator (exercises the collective path)
     if (!nccl_load()) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_NCCL, "cannot load libnccl.so.2");
@@ -631,7 +634,7 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
   const Cand* cand;
   int S;
-  if (G == 1) {
+  if (!ctx->comm) {
     if ((s = run_local(ctx, emb, dtype, N, st, &cand, &S, nullptr))) return s;
   } else {
     if ((s = run_local(ctx, emb, dtype, N, st, &cand, &S, ctx->cand_rank))) return s;

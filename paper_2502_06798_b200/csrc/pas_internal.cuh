@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/pas.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
@@ -16,6 +18,34 @@
 #endif
 
 namespace pas {
+
+// Programmatic dependent launch: every kernel of the batch pipeline is launched with
+// programmatic stream serialization and starts with pdl_entry(), which lets the NEXT kernel be
+// scheduled immediately (its launch latency hides behind this one) and then waits until the
+// PREVIOUS kernel has completed and its writes are visible.  Outside PDL both are no-ops.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// zero up to three int32 buffers in one launch
+cudaError_t launch_zero(int32_t* a, int64_t na, int32_t* b, int64_t nb, int32_t* c, int64_t nc, cudaStream_t st);
 
 constexpr int kMaxLevels = PAS_MAX_LEVELS;
 constexpr int kMaxInst = PAS_MAX_INSTANCES;

@@ -397,3 +397,25 @@ def test_many_instances(pas, mode):
     cfg = CONFIGS["C2"]
     inst = [i % 6 for i in range(40)]
     _full_parity(pas, cfg, N=2000, M=5000, instance_level=inst, mode=mode, bstar=1 if mode else 3)
+
+
+def test_nccl_collective_path_single_rank(pas):
+    """The world > 1 data path through real NCCL: a 1-rank communicator makes pas_route_batch run
+    local merge -> ncclAllGather -> S = G merge; the result is byte-identical to the direct path."""
+    cfg = CONFIGS["C2"]
+    N, M = 600, 7000
+    w = Workload(cfg, device=DEV, M=M)
+    C_ = w.cache_rows(0, M).contiguous()
+    P = w.prompts(N)
+    ref, _ = _small(pas, C_, P, name="C2")
+    nid = pas.pas_nccl_unique_id()
+    r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M, device=0, world=1, nccl_id=nid,
+                   seed=cfg.route_seed)
+    r.set_bands(cfg.grid, cfg.thresholds)
+    r.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
+    r.load_cache(C_)
+    got = _host(r.route(P))
+    torch.cuda.synchronize()
+    for key in ("K", "K_prime", "instance", "slot", "topk_id", "topk_score", "bucket_prompts"):
+        assert np.array_equal(got[key], ref[key]), key
+    r.close()

@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample-prompts", type=int, default=32)
+    ap.add_argument("--force-collective", action="store_true",
+                    help="use the NCCL all-gather path even with one rank (transport self-test)")
     return ap.parse_args()
 
 
@@ -185,14 +187,17 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_collective:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     from paper_2502_06798_b200 import dist as pdist
     from paper_2502_06798_b200 import pas
 
-    nccl_id = pdist.bootstrap_nccl_id(rank) if world > 1 else None
+    nccl_id = pdist.bootstrap_nccl_id(rank) if (world > 1 or args.force_collective) else None
     G = world
     M_local = max(1, pdist.shard_rows(M, G, rank))
     router = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M_local, device=local,

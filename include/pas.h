@@ -58,6 +58,7 @@ typedef enum { PAS_GREEDY = 0, PAS_UNIFORM = 1 } pas_mode;  /* P:104 high / low 
 #define PAS_MAX_LEVELS 16        /* nK <= 16 (configs use 6 and 10) */
 #define PAS_MAX_INSTANCES 64     /* W <= 64 serving instances */
 #define PAS_T_TOTAL 50           /* total denoising steps */
+#define PAS_MAX_FORECAST_WINDOW (1 << 22)   /* f1 predictor window (paper: 1000) */
 #define PAS_MAX_TOPK 16
 #define PAS_NCCL_ID_BYTES 128
 
@@ -112,6 +113,18 @@ typedef struct {
   float stage_ms[8];    /* device ms per stage of the last batch: [0] normalise, [1] similarity+top-k,
                            [2] merge + collective + optimal-K/H_K, [3] plan, [4] redirect,
                            [5] route-and-batch, [6] total, [7] unused */
+  /* forecast-driven mode (pas_set_forecast; all zero in the exact mode).  There, f and x are the
+   * REALISED K' counts and moves, D_Q the realised sum_p D(K'_p, K_p) / N, and D_Q_LP the Eq. 1 value
+   * of the fixed-point plan the batch was routed with (R22). */
+  int forecast;                                 /* 1 if the last batch ran in forecast mode */
+  int fc_replanned;                             /* the plan was rebuilt for this batch (R24) */
+  int64_t fc_plan_n;                            /* window length the plan was built from (0: uniform) */
+  int64_t fc_plan_counts[PAS_MAX_LEVELS];       /* window level counts the plan was built from */
+  int64_t fc_window_n;                          /* window length after this batch */
+  double fc_l2_error;                           /* |forecast H_K - realised h/N|_2 */
+  int64_t n_unforecast;                         /* prompts of a level the forecast gave no mass (R23) */
+  uint64_t fc_Hc[PAS_MAX_LEVELS + 1];           /* cumulative forecast mass, units of 2^-32 */
+  uint64_t fc_Fc[PAS_MAX_LEVELS + 1];           /* cumulative F, units of 2^-32 */
 } pas_stats;
 
 /* Library and build identification ("sm_100a", version). Never fails. */
@@ -165,6 +178,18 @@ pas_status pas_set_degradation(pas_ctx* ctx, const double* c_of_dK, int len);
  * Errors: PAS_ERR_STATE, PAS_ERR_FRACTIONS, PAS_ERR_NO_INSTANCE, PAS_ERR_ARG. */
 pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* instance_level, int W,
                              int bstar, pas_mode mode);
+
+/* NEXT f1, forecast-driven streaming mode (R21-R24).
+ * window > 0: from the next batch on, the Optimal-K Predictor is a ring buffer of the last `window`
+ * optimal-K levels (fed with every routed batch, prompt order; empty = uniform forecast), the Route-
+ * Plan P(K'|K) is the Eq. 1 optimum (monotone coupling, 2^-32 fixed point) of that forecast and F,
+ * rebuilt every `replan_every`-th batch and whenever F changed, and every prompt draws its K' i.i.d.
+ * from its plan row (Philox stream 3) instead of the exact per-batch integer plan.  Route-and-batch,
+ * outputs and buckets are unchanged.  window == 0 returns to the exact mode.  Resets the window
+ * (also reset by pas_set_bands).  Synchronises the device.  Requires pas_set_bands for window > 0.
+ * Errors: PAS_ERR_ARG (window outside [0, PAS_MAX_FORECAST_WINDOW], replan_every < 1), PAS_ERR_STATE,
+ * PAS_ERR_CUDA. */
+pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every);
 
 /* Reset the Philox key and the batch sequence number (R18). */
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);

@@ -8,119 +8,94 @@
 // Uniform (low load, R14): instance chosen by Philox in K6; slot = FIFO rank among the prompts of that
 //   instance (batch size 1).
 // Both need the stable rank t of every prompt among the prompts of its class (C classes: the nK <= 16
-// K' levels in greedy mode, the W <= 64 instances in uniform mode) in prompt order.  Tiles of 1024
-// prompts, 4 consecutive prompts per thread (16-byte loads and stores, no shared-memory staging):
-//   k_cls_count  per-tile class counts, written class-major [64][tiles]
+// K' levels in greedy mode, the W <= 64 instances in uniform mode) in prompt order.  The class is a
+// byte per prompt.  Tiles of 4096 prompts; each warp takes 512 consecutive prompts as ROWS = 16 rows
+// of 32 (lane l of row j holds prompt 32 j + l; coalesced loads, all 16 in flight before any compute):
+//   k_cls_count  per-tile class counts, written class-major [C][tiles]
 //   scan         device-wide exclusive scan of that array: entry (c, b) = prompts of classes < c plus
 //                prompts of class c in tiles < b
-//   k_cls_rank   t = scan(c, b) - scan(c, 0) + rank inside the tile: per warp, one ballot per class and
-//                element slot (popc of the lanes below), per block an exclusive prefix over the 8 warps.
-//   k_offsets    per-instance counts in closed form from the class totals (greedy: each I_j[m] gets
-//                the t's whose (t div b*) mod n_j = m), their exclusive scan (the batch-list offsets)
+//   k_cls_rank   t = scan(c, b) - scan(c, 0) + rank inside the tile.  Inside a warp, row by row:
+//                match.any gives the lanes holding the same class, popc of those below a lane is its
+//                rank in the row, and a per-warp running count per class (shared memory, bumped by the
+//                lowest lane of each match group) carries the earlier rows; per block an exclusive
+//                prefix over the 8 warps.  Cost per row is independent of C.  Block 0 also turns the
+//                class totals into per-instance counts (closed form, greedy: each I_j[m] gets the t's
+//                whose (t div b*) mod n_j = m) and the batch-list offsets.
 //   k_bucket     scatter prompt ids to offsets[instance] + slot.
-// HBM per prompt: class 4 B read twice, instance + slot 8 B written, bucket list 8 B read + 4 B written.
+// (A single-pass decoupled look-back variant was 60 % slower at 64M prompts: with ~1200 tiles in
+// flight the look-back walks hundreds of predecessors per tile.)
+// HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 8 B read + 4 B written.
 #include "pas_internal.cuh"
 
 namespace pas {
 namespace {
 
 constexpr int THREADS = 256;
-constexpr int PER = 4;                   // prompts per thread
-constexpr int TILE = THREADS * PER;      // prompts per CTA
-constexpr int NCLS = 64;
 constexpr int WARPS = THREADS / 32;
+constexpr int ROWS = 16;                       // rows of 32 prompts per warp
+constexpr int TILE = THREADS * ROWS;           // prompts per CTA
+constexpr int NCLS = 64;
 
-__device__ __forceinline__ void load4(const int32_t* __restrict__ src, int64_t base, int n, int (&v)[PER]) {
-  const int i0 = PER * threadIdx.x;
-  if (i0 + PER - 1 < n) {
-    const int4 x = __ldg(reinterpret_cast<const int4*>(src + base) + threadIdx.x);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-  } else {
-#pragma unroll
-    for (int j = 0; j < PER; ++j) v[j] = (i0 + j < n) ? src[base + i0 + j] : -1;
-  }
-}
-__device__ __forceinline__ void store4(int32_t* __restrict__ dst, int64_t base, int n, const int (&v)[PER]) {
-  const int i0 = PER * threadIdx.x;
-  if (i0 + PER - 1 < n) {
-    reinterpret_cast<int4*>(dst + base)[threadIdx.x] = make_int4(v[0], v[1], v[2], v[3]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (i0 + j < n) dst[base + i0 + j] = v[j];
-  }
-}
-
-// Warp-level class ranking by ballots (uniform loop over the C <= 64 classes): for an element of
-// class c held by lane l at position j of its 4, the number of earlier class-c elements in the warp
-// is  sum_k popc(ballot_k(class == c) & lanes_below(l))  +  #{k < j : v[k] == c}.  Lane (c mod 32)
-// ends with the warp's total of class c in lane_total[c / 32].
-__device__ __forceinline__ void warp_class_rank(const int (&v)[PER], int nC, int (&r)[PER], int (&lane_total)[2]) {
+// Row j of this warp's chunk: prompt base + 32 j + lane (-1 past the end).
+__device__ __forceinline__ void load_rows(const uint8_t* __restrict__ src, int64_t base, int64_t N, int (&v)[ROWS]) {
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1;
 #pragma unroll
-  for (int j = 0; j < PER; ++j) r[j] = 0;
-  lane_total[0] = lane_total[1] = 0;
-  for (int c = 0; c < nC; ++c) {
-    int before = 0, tot = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const unsigned b = __ballot_sync(0xffffffffu, v[j] == c);
-      before += __popc(b & lt);
-      tot += __popc(b);
-    }
-    int mine = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      if (v[j] == c) r[j] = before + mine;
-      mine += (v[j] == c) ? 1 : 0;
-    }
-    if (lane == (c & 31)) lane_total[c >> 5] = tot;
+  for (int j = 0; j < ROWS; ++j) {
+    const int64_t p = base + 32 * j + lane;
+    v[j] = p < N ? (int)__ldg(src + p) : -1;
   }
 }
 
-__global__ void __launch_bounds__(THREADS) k_cls_count(const int32_t* __restrict__ cls, int64_t N, int ntiles,
-                                                       int nC, int32_t* __restrict__ counts /*[64][ntiles]*/) {
+__global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict__ cls, int64_t N, int ntiles,
+                                                       int nC, int32_t* __restrict__ counts /*[nC][ntiles]*/) {
   pdl_entry();
   __shared__ int32_t cnt[NCLS];
   if (threadIdx.x < NCLS) cnt[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * TILE;
-  const int n = (int)min((int64_t)TILE, N - base);
-  int v[PER];
-  load4(cls, base, n, v);
-  const int lane = threadIdx.x & 31;
-  int r[PER], tot[2];
-  warp_class_rank(v, nC, r, tot);
-  if (lane < nC && tot[0]) atomicAdd(&cnt[lane], tot[0]);
-  if (lane + 32 < nC && tot[1]) atomicAdd(&cnt[lane + 32], tot[1]);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int v[ROWS];
+  load_rows(cls, (int64_t)blockIdx.x * TILE + w * 32 * ROWS, N, v);
+#pragma unroll
+  for (int j = 0; j < ROWS; ++j) {
+    const unsigned m = __match_any_sync(0xffffffffu, v[j]);
+    if (v[j] >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[v[j]], __popc(m));
+  }
   __syncthreads();
-  if (threadIdx.x < NCLS) counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x < nC) counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(THREADS) k_cls_rank(const int32_t* __restrict__ cls, const RouteParams P,
+__global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
-                                                      const DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
-                                                      int32_t* __restrict__ slot) {
+                                                      DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
+                                                      int32_t* __restrict__ slot, int32_t* __restrict__ off,
+                                                      int32_t* __restrict__ user_off) {
   pdl_entry();
-  __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp class totals, then exclusive prefix over warps
+  __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tile = blockIdx.x;
-  const int64_t base = (int64_t)tile * TILE;
-  const int n = (int)min((int64_t)TILE, P.N - base);
-  if (threadIdx.x < NCLS) {
+  const int64_t base = (int64_t)tile * TILE + w * 32 * ROWS;
+  int c[ROWS];
+  load_rows(cls, base, P.N, c);
+  for (int i = threadIdx.x; i < WARPS * NCLS; i += THREADS) (&wcnt[0][0])[i] = 0;
+  if (threadIdx.x < nC) {
     const int64_t row = (int64_t)threadIdx.x * ntiles;
     tile_off[threadIdx.x] = scanned[row + tile] - scanned[row];
   }
-  int c[PER];
-  load4(cls, base, n, c);
-  int r[PER], tot[2];
-  warp_class_rank(c, nC, r, tot);
-  wcnt[w][lane] = lane < nC ? tot[0] : 0;
-  wcnt[w][lane + 32] = lane + 32 < nC ? tot[1] : 0;
   __syncthreads();
-  if (threadIdx.x < NCLS) {   // exclusive prefix over warps, per class
+  const unsigned lt = (1u << lane) - 1;
+  int r[ROWS];
+#pragma unroll
+  for (int j = 0; j < ROWS; ++j) {
+    const unsigned m = __match_any_sync(0xffffffffu, c[j]);
+    const bool lead = lane == __ffs(m) - 1;
+    r[j] = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
+    __syncwarp();
+    if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < nC) {   // exclusive prefix over warps, per class
     int run = 0;
     for (int v2 = 0; v2 < WARPS; ++v2) {
       const int x = wcnt[v2][threadIdx.x];
@@ -129,61 +104,55 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const int32_t* __restrict_
     }
   }
   __syncthreads();
-  int inst[PER], sl[PER];
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    inst[j] = -1;
-    sl[j] = 0;
+  for (int j = 0; j < ROWS; ++j) {
+    const int64_t p = base + 32 * j + lane;
     if (c[j] < 0) continue;
     const int t = tile_off[c[j]] + wcnt[w][c[j]] + r[j];
+    int inst, sl;
     if (P.mode == PAS_UNIFORM) {
-      inst[j] = c[j];
-      sl[j] = t;
+      inst = c[j];
+      sl = t;
     } else {
       // q1 = t div b*, q2 = q1 div n_j (exact multiply-high, t < 2^26, n_j <= 64):
       // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
       const uint32_t b = (uint32_t)P.bstar;
       const uint32_t q1 = P.bstar_shift >= 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
       const uint32_t q2 = (uint32_t)(((uint64_t)q1 * plan->n_inst_magic[c[j]]) >> 32);
-      inst[j] = plan->inst_list[c[j]][q1 - q2 * (uint32_t)plan->n_inst[c[j]]];
-      sl[j] = (int)(q2 * b + ((uint32_t)t - q1 * b));
+      inst = plan->inst_list[c[j]][q1 - q2 * (uint32_t)plan->n_inst[c[j]]];
+      sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
+    instance[p] = inst;
+    slot[p] = sl;
   }
-  store4(instance, base, n, inst);
-  store4(slot, base, n, sl);
-}
-
-// Per-instance counts from the class totals (scan of the class-major counts), then offsets.
-__global__ void k_offsets(const int32_t* __restrict__ scanned, int ntiles, int64_t N, const RouteParams P,
-                          DevPlan* __restrict__ plan, int32_t* __restrict__ off, int32_t* __restrict__ user_off) {
-  pdl_entry();
-  if (threadIdx.x != 0) return;
-  const int nC = P.mode == PAS_UNIFORM ? P.W : P.nK;
-  int count[kMaxInst];
-  for (int w = 0; w < P.W; ++w) count[w] = 0;
-  for (int c = 0; c < nC; ++c) {
-    const int64_t start = scanned[(int64_t)c * ntiles];
-    const int64_t end = c + 1 < NCLS ? scanned[(int64_t)(c + 1) * ntiles] : N;
-    const int total = (int)(end - start);
-    if (P.mode == PAS_UNIFORM) {
-      count[c] = total;
-    } else {
-      const int nj = plan->n_inst[c], b = P.bstar;
-      if (nj == 0) continue;
-      const int full = total / (b * nj), rem = total % (b * nj);
-      for (int m = 0; m < nj; ++m) {
-        const int extra = rem - m * b;
-        count[plan->inst_list[c][m]] = full * b + (extra < 0 ? 0 : (extra > b ? b : extra));
+  if (tile == 0 && threadIdx.x == 0) {
+    // class totals (from the scanned counts) -> per-instance counts (closed form) -> offsets
+    int count[kMaxInst];
+    for (int i = 0; i < P.W; ++i) count[i] = 0;
+    for (int cc = 0; cc < nC; ++cc) {
+      const int64_t start = scanned[(int64_t)cc * ntiles];
+      const int64_t end = cc + 1 < nC ? scanned[(int64_t)(cc + 1) * ntiles] : P.N;
+      const int total = (int)(end - start);
+      if (P.mode == PAS_UNIFORM) {
+        count[cc] = total;
+      } else {
+        const int nj = plan->n_inst[cc], b = P.bstar;
+        if (nj == 0) continue;
+        const int full = total / (b * nj), rem = total % (b * nj);
+        for (int m = 0; m < nj; ++m) {
+          const int extra = rem - m * b;
+          count[plan->inst_list[cc][m]] = full * b + (extra < 0 ? 0 : (extra > b ? b : extra));
+        }
       }
     }
-  }
-  int run = 0;
-  for (int w = 0; w <= P.W; ++w) {
-    off[w] = run;
-    if (user_off) user_off[w] = run;
-    if (w < P.W) {
-      plan->inst_count[w] = count[w];
-      run += count[w];
+    int run = 0;
+    for (int i = 0; i <= P.W; ++i) {
+      off[i] = run;
+      if (user_off) user_off[i] = run;
+      if (i < P.W) {
+        plan->inst_count[i] = count[i];
+        run += count[i];
+      }
     }
   }
 }
@@ -219,13 +188,11 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
   const int ntiles = batch_tiles(p.N);
   const int nclasses = p.mode == PAS_UNIFORM ? p.W : p.nK;
   launch_pdl(k_cls_count, ntiles, THREADS, 0, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
-  cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, NCLS * ntiles, w.scan_tmp, st, launches);
+  cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, nclasses * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
-  launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot);
+  launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot,
+             w.offsets, bucket_offsets);
   *launches += 2;
-  if (e != cudaSuccess) return e;
-  launch_pdl(k_offsets, 1, 32, 0, st, w.blk_off, ntiles, p.N, p, plan, w.offsets, bucket_offsets);
-  *launches += 1;
   if (bucket_prompts) {
     launch_pdl(k_bucket, (unsigned)((p.N + 1023) / 1024), 256, 0, st, instance, slot, p.N, w.offsets, bucket_prompts);
     *launches += 1;

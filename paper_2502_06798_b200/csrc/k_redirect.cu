@@ -48,7 +48,7 @@ __global__ void k_scatter(const uint64_t* __restrict__ key, const int32_t* __res
 // (key, p), hence its global rank, its rank within its optimal-K class, its K' and its K7 class.
 __global__ void k_rank(const KeyEntry* __restrict__ sorted, RouteParams P, const DevPlan* __restrict__ plan,
                        const int32_t* __restrict__ bcount, const int32_t* __restrict__ bstart,
-                       int32_t* __restrict__ cls7, int32_t* __restrict__ K_prime) {
+                       uint8_t* __restrict__ cls7, int32_t* __restrict__ K_prime) {
   pdl_entry();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.N) return;

@@ -19,6 +19,15 @@
 // units u = id + i*count with m fastest, so concurrently running CTAs stream the SAME cache tiles
 // (L2 reuse of the big operand) against different prompt tiles.
 //
+// Progress leash (used only for small N, see simtopk_leash_slack).  CTAs that stream the same cache
+// range in the same wave re-use each tile from L2 only while they stay within L2's reach of each
+// other; free-running, they drift apart by more than that over a range of thousands of tiles and
+// tiles are fetched from DRAM again and again (C4: 491 GB of DRAM reads per launch for a 15.4 GB
+// cache).  So each producer warp publishes its tile
+// count (epoch-tagged, one 8-B word per CTA) and, before issuing a tile, waits until it is at most
+// `slack` tiles ahead of the slowest CTA still working; slack is sized so that the tiles between
+// the slowest and the fastest CTA of every concurrently streamed range fit in a share of L2.
+//
 // Warp roles per CTA (320 threads, 1 CTA/SM):
 //   warp 0      TMA producer (128-B swizzle, mbarrier complete_tx).
 //   warp 1      TMEM allocation (512 columns = two 256-column fp32 accumulators) and one lane issuing
@@ -142,6 +151,29 @@ __device__ __forceinline__ void merge_lists(float (&s)[KMAX], int32_t (&gl)[KMAX
   }
 }
 
+// Whole producer warp: publish `issued` and wait until issued - min(progress of live CTAs) <= slack.
+// Bounded (a CTA that never gets a slot cannot deadlock the grid: the leash just lets go).
+__device__ __noinline__ void leash_wait(uint64_t* progress, int worker, int nworkers, uint32_t epoch,
+                                        uint32_t issued, uint32_t slack) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane == 0)
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(progress + worker),
+                 "l"(((uint64_t)epoch << 32) | issued) : "memory");
+  if (issued <= slack) return;
+  for (int spin = 0; spin < (1 << 16); ++spin) {
+    uint32_t mn = 0xFFFFFFFFu;
+    for (int w = (int)lane; w < nworkers; w += 32) {
+      uint64_t v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(progress + w) : "memory");
+      mn = min(mn, (uint32_t)(v >> 32) == epoch ? (uint32_t)v : 0u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (issued - min(mn, issued) <= slack) return;
+    __nanosleep(512);
+  }
+}
+
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
@@ -150,7 +182,7 @@ template <int KMAX, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
-              float* __restrict__ dump) {
+              float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -197,15 +229,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
-    if (ptx::elect_one()) {
+    // The whole warp walks the schedule (for the leash); lane 0 waits on the ring and issues TMA.
+    {
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t issued = 0;
       for (int u = worker; u < units; u += nworkers) {
         const int m = u % MT, r = u / MT;
         const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
         const int qrow = m * UNIT_ROWS + (int)crank * BM;
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++issued) {
+          if (slack) {
+            if (leader) leash_wait(progress, worker, nworkers, epoch, issued, slack);
+            __syncwarp();
+          }
           const int crow = t * BN + (int)crank * BN_CTA;
+          if (lane == 0)
           for (int kb = 0; kb < kblocks; ++kb) {
             ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
             if (PAIR) {
@@ -220,8 +259,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
+          __syncwarp();
         }
       }
+      if (slack && leader && lane == 0)   // done: never hold anyone back
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(progress + worker),
+                     "l"(((uint64_t)epoch << 32) | 0xFFFFFFFFull) : "memory");
     }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer ---------------------------------
@@ -558,7 +601,7 @@ cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream
 }
 
 template <int KMAX, bool DUMP>
-cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
+cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -574,7 +617,7 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, cudaS
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP>, *a.tmap_q, *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
-                            a.rank, a.R, MT, NT, a.out, a.dump);
+                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack);
 }
 
 }  // namespace
@@ -622,6 +665,28 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d) 
   return best;
 }
 
+// Leash slack in tiles (0 = off): the ranges streamed concurrently by one wave of `workers` CTAs,
+// each spread over at most `slack` tiles, must fit in PAS_K2_LEASH_MB of L2 next to the prompt tiles.
+// Measured on one B200 (profiles/r01_leash/): the leash cuts K2's DRAM reads at C4 from
+// 491 GB to 73 GB per launch but costs 9 % throughput there (CTAs wait for the slowest SM; DRAM is
+// not K2's bound), and gains 4-6 % only when many ranges are streamed at once (MT <= 16 prompt
+// tiles, i.e. N <= 2048).  So it is on only in that regime, and off when units are short or a
+// range has a single reader.
+#ifndef PAS_K2_LEASH_MB
+#define PAS_K2_LEASH_MB 48
+#endif
+uint32_t simtopk_leash_slack(int MT, int NT, int R, int workers) {
+  if (PAS_K2_LEASH_MB <= 0 || MT < 2 || MT > 16 || workers < 2) return 0;
+  const int64_t tiles_per_unit = ((int64_t)NT + R - 1) / R;
+  const int64_t ranges = MT >= workers ? 2 : (workers + MT - 1) / MT + 1;   // +1: a wave straddles two
+  const int64_t tile_bytes = (int64_t)BN * 768 * 2;
+  int64_t slack = ((int64_t)PAS_K2_LEASH_MB << 20) / (ranges * tile_bytes);
+  if (slack < 2) slack = 2;
+  if (slack > 64) slack = 64;
+  if (tiles_per_unit < 8 * slack) return 0;
+  return (uint32_t)slack;
+}
+
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   const int MT = (int)((a.N + UNIT_ROWS - 1) / UNIT_ROWS);
   const int NT = (int)((a.M_local + tile_rows(a.d) - 1) / tile_rows(a.d));
@@ -634,9 +699,10 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
     if (a.k <= 8) return launch_ta<8, false>(a, MT, NT, grid, st);
     return launch_ta<16, false>(a, MT, NT, grid, st);
   }
-  if (a.dump) return launch_variant<8, true>(a, MT, NT, grid, st);
-  if (a.k <= 8) return launch_variant<8, false>(a, MT, NT, grid, st);
-  return launch_variant<16, false>(a, MT, NT, grid, st);
+  const uint32_t slack = a.progress ? simtopk_leash_slack(MT, NT, a.R, grid / CTAS) : 0;
+  if (a.dump) return launch_variant<8, true>(a, MT, NT, grid, slack, st);
+  if (a.k <= 8) return launch_variant<8, false>(a, MT, NT, grid, slack, st);
+  return launch_variant<16, false>(a, MT, NT, grid, slack, st);
 }
 
 }  // namespace pas

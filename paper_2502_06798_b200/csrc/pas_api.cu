@@ -102,6 +102,16 @@ struct pas_ctx {
   Cand* cand_local = nullptr;
   Cand* cand_rank = nullptr;
   Cand* cand_all = nullptr;
+  uint64_t* k2_progress = nullptr;   // K2 leash words [kNumSMs]
+  // f1 forecast-driven mode (0 = exact per-batch plan)
+  int fc_window = 0, fc_replan_every = 1;
+  int64_t fc_tick = 0;
+  bool fc_planned = false;
+  double fc_F_planned[kMaxLevels] = {};
+  uint8_t* fc_ring = nullptr;
+  FcState* fc_state = nullptr;
+  bool fc_stats_valid = false;
+  uint32_t k2_epoch = 0;
   uint8_t* level = nullptr;
   int* hist = nullptr;
   int* invalid_count = nullptr;
@@ -238,6 +248,8 @@ pas_status ensure_prompt_ws(pas_ctx* ctx) {
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = dmalloc(&ctx->qhat, (size_t)(ctx->q_rows * d));
   if (e == cudaSuccess) e = dmalloc(&ctx->pflags, (size_t)mb);
+  if (e == cudaSuccess) e = dmalloc(&ctx->k2_progress, (size_t)kNumSMs);
+  if (e == cudaSuccess) e = cudaMemset(ctx->k2_progress, 0, sizeof(uint64_t) * kNumSMs);   // epoch 0 = none
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_local, (size_t)(ctx->cand_cap * k));
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_rank, (size_t)(mb * k));
   if (e == cudaSuccess && (ctx->cfg.world > 1 || ctx->comm))
@@ -263,8 +275,10 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
       const int r = atoi(ov);
       if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
     }
+    if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
-                  ctx->qhat, ctx->cand_local, nullptr};
+                  ctx->qhat, ctx->cand_local, nullptr, getenv("PAS_K2_NOLEASH") ? nullptr : ctx->k2_progress,
+                  ctx->k2_epoch};
     CUDA_TRY(ctx, launch_simtopk(a, st));
   } else {
     CUDA_TRY(ctx, launch_fill_sentinel(ctx->cand_local, N * k, st));
@@ -295,10 +309,28 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
-  CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
-  ctx->launches++;
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
-  CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, st, &ctx->launches));
+  if (ctx->fc_window > 0) {
+    // f1: plan from the forecast (held between rebuilds, R24), i.i.d. K' (R23), window update (R21)
+    bool replan = !ctx->fc_planned || ctx->fc_tick % ctx->fc_replan_every == 0;
+    for (int j = 0; j < ctx->nK; ++j) replan = replan || ctx->F[j] != ctx->fc_F_planned[j];
+    if (replan) {
+      for (int j = 0; j < kMaxLevels; ++j) ctx->fc_F_planned[j] = ctx->F[j];
+      ctx->fc_planned = true;
+    }
+    ctx->fc_tick++;
+    CUDA_TRY(ctx, launch_fc_plan(ctx->hist, p, ctx->plan, ctx->fc_state, replan, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(ctx, launch_fc_sample(ctx->level, p, ctx->plan, ctx->fc_state, out->K_prime, ctx->rw.cls7, st));
+    CUDA_TRY(ctx, launch_fc_window(ctx->level, p, ctx->plan, ctx->fc_state, ctx->fc_ring, ctx->fc_window, st));
+    ctx->launches += 3;
+    ctx->fc_stats_valid = true;
+  } else {
+    CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
+    ctx->launches++;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, st, &ctx->launches));
+    ctx->fc_stats_valid = false;
+  }
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
   CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, ctx->bw, out->instance, out->slot,
                                        out->bucket_offsets, out->bucket_prompts, st, &ctx->launches));
@@ -341,7 +373,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
     if (ctx->poisoned) g_nccl.CommAbort(ctx->comm);
     else g_nccl.CommDestroy(ctx->comm);
   }
-  void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all,
+  void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all, ctx->k2_progress, ctx->fc_ring, ctx->fc_state,
                   ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
                   ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.sorted,    ctx->rw.cls7,
                   ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp, ctx->rw.scan_tmp,
@@ -518,6 +550,42 @@ pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const fl
   }
   ctx->bands_set = true;
   ctx->fractions_set = false;
+  if (ctx->fc_window > 0) {   // the window holds level indices of the old bands: start afresh
+    CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+    CUDA_TRY(ctx, cudaMemset(ctx->fc_state, 0, sizeof(FcState)));
+    ctx->fc_tick = 0;
+    ctx->fc_planned = false;
+  }
+  return PAS_OK;
+}
+
+pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (window < 0 || window > PAS_MAX_FORECAST_WINDOW)
+    return fail(ctx, PAS_ERR_ARG, "window must be in [0, %d]", PAS_MAX_FORECAST_WINDOW);
+  if (replan_every < 1) return fail(ctx, PAS_ERR_ARG, "replan_every must be >= 1");
+  if (window > 0 && !ctx->bands_set) return fail(ctx, PAS_ERR_STATE, "pas_set_bands must precede pas_set_forecast");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());   // no batch in flight may still read the old window
+  if (window > 0) {
+    if (window > ctx->fc_window) {
+      if (ctx->fc_ring) cudaFree(ctx->fc_ring);
+      ctx->fc_ring = nullptr;
+      cudaError_t e = dmalloc(&ctx->fc_ring, (size_t)window);
+      if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "forecast window allocation failed");
+    }
+    if (!ctx->fc_state) {
+      cudaError_t e = dmalloc(&ctx->fc_state, 1);
+      if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "forecast state allocation failed");
+    }
+    CUDA_TRY(ctx, cudaMemset(ctx->fc_state, 0, sizeof(FcState)));
+  }
+  ctx->fc_window = window;
+  ctx->fc_replan_every = replan_every;
+  ctx->fc_tick = 0;
+  ctx->fc_planned = false;
+  ctx->fc_stats_valid = false;
   return PAS_OK;
 }
 
@@ -728,6 +796,21 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
   out->n_near_top1 = p.n_near_top1;
   out->n_near_threshold = p.n_near_threshold;
   for (int w = 0; w < ctx->W; ++w) out->bucket_count[w] = p.inst_count[w];
+  if (ctx->fc_stats_valid) {
+    FcState f;
+    CUDA_TRY(ctx, cudaMemcpy(&f, ctx->fc_state, sizeof f, cudaMemcpyDeviceToHost));
+    out->forecast = 1;
+    out->fc_replanned = f.replanned;
+    out->fc_plan_n = f.plan_n;
+    for (int i = 0; i < ctx->nK; ++i) out->fc_plan_counts[i] = f.plan_cnt[i];
+    out->fc_window_n = f.n;
+    out->fc_l2_error = f.l2;
+    out->n_unforecast = f.n_unforecast;
+    for (int i = 0; i <= ctx->nK; ++i) {
+      out->fc_Hc[i] = f.Hc[i];
+      out->fc_Fc[i] = f.Fc[i];
+    }
+  }
   for (int i = 0; i < 6; ++i) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) out->stage_ms[i] = ms;
@@ -749,7 +832,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
-                ctx->qhat, ctx->cand_local, scores_dev};
+                ctx->qhat, ctx->cand_local, scores_dev, nullptr, 0};
   CUDA_TRY(ctx, launch_simtopk(a, st));
   return PAS_OK;
 }

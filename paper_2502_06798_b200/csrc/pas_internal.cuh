@@ -110,6 +110,8 @@ struct SimTopkArgs {
   const __nv_bfloat16* qhat;      // [rows_q x d] (A-in-TMEM variant reads the prompt rows directly)
   Cand* out;                      // [R][N][k]
   float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
+  uint64_t* progress;             // [kNumSMs] leash words (epoch << 32 | tiles issued), or null: no leash
+  uint32_t epoch;                 // this launch's epoch (never 0: zeroed words read as "not started")
 };
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
@@ -151,16 +153,36 @@ struct RedirectWs {
   int32_t* bstart;        // [nK << kb]
   int32_t* bfill;         // [nK << kb]   zeroed
   KeyEntry* sorted;       // [N] bucket order
-  int32_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
+  uint8_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
   int32_t* scan_tmp;      // scan_tmp_ints(nK << kb)
 };
 cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan,
                             const RedirectWs& w, int32_t* K_prime, cudaStream_t st, int* launches);
 
+// f1 forecast-driven mode (R21-R24): predictor ring buffer + fixed-point Route-Plan.
+struct FcState {
+  int32_t head, n;                  // ring write position, valid entries (<= window)
+  int32_t cnt[kMaxLevels];          // level counts over the window (after the last batch)
+  int32_t plan_cnt[kMaxLevels];     // the counts the held plan was built from
+  int32_t plan_n;
+  int32_t replanned;                // this batch rebuilt the plan
+  uint64_t Hc[kMaxLevels + 1];      // cumulative forecast mass, units of 2^-32
+  uint64_t Fc[kMaxLevels + 1];      // cumulative F, units of 2^-32
+  double D_Q_plan, l2;
+  int32_t n_unforecast;
+  int32_t pad;
+};
+cudaError_t launch_fc_plan(const int* hist, const RouteParams& p, DevPlan* plan, FcState* fcs, bool replan,
+                           cudaStream_t st);
+cudaError_t launch_fc_sample(const uint8_t* level, const RouteParams& p, DevPlan* plan, FcState* fcs,
+                             int32_t* K_prime, uint8_t* cls7, cudaStream_t st);
+cudaError_t launch_fc_window(const uint8_t* level, const RouteParams& p, DevPlan* plan, FcState* fcs,
+                             uint8_t* ring, int window, cudaStream_t st);
+
 // K7 route-and-batch
 struct BatchWs {
-  int32_t* blk_counts;   // [64 * batch_tiles(N)], class-major
-  int32_t* blk_off;      // [64 * batch_tiles(N)]
+  int32_t* blk_counts;   // [C * batch_tiles(N)], class-major (C <= 64 classes)
+  int32_t* blk_off;      // [C * batch_tiles(N)]
   int32_t* offsets;      // [W+1]
   int32_t* scan_tmp;     // scan_tmp_ints(64 * batch_tiles(N))
 };

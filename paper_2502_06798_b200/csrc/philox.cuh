@@ -8,6 +8,7 @@ namespace pas {
 
 constexpr uint32_t kStreamRedirect = 1;
 constexpr uint32_t kStreamUniform = 2;
+constexpr uint32_t kStreamForecast = 3;   // f1: i.i.d. K' draw from the forecast Route-Plan (R23)
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll

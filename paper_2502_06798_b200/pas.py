@@ -21,6 +21,7 @@ STATUS = {0: "PAS_OK", -1: "PAS_ERR_ARG", -2: "PAS_ERR_STATE", -3: "PAS_ERR_FRAC
 PAS_F32, PAS_BF16 = 0, 1
 PAS_GREEDY, PAS_UNIFORM = 0, 1
 PAS_MAX_LEVELS, PAS_MAX_INSTANCES, PAS_T_TOTAL, PAS_MAX_TOPK = 16, 64, 50, 16
+PAS_MAX_FORECAST_WINDOW = 1 << 22
 PAS_NCCL_ID_BYTES = 128
 FLAG_INVALID, FLAG_COLD, FLAG_NEAR_TOP1, FLAG_NEAR_THRESHOLD = 1, 2, 4, 8
 
@@ -44,7 +45,11 @@ class PasStats(C.Structure):
                 ("D_Q", C.c_double), ("D_Q_LP", C.c_double),
                 ("n_redirected", C.c_int64), ("n_upgraded", C.c_int64), ("n_downgraded", C.c_int64),
                 ("n_invalid", C.c_int64), ("n_near_top1", C.c_int64), ("n_near_threshold", C.c_int64),
-                ("bucket_count", C.c_int64 * PAS_MAX_INSTANCES), ("stage_ms", C.c_float * 8)]
+                ("bucket_count", C.c_int64 * PAS_MAX_INSTANCES), ("stage_ms", C.c_float * 8),
+                ("forecast", C.c_int), ("fc_replanned", C.c_int), ("fc_plan_n", C.c_int64),
+                ("fc_plan_counts", C.c_int64 * PAS_MAX_LEVELS), ("fc_window_n", C.c_int64),
+                ("fc_l2_error", C.c_double), ("n_unforecast", C.c_int64),
+                ("fc_Hc", C.c_uint64 * (PAS_MAX_LEVELS + 1)), ("fc_Fc", C.c_uint64 * (PAS_MAX_LEVELS + 1))]
 
 
 class PasError(RuntimeError):
@@ -71,6 +76,7 @@ _SIG = {
     "pas_set_degradation": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
     "pas_set_fractions": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int]),
     "pas_set_seed": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
+    "pas_set_forecast": (C.c_int, [_P, C.c_int, C.c_int]),
     "pas_route_batch": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_batch_host": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_local": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
@@ -182,6 +188,10 @@ def pas_set_seed(ctx, seed, batch_seq=0):
     _check(ctx, lib.pas_set_seed(ctx, seed, batch_seq))
 
 
+def pas_set_forecast(ctx, window, replan_every=1):
+    _check(ctx, lib.pas_set_forecast(ctx, window, replan_every))
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -222,7 +232,11 @@ def pas_plan_stats(ctx) -> dict:
                 x=[list(s.x[i][:nK]) for i in range(nK)], D_Q=s.D_Q, D_Q_LP=s.D_Q_LP,
                 n_redirected=s.n_redirected, n_upgraded=s.n_upgraded, n_downgraded=s.n_downgraded,
                 n_invalid=s.n_invalid, n_near_top1=s.n_near_top1, n_near_threshold=s.n_near_threshold,
-                bucket_count=list(s.bucket_count[:W]), stage_ms=list(s.stage_ms))
+                bucket_count=list(s.bucket_count[:W]), stage_ms=list(s.stage_ms),
+                forecast=s.forecast, fc_replanned=s.fc_replanned, fc_plan_n=s.fc_plan_n,
+                fc_plan_counts=list(s.fc_plan_counts[:nK]), fc_window_n=s.fc_window_n,
+                fc_l2_error=s.fc_l2_error, n_unforecast=s.n_unforecast,
+                fc_Hc=list(s.fc_Hc[:nK + 1]), fc_Fc=list(s.fc_Fc[:nK + 1]))
 
 
 def pas_last_launch_count(ctx) -> int:
@@ -276,6 +290,9 @@ class Router:
 
     def set_seed(self, seed, batch_seq=0):
         pas_set_seed(self.ctx, seed, batch_seq)
+
+    def set_forecast(self, window, replan_every=1):
+        pas_set_forecast(self.ctx, window, replan_every)
 
     def alloc_out(self, N, optional=True, device=None):
         t = self.torch

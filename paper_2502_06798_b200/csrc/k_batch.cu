@@ -9,21 +9,22 @@
 //   instance (batch size 1).
 // Both need the stable rank t of every prompt among the prompts of its class (C classes: the nK <= 16
 // K' levels in greedy mode, the W <= 64 instances in uniform mode) in prompt order.  The class is a
-// byte per prompt.  Tiles of 4096 prompts; each warp takes 512 consecutive prompts as ROWS = 16 rows
-// of 32 (lane l of row j holds prompt 32 j + l; coalesced loads, all 16 in flight before any compute):
-//   k_cls_count  per-tile class counts, written class-major [C][tiles]
+// byte per prompt.  Tiles of 4096 prompts:
+//   k_cls_count  per-tile class counts, written class-major [C][tiles]: 16 consecutive prompts per
+//                thread (one 16-byte load), counted in a private shared-memory column cnt[c][thread]
+//                (conflict-free: the column is the bank), rows summed by one warp per class.
 //   scan         device-wide exclusive scan of that array: entry (c, b) = prompts of classes < c plus
 //                prompts of class c in tiles < b
-//   k_cls_rank   t = scan(c, b) - scan(c, 0) + rank inside the tile.  Inside a warp, row by row:
-//                match.any gives the lanes holding the same class, popc of those below a lane is its
-//                rank in the row, and a per-warp running count per class (shared memory, bumped by the
-//                lowest lane of each match group) carries the earlier rows; per block an exclusive
-//                prefix over the 8 warps.  Cost per row is independent of C.  Block 0 also turns the
-//                class totals into per-instance counts (closed form, greedy: each I_j[m] gets the t's
-//                whose (t div b*) mod n_j = m) and the batch-list offsets.
+//   k_cls_rank   t = scan(c, b) - scan(c, 0) + rank inside the tile.  Each warp takes 512 consecutive
+//                prompts as 16 rows of 32 (coalesced loads and stores); row by row, match.any gives the
+//                lanes of one class, popc of those below a lane is its rank in the row, a per-warp
+//                running count per class carries the earlier rows; per block an exclusive prefix over
+//                the 8 warps.  Block 0 also turns the class totals into per-instance counts (closed
+//                form, greedy: each I_j[m] gets the t's whose (t div b*) mod n_j = m) and the offsets.
 //   k_bucket     scatter prompt ids to offsets[instance] + slot.
-// (A single-pass decoupled look-back variant was 60 % slower at 64M prompts: with ~1200 tiles in
-// flight the look-back walks hundreds of predecessors per tile.)
+// Measured alternatives (64M prompts, profiles/r01_stream): match.any counting is ADU-bound (98 %);
+// one ballot per class bit is slower still; the column scheme ranks slower than match.any (262 vs
+// 207 us); a single-pass decoupled look-back is 60 % slower than count + scan + rank.
 // HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 8 B read + 4 B written.
 #include "pas_internal.cuh"
 
@@ -32,11 +33,26 @@ namespace {
 
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int ROWS = 16;                       // rows of 32 prompts per warp
-constexpr int TILE = THREADS * ROWS;           // prompts per CTA
+constexpr int PER = 16;                        // consecutive prompts per thread (k_cls_count)
+constexpr int ROWS = 16;                       // rows of 32 prompts per warp (k_cls_rank)
+constexpr int TILE = THREADS * PER;            // prompts per CTA (both kernels: same tiles)
+static_assert(PER == ROWS, "k_cls_count and k_cls_rank must cut the same tiles");
 constexpr int NCLS = 64;
 
-// Row j of this warp's chunk: prompt base + 32 j + lane (-1 past the end).
+// This thread's 16 consecutive classes (-1 past the end): one 16-byte load.
+__device__ __forceinline__ void load_cls(const uint8_t* __restrict__ src, int64_t p0, int64_t N, int (&v)[PER]) {
+  if (p0 + PER <= N) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + p0));
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < PER; ++e) v[e] = (int)((w[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+  } else {
+#pragma unroll
+    for (int e = 0; e < PER; ++e) v[e] = p0 + e < N ? (int)src[p0 + e] : -1;
+  }
+}
+
+// Row j of this warp's chunk for k_cls_rank: prompt base + 32 j + lane (-1 past the end).
 __device__ __forceinline__ void load_rows(const uint8_t* __restrict__ src, int64_t base, int64_t N, int (&v)[ROWS]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -46,22 +62,37 @@ __device__ __forceinline__ void load_rows(const uint8_t* __restrict__ src, int64
   }
 }
 
+// Per-thread class counts in the private column cnt[c * THREADS + tid]; r[e] = rank of element e
+// among this thread's earlier elements of its class.
+__device__ __forceinline__ void column_counts(int32_t* cnt, int nC, const int (&v)[PER], int (&r)[PER]) {
+  const int t = threadIdx.x;
+  for (int c = 0; c < nC; ++c) cnt[c * THREADS + t] = 0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    if (v[e] < 0) continue;
+    int32_t* a = cnt + v[e] * THREADS + t;
+    r[e] = *a;
+    *a = r[e] + 1;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict__ cls, int64_t N, int ntiles,
                                                        int nC, int32_t* __restrict__ counts /*[nC][ntiles]*/) {
   pdl_entry();
-  __shared__ int32_t cnt[NCLS];
-  if (threadIdx.x < NCLS) cnt[threadIdx.x] = 0;
-  __syncthreads();
+  extern __shared__ int32_t cnt[];      // [nC][THREADS]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int v[ROWS];
-  load_rows(cls, (int64_t)blockIdx.x * TILE + w * 32 * ROWS, N, v);
-#pragma unroll
-  for (int j = 0; j < ROWS; ++j) {
-    const unsigned m = __match_any_sync(0xffffffffu, v[j]);
-    if (v[j] >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[v[j]], __popc(m));
-  }
+  int v[PER], r[PER];
+  load_cls(cls, (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * PER, N, v);
+  column_counts(cnt, nC, v, r);
   __syncthreads();
-  if (threadIdx.x < nC) counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+  for (int c = w; c < nC; c += WARPS) {   // one warp per class: sum its row
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < THREADS / 32; ++i) sum += cnt[c * THREADS + lane + 32 * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) counts[(int64_t)c * ntiles + blockIdx.x] = sum;
+  }
 }
 
 __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
@@ -72,17 +103,30 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
   pdl_entry();
   __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
+  __shared__ uint64_t magic_s[kMaxLevels];
+  __shared__ int32_t ninst_s[kMaxLevels];
+  __shared__ int32_t ilist_s[kMaxLevels][kMaxInst];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * TILE + w * 32 * ROWS;
   int c[ROWS];
   load_rows(cls, base, P.N, c);
   for (int i = threadIdx.x; i < WARPS * NCLS; i += THREADS) (&wcnt[0][0])[i] = 0;
+  if (P.mode != PAS_UNIFORM) {   // the instance lists of the K' levels, staged once per block
+    if (threadIdx.x < nC) {
+      magic_s[threadIdx.x] = plan->n_inst_magic[threadIdx.x];
+      ninst_s[threadIdx.x] = plan->n_inst[threadIdx.x];
+    }
+    for (int i = threadIdx.x; i < nC * kMaxInst; i += THREADS)
+      ilist_s[i / kMaxInst][i % kMaxInst] = plan->inst_list[i / kMaxInst][i % kMaxInst];
+  }
   if (threadIdx.x < nC) {
     const int64_t row = (int64_t)threadIdx.x * ntiles;
     tile_off[threadIdx.x] = scanned[row + tile] - scanned[row];
   }
   __syncthreads();
+  // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count
+  // per class (bumped by the lowest lane of each group) carries the earlier rows
   const unsigned lt = (1u << lane) - 1;
   int r[ROWS];
 #pragma unroll
@@ -118,8 +162,8 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
       // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
       const uint32_t b = (uint32_t)P.bstar;
       const uint32_t q1 = P.bstar_shift >= 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
-      const uint32_t q2 = (uint32_t)(((uint64_t)q1 * plan->n_inst_magic[c[j]]) >> 32);
-      inst = plan->inst_list[c[j]][q1 - q2 * (uint32_t)plan->n_inst[c[j]]];
+      const uint32_t q2 = (uint32_t)(((uint64_t)q1 * magic_s[c[j]]) >> 32);
+      inst = ilist_s[c[j]][q1 - q2 * (uint32_t)ninst_s[c[j]]];
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
     instance[p] = inst;
@@ -181,13 +225,22 @@ __global__ void k_bucket(const int32_t* __restrict__ instance, const int32_t* __
 
 int batch_tiles(int64_t N) { return (int)((N + TILE - 1) / TILE); }
 
+// Up to 64 classes x 256 threads of int32 columns (64 KB) needs the > 48 KB opt-in.
+cudaError_t batch_init() {
+  const int bytes = NCLS * THREADS * (int)sizeof(int32_t);
+  cudaError_t e = cudaFuncSetAttribute(k_cls_count, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  return e;
+}
+
 cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan, const BatchWs& w,
                                    int32_t* instance, int32_t* slot, int32_t* bucket_offsets,
                                    int32_t* bucket_prompts, cudaStream_t st, int* launches) {
   if (p.N <= 0) return cudaSuccess;
   const int ntiles = batch_tiles(p.N);
   const int nclasses = p.mode == PAS_UNIFORM ? p.W : p.nK;
-  launch_pdl(k_cls_count, ntiles, THREADS, 0, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
+  const size_t smem = (size_t)nclasses * THREADS * sizeof(int32_t);
+  launch_pdl(k_cls_count, ntiles, THREADS, smem, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
   cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, nclasses * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
   launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot,

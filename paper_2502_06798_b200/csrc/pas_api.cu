@@ -461,7 +461,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
   }
-  if ((e = simtopk_init()) != cudaSuccess) {
+  if ((e = simtopk_init()) != cudaSuccess || (e = batch_init()) != cudaSuccess) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "kernel attribute setup failed: %s", cudaGetErrorString(e));
   }

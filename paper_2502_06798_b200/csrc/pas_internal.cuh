@@ -187,6 +187,7 @@ struct BatchWs {
   int32_t* scan_tmp;     // scan_tmp_ints(64 * batch_tiles(N))
 };
 int batch_tiles(int64_t N);
+cudaError_t batch_init();   // kernel attributes (once per device)
 cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan,
                                    const BatchWs& w, int32_t* instance, int32_t* slot,
                                    int32_t* bucket_offsets, int32_t* bucket_prompts,

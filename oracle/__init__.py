@@ -9,13 +9,15 @@ in ``synth/``, which holds none of the method's arithmetic.
 It is a plain, slow, obviously-correct restatement of what the paper's Query
 Dispatcher and K-to-K' Route Planner compute for one batch of prompts
 (PAPER.md P:88-P:104, Eq. 1 at P:96), in float64 unless a step fixes another
-precision, following the readings R1..R20 listed in DESIGN.md.
+precision, following the readings R1..R24 listed in DESIGN.md.
 
 Modules
 -------
 philox  -- Philox4x32-10 counter-based generator (Random123), scalar and vectorised.
 route   -- O1..O10: similarity, top-k, optimal-K, H_K, apportionment, Eq. 1 plan,
            D_Q, redirection, route-and-batch, buckets, and the composite ``route``.
+forecast-- NEXT f1: the forecast-driven streaming mode (ring-buffer H_K predictor,
+           fixed-point Eq. 1 plan, i.i.d. K' sampling, L2 forecast error; R21-R24).
 
 Parity status of every function is stated in its docstring; functions whose
 result is pinned only by internal invariants (no paper-printed value exists)

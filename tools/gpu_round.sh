@@ -6,5 +6,5 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_(simtopk|normalize|merge|select|plan|keys|scan|tile|scatter|rank|cls|offsets|bucket|fill)" -s 153 -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?" >> gpurun_out/ncu_launch.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_(simtopk|normalize|merge|select|plan|keys|scan|tile|scatter|rank|cls|offsets|bucket|fill|zero|fc)" -s 153 -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?" >> gpurun_out/ncu_launch.log
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_simtopk -c 1 -o gpurun_out/k2_c4 $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?" >> gpurun_out/ncu_full.log

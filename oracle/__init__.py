@@ -9,7 +9,7 @@ in ``synth/``, which holds none of the method's arithmetic.
 It is a plain, slow, obviously-correct restatement of what the paper's Query
 Dispatcher and K-to-K' Route Planner compute for one batch of prompts
 (PAPER.md P:88-P:104, Eq. 1 at P:96), in float64 unless a step fixes another
-precision, following the readings R1..R24 listed in DESIGN.md.
+precision, following the readings R1..R27 listed in DESIGN.md.
 
 Modules
 -------
@@ -18,6 +18,8 @@ route   -- O1..O10: similarity, top-k, optimal-K, H_K, apportionment, Eq. 1 plan
            D_Q, redirection, route-and-batch, buckets, and the composite ``route``.
 forecast-- NEXT f1: the forecast-driven streaming mode (ring-buffer H_K predictor,
            fixed-point Eq. 1 plan, i.i.d. K' sampling, L2 forecast error; R21-R24).
+cache   -- NEXT f2: LRU maintenance of the store (vanilla-completion inserts, eviction with
+           slot reuse; R25-R27).
 
 Parity status of every function is stated in its docstring; functions whose
 result is pinned only by internal invariants (no paper-printed value exists)

@@ -154,6 +154,35 @@ pas_status pas_nccl_unique_id(unsigned char* out);
 pas_status pas_cache_load(pas_ctx* ctx, const void* rows_dev, pas_dtype dtype, int64_t M,
                           int64_t* first_gid, pas_stream stream);
 
+/* NEXT f2, cache maintenance (
+ * DESIGN.md R25-R27).  The store has G x max_rows_per_rank global slots; gid g lives on rank g % G.
+ * A logical clock ticks once per routed batch, per insert call and per pas_cache_load; an entry's
+ * stamp is the tick of its insertion or of the last batch that used it as a prompt's top-1 (every
+ * routed batch stamps the top-1 of each valid prompt, on every rank).
+ *
+ * pas_cache_insert: n rows (device [n x d] of dtype, the SAME rows on every rank, n <= max_batch and
+ * <= the global capacity).  Free slots at the end are used first (ascending gids); when they run
+ * out, the entries smallest in (stamp, gid) are evicted -- exactly as many as needed -- and their
+ * slots reused in ascending gid order.  gids_out (optional, device int32 [n]) receives the gid of
+ * each row.  Rows are normalised and rounded like pas_cache_load (a2).  Synchronises the stream.
+ * Errors: PAS_ERR_INVALID_ROWS (a row non-finite or zero-norm: nothing inserted, nothing evicted),
+ * PAS_ERR_CAPACITY, PAS_ERR_ARG. */
+pas_status pas_cache_insert(pas_ctx* ctx, const void* rows_dev, pas_dtype dtype, int64_t n,
+                            int32_t* gids_out_dev, pas_stream stream);
+
+/* The warm-up policy: insert the prompts of a routed batch that were served by vanilla
+ * diffusion (K'_dev[p] == 0, device int32 [N], e.g. pas_route_out.K_prime) once their generations
+ * complete, in prompt order, skipping invalid embeddings; emb_dev: the batch's embeddings [N x d].
+ * gids_by_prompt_dev (optional, device int32 [N]): the new gid of each inserted prompt, -1 for the
+ * others.  n_inserted (optional, host): how many.  Same eviction rule as pas_cache_insert.
+ * Synchronises the stream.  Errors: PAS_ERR_CAPACITY, PAS_ERR_ARG. */
+pas_status pas_cache_insert_vanilla(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
+                                    const int32_t* K_prime_dev, int32_t* gids_by_prompt_dev,
+                                    int64_t* n_inserted, pas_stream stream);
+
+/* Test hook: copy the first n LRU stamps (uint32, one per global slot) to stamps_dev. */
+pas_status pas_cache_stamps(pas_ctx* ctx, uint32_t* stamps_dev, int64_t n, pas_stream stream);
+
 /* Drop every cached row (global count back to 0).  Stream-ordered. */
 pas_status pas_cache_clear(pas_ctx* ctx);
 

@@ -89,7 +89,7 @@ struct Tally {
   }
 };
 
-__device__ __forceinline__ void select_one(float s1, float s2, int64_t p, bool invalid, bool cold,
+__device__ __forceinline__ void select_one(float s1, float s2, int32_t g1, int64_t p, bool invalid, bool cold,
                                            const RouteParams& P, const SelectOut& o, Tally& ty) {
   int lvl = 0;
   uint8_t fl = 0;
@@ -103,6 +103,7 @@ __device__ __forceinline__ void select_one(float s1, float s2, int64_t p, bool i
     if ((lvl > 0 && s1 - P.thr[lvl - 1] < 2e-2f) || (lvl < P.nK - 1 && P.thr[lvl] - s1 < 2e-2f))
       fl |= PAS_FLAG_NEAR_THRESHOLD;
   }
+  if (P.lru_stamp && !invalid && !cold && g1 >= 0) P.lru_stamp[g1] = P.lru_tick;   // f2: top-1 reused (R26)
   o.level[p] = (uint8_t)lvl;
   o.K[p] = P.grid[lvl];
   if (o.flags) o.flags[p] = fl;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restr
       if (o.topk_score) o.topk_score[p * k + i] = c.s;
       if (o.cand_out) o.cand_out[p * k + i] = c;
     }
-    if (lane == 0) select_one(res[w][0].s, k > 1 ? res[w][1].s : -INFINITY, p, invalid, cold, P, o, ty);
+    if (lane == 0) select_one(res[w][0].s, k > 1 ? res[w][1].s : -INFINITY, res[w][0].g, p, invalid, cold, P, o, ty);
   }
   flush_tally(P, o, ty);
 }
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __r
         sid[t * kp + i] = res[i].g;
         ssc[t * kp + i] = res[i].s;
       }
-      select_one(res[0].s, k > 1 ? res[1].s : -INFINITY, p, invalid, cold, P, o, ty);
+      select_one(res[0].s, k > 1 ? res[1].s : -INFINITY, res[0].g, p, invalid, cold, P, o, ty);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < np * k; i += TP_THREADS) {   // coalesced global writes
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict
     if (o.topk_score) reinterpret_cast<float2*>(o.topk_score)[e] = make_float2(c0.s, c1.s);
     if (o.cand_out) reinterpret_cast<int4*>(o.cand_out)[e] = make_int4(__float_as_int(c0.s), c0.g,
                                                                        __float_as_int(c1.s), c1.g);
-    if (e == p * half) select_one(c0.s, c1.s, p, invalid, cold, P, o, ty);
+    if (e == p * half) select_one(c0.s, c1.s, c0.g, p, invalid, cold, P, o, ty);
   }
   flush_tally(P, o, ty);
 }

@@ -229,8 +229,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
-    // The whole warp walks the schedule (for the leash); lane 0 waits on the ring and issues TMA.
-    {
+    // Lane 0 waits on the ring and issues TMA; with the leash on, the whole warp walks the schedule
+    // (the look-up of the other CTAs' progress is warp-parallel).
+    if (slack || lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t issued = 0;
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
+          if (slack) __syncwarp();
         }
       }
       if (slack && leader && lane == 0)   // done: never hold anyone back

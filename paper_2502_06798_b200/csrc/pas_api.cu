@@ -112,6 +112,12 @@ struct pas_ctx {
   FcState* fc_state = nullptr;
   bool fc_stats_valid = false;
   uint32_t k2_epoch = 0;
+  // f2 LRU maintenance: stamps of every global slot (replicated on all ranks) + insert workspace
+  uint32_t* stamps = nullptr;
+  uint32_t lru_tick = 0;
+  LruSel* lru_sel = nullptr;
+  int32_t *lru_counts = nullptr, *lru_scanned = nullptr, *lru_scan_tmp = nullptr, *lru_victims = nullptr;
+  int32_t *ins_idx = nullptr, *ins_count = nullptr;
   uint8_t* level = nullptr;
   int* hist = nullptr;
   int* invalid_count = nullptr;
@@ -213,6 +219,8 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   }
   for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
   for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
+  p.lru_stamp = ctx->stamps;
+  p.lru_tick = ctx->lru_tick;
   return p;
 }
 
@@ -299,6 +307,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
 
 // a4 (final merge) .. a8 for all N prompts from S candidate blocks [S][N][k].
 pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
+  ctx->lru_tick++;   // f2 clock: one tick per routed batch (R26)
   RouteParams p = make_params(ctx, N);
   static_assert(sizeof(DevPlan) % 4 == 0, "DevPlan zeroed as int32 words");
   CUDA_TRY(ctx, launch_zero(ctx->hist, kMaxLevels, reinterpret_cast<int32_t*>(ctx->plan), sizeof(DevPlan) / 4,
@@ -374,6 +383,8 @@ pas_status pas_destroy(pas_ctx* ctx) {
     else g_nccl.CommDestroy(ctx->comm);
   }
   void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all, ctx->k2_progress, ctx->fc_ring, ctx->fc_state,
+                  ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
+                  ctx->ins_idx, ctx->ins_count,
                   ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
                   ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.sorted,    ctx->rw.cls7,
                   ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp, ctx->rw.scan_tmp,
@@ -431,6 +442,9 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
 #define ALLOC(ptr, n) \
   if (e == cudaSuccess) e = dmalloc(&(ptr), (size_t)(n))
   ALLOC(ctx->store, (ctx->cap_rows > 0 ? ctx->cap_rows : 1) * d);
+  ALLOC(ctx->stamps, (int64_t)cfg->world * (ctx->cap_rows > 0 ? ctx->cap_rows : 1));
+  if (e == cudaSuccess)
+    e = cudaMemset(ctx->stamps, 0, sizeof(uint32_t) * (size_t)cfg->world * (ctx->cap_rows > 0 ? ctx->cap_rows : 1));
   ALLOC(ctx->level, mb);
   ALLOC(ctx->hist, kMaxLevels);
   ALLOC(ctx->invalid_count, 1);
@@ -523,8 +537,114 @@ pas_status pas_cache_load(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64
   CUDA_TRY(ctx, cudaMemcpyAsync(&bad, ctx->invalid_count, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (bad) return fail(ctx, PAS_ERR_INVALID_ROWS, "%d of the rows are non-finite or have zero norm", bad);
+  ctx->lru_tick++;
+  CUDA_TRY(ctx, launch_fill_u32(ctx->stamps + ctx->M_total, M, ctx->lru_tick, st));
   ctx->M_total = new_total;
   ctx->M_local = new_local;
+  return PAS_OK;
+}
+
+namespace {
+
+pas_status ensure_lru_ws(pas_ctx* ctx) {
+  if (ctx->lru_sel) return PAS_OK;
+  const int64_t cap = (int64_t)ctx->cfg.world * ctx->cap_rows;
+  const int64_t span = cap > ctx->cfg.max_batch ? cap : ctx->cfg.max_batch;
+  const int64_t tiles = 2 * (int64_t)lru_tiles(span);
+  cudaError_t e = dmalloc(&ctx->lru_sel, 1);
+  if (e == cudaSuccess) e = dmalloc(&ctx->lru_counts, (size_t)tiles);
+  if (e == cudaSuccess) e = dmalloc(&ctx->lru_scanned, (size_t)tiles);
+  if (e == cudaSuccess) e = dmalloc(&ctx->lru_scan_tmp, (size_t)scan_tmp_ints(tiles));
+  if (e == cudaSuccess) e = dmalloc(&ctx->lru_victims, (size_t)ctx->cfg.max_batch);
+  if (e == cudaSuccess) e = dmalloc(&ctx->ins_idx, (size_t)ctx->cfg.max_batch);
+  if (e == cudaSuccess) e = dmalloc(&ctx->ins_count, 1);
+  if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "LRU workspace allocation failed: %s", cudaGetErrorString(e));
+  return PAS_OK;
+}
+
+// Rows already normalised in ctx->qhat (staged); src = staged row of insert i (nullptr: i).  R26/R27:
+// append at the free end first, then take the n_evict LRU slots in ascending gid order.
+pas_status insert_staged(pas_ctx* ctx, const int32_t* src, int64_t n, int32_t* gids_out, int32_t* gids_by_prompt,
+                         cudaStream_t st) {
+  const int G = ctx->cfg.world, rank = ctx->cfg.rank;
+  const int64_t cap = (int64_t)G * ctx->cap_rows;
+  if (n > cap) return fail(ctx, PAS_ERR_CAPACITY, "%lld rows exceed the store capacity %lld", (long long)n,
+                           (long long)cap);
+  ctx->lru_tick++;
+  const int64_t n_append = n < cap - ctx->M_total ? n : cap - ctx->M_total;
+  const int64_t n_evict = n - n_append;
+  if (n_evict > 0)
+    CUDA_TRY(ctx, launch_lru_victims(ctx->stamps, ctx->M_total, (int32_t)n_evict, ctx->lru_sel, ctx->lru_counts,
+                                     ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims, st));
+  CUDA_TRY(ctx, launch_store_rows(ctx->qhat, src, n, n_append, ctx->M_total, ctx->lru_victims, ctx->cfg.d, G, rank,
+                                  ctx->store, ctx->stamps, ctx->lru_tick, gids_out, gids_by_prompt, st));
+  ctx->M_total += n_append;
+  ctx->M_local = local_rows_below(ctx->M_total, G, rank);
+  ctx->last_local_N = -1;   // the staging buffers no longer hold the last routed batch
+  return PAS_OK;
+}
+
+}  // namespace
+
+pas_status pas_cache_insert(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64_t n, int32_t* gids_out,
+                            pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
+  if (n < 0 || (n > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / n");
+  if (n > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "n > max_batch (rows are staged like a batch)");
+  if (n == 0) return PAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;
+  if ((s = ensure_lru_ws(ctx))) return s;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->invalid_count, 0, sizeof(int), st));
+  CUDA_TRY(ctx, launch_normalize(rows, dtype, n, ctx->cfg.d, ctx->qhat, nullptr, 0, 1, 0, ctx->invalid_count, st));
+  int bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&bad, ctx->invalid_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (bad) return fail(ctx, PAS_ERR_INVALID_ROWS, "%d of the rows are non-finite or have zero norm", bad);
+  if ((s = insert_staged(ctx, nullptr, n, gids_out, nullptr, st))) return s;
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return PAS_OK;
+}
+
+pas_status pas_cache_insert_vanilla(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N,
+                                    const int32_t* K_prime, int32_t* gids_by_prompt, int64_t* n_inserted,
+                                    pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (n_inserted) *n_inserted = 0;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
+  if (N < 0 || (N > 0 && (!emb || !K_prime))) return fail(ctx, PAS_ERR_ARG, "bad emb / K_prime / N");
+  if (N > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "N > max_batch");
+  if (N == 0) return PAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;
+  if ((s = ensure_lru_ws(ctx))) return s;
+  // stage all N (validity flags; invalid prompts are skipped, R25), then compact K' == 0 in order
+  CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
+  CUDA_TRY(ctx, launch_vanilla_compact(K_prime, ctx->pflags, N, ctx->lru_counts, ctx->lru_scanned,
+                                       ctx->lru_scan_tmp, ctx->ins_idx, ctx->ins_count, gids_by_prompt, st));
+  int n = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&n, ctx->ins_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (n > 0 && (s = insert_staged(ctx, ctx->ins_idx, n, nullptr, gids_by_prompt, st))) return s;
+  ctx->last_local_N = -1;
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (n_inserted) *n_inserted = n;
+  return PAS_OK;
+}
+
+pas_status pas_cache_stamps(pas_ctx* ctx, uint32_t* stamps_dev, int64_t n, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!stamps_dev || n < 0 || n > (int64_t)ctx->cfg.world * ctx->cap_rows)
+    return fail(ctx, PAS_ERR_ARG, "bad stamps buffer / n");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaMemcpyAsync(stamps_dev, ctx->stamps, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice,
+                                (cudaStream_t)stream));
   return PAS_OK;
 }
 

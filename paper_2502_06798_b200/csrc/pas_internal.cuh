@@ -74,6 +74,8 @@ struct RouteParams {
   double F[kMaxLevels];          // load fractions
   double c[kTTotal];             // degradation c(dK)
   int inst_level[kMaxInst];      // level index of each serving instance
+  uint32_t* lru_stamp;           // f2: [global slots] last-use ticks (K4 stamps each usable top-1)
+  uint32_t lru_tick;             // this batch's tick
 };
 
 // Device-side plan + counters of one batch (K5 writes, pas_plan_stats reads).
@@ -178,6 +180,25 @@ cudaError_t launch_fc_sample(const uint8_t* level, const RouteParams& p, DevPlan
                              int32_t* K_prime, uint8_t* cls7, cudaStream_t st);
 cudaError_t launch_fc_window(const uint8_t* level, const RouteParams& p, DevPlan* plan, FcState* fcs,
                              uint8_t* ring, int window, cudaStream_t st);
+
+// f2 LRU maintenance of the store (R25-R27)
+struct LruSel {
+  uint32_t prefix, mask;   // radix-select state: the threshold stamp T after 4 passes
+  int32_t k;               // rank still needed inside the current prefix (after: r entries of stamp T)
+  int32_t pad;
+  int32_t hist[256];
+};
+int lru_tiles(int64_t M);
+cudaError_t launch_lru_victims(const uint32_t* stamps, int64_t M, int32_t n_evict, LruSel* sel, int32_t* counts,
+                               int32_t* scanned, int32_t* scan_tmp, int32_t* victims, cudaStream_t st);
+cudaError_t launch_store_rows(const __nv_bfloat16* staged, const int32_t* src, int64_t n, int64_t n_append,
+                              int64_t first_new, const int32_t* victims, int d, int G, int rank,
+                              __nv_bfloat16* store, uint32_t* stamps, uint32_t tick, int32_t* gids_out,
+                              int32_t* gids_by_prompt, cudaStream_t st);
+cudaError_t launch_fill_u32(uint32_t* a, int64_t n, uint32_t v, cudaStream_t st);
+cudaError_t launch_vanilla_compact(const int32_t* K_prime, const uint8_t* pflags, int64_t N, int32_t* counts,
+                                   int32_t* scanned, int32_t* scan_tmp, int32_t* idx, int32_t* count,
+                                   int32_t* gids_by_prompt, cudaStream_t st);
 
 // K7 route-and-batch
 struct BatchWs {

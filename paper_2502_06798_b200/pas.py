@@ -71,6 +71,9 @@ _SIG = {
     "pas_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "pas_cache_load": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(C.c_int64), _P]),
     "pas_cache_clear": (C.c_int, [_P]),
+    "pas_cache_insert": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
+    "pas_cache_insert_vanilla": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P, C.POINTER(C.c_int64), _P]),
+    "pas_cache_stamps": (C.c_int, [_P, _P, C.c_int64, _P]),
     "pas_cache_size": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pas_set_bands": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_float)]),
     "pas_set_degradation": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
@@ -188,6 +191,24 @@ def pas_set_seed(ctx, seed, batch_seq=0):
     _check(ctx, lib.pas_set_seed(ctx, seed, batch_seq))
 
 
+def pas_cache_insert(ctx, rows, gids_out=None, stream=None):
+    _check(ctx, lib.pas_cache_insert(ctx, _P(rows.data_ptr()), _dtype_code(rows), rows.shape[0],
+                                     _P(gids_out.data_ptr()) if gids_out is not None else None, _stream(stream)))
+
+
+def pas_cache_insert_vanilla(ctx, emb, K_prime, gids_by_prompt=None, stream=None) -> int:
+    n = C.c_int64(0)
+    _check(ctx, lib.pas_cache_insert_vanilla(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0],
+                                             _P(K_prime.data_ptr()),
+                                             _P(gids_by_prompt.data_ptr()) if gids_by_prompt is not None else None,
+                                             C.byref(n), _stream(stream)))
+    return n.value
+
+
+def pas_cache_stamps(ctx, out, stream=None):
+    _check(ctx, lib.pas_cache_stamps(ctx, _P(out.data_ptr()), out.numel(), _stream(stream)))
+
+
 def pas_set_forecast(ctx, window, replan_every=1):
     _check(ctx, lib.pas_set_forecast(ctx, window, replan_every))
 
@@ -290,6 +311,12 @@ class Router:
 
     def set_seed(self, seed, batch_seq=0):
         pas_set_seed(self.ctx, seed, batch_seq)
+
+    def insert(self, rows, gids_out=None, stream=None):
+        pas_cache_insert(self.ctx, rows, gids_out, stream)
+
+    def insert_vanilla(self, emb, K_prime, gids_by_prompt=None, stream=None) -> int:
+        return pas_cache_insert_vanilla(self.ctx, emb, K_prime, gids_by_prompt, stream)
 
     def set_forecast(self, window, replan_every=1):
         pas_set_forecast(self.ctx, window, replan_every)

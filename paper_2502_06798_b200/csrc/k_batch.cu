@@ -19,13 +19,14 @@
 //                prompts as 16 rows of 32 (coalesced loads and stores); row by row, match.any gives the
 //                lanes of one class, popc of those below a lane is its rank in the row, a per-warp
 //                running count per class carries the earlier rows; per block an exclusive prefix over
-//                the 8 warps.  Block 0 also turns the class totals into per-instance counts (closed
-//                form, greedy: each I_j[m] gets the t's whose (t div b*) mod n_j = m) and the offsets.
-//   k_bucket     scatter prompt ids to offsets[instance] + slot.
+//                the 8 warps.  Every block turns the class totals into per-instance counts (closed
+//                form, greedy: each I_j[m] gets the t's whose (t div b*) mod n_j = m) and batch-list
+//                offsets (W <= 64, in shared memory), so the same pass also scatters each prompt id to
+//                offsets[instance] + slot (the counting sort's scatter; block 0 publishes the offsets).
 // Measured alternatives (64M prompts, profiles/r01_stream): match.any counting is ADU-bound (98 %);
 // one ballot per class bit is slower still; the column scheme ranks slower than match.any (262 vs
 // 207 us); a single-pass decoupled look-back is 60 % slower than count + scan + rank.
-// HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 8 B read + 4 B written.
+// HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 4 B written.
 #include "pas_internal.cuh"
 
 namespace pas {
@@ -98,11 +99,12 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
 __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
-                                                      int32_t* __restrict__ slot, int32_t* __restrict__ off,
+                                                      int32_t* __restrict__ slot, int32_t* __restrict__ prompts,
                                                       int32_t* __restrict__ user_off) {
   pdl_entry();
   __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
+  __shared__ int32_t icount[kMaxInst], ioff[kMaxInst + 1];   // per-instance counts, batch-list offsets
   __shared__ uint64_t magic_s[kMaxLevels];
   __shared__ int32_t ninst_s[kMaxLevels];
   __shared__ int32_t ilist_s[kMaxLevels][kMaxInst];
@@ -124,7 +126,37 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
     const int64_t row = (int64_t)threadIdx.x * ntiles;
     tile_off[threadIdx.x] = scanned[row + tile] - scanned[row];
   }
+  if (threadIdx.x < P.W) {
+    // class totals (from the scanned counts) -> this instance's count (closed form, R13 / R14)
+    const int i = threadIdx.x;
+    const int cc = P.mode == PAS_UNIFORM ? i : P.inst_level[i];
+    const int64_t start = scanned[(int64_t)cc * ntiles];
+    const int64_t end = cc + 1 < nC ? scanned[(int64_t)(cc + 1) * ntiles] : P.N;
+    const int total = (int)(end - start);
+    int cnt = total;
+    if (P.mode != PAS_UNIFORM) {
+      int m = 0, nj = 0;   // position of i among the instances of its level, their number
+      for (int q = 0; q < P.W; ++q) {
+        m += (P.inst_level[q] == cc && q < i) ? 1 : 0;
+        nj += (P.inst_level[q] == cc) ? 1 : 0;
+      }
+      const int b = P.bstar, full = total / (b * nj), rem = total % (b * nj), extra = rem - m * b;
+      cnt = full * b + (extra < 0 ? 0 : (extra > b ? b : extra));
+    }
+    icount[i] = cnt;
+  }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i <= P.W; ++i) {
+      ioff[i] = run;
+      if (tile == 0) {
+        if (user_off) user_off[i] = run;
+        if (i < P.W) plan->inst_count[i] = icount[i];
+      }
+      if (i < P.W) run += icount[i];
+    }
+  }
   // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count
   // per class (bumped by the lowest lane of each group) carries the earlier rows
   const unsigned lt = (1u << lane) - 1;
@@ -168,56 +200,7 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
     }
     instance[p] = inst;
     slot[p] = sl;
-  }
-  if (tile == 0 && threadIdx.x == 0) {
-    // class totals (from the scanned counts) -> per-instance counts (closed form) -> offsets
-    int count[kMaxInst];
-    for (int i = 0; i < P.W; ++i) count[i] = 0;
-    for (int cc = 0; cc < nC; ++cc) {
-      const int64_t start = scanned[(int64_t)cc * ntiles];
-      const int64_t end = cc + 1 < nC ? scanned[(int64_t)(cc + 1) * ntiles] : P.N;
-      const int total = (int)(end - start);
-      if (P.mode == PAS_UNIFORM) {
-        count[cc] = total;
-      } else {
-        const int nj = plan->n_inst[cc], b = P.bstar;
-        if (nj == 0) continue;
-        const int full = total / (b * nj), rem = total % (b * nj);
-        for (int m = 0; m < nj; ++m) {
-          const int extra = rem - m * b;
-          count[plan->inst_list[cc][m]] = full * b + (extra < 0 ? 0 : (extra > b ? b : extra));
-        }
-      }
-    }
-    int run = 0;
-    for (int i = 0; i <= P.W; ++i) {
-      off[i] = run;
-      if (user_off) user_off[i] = run;
-      if (i < P.W) {
-        plan->inst_count[i] = count[i];
-        run += count[i];
-      }
-    }
-  }
-}
-
-// 4 prompts per thread (16-byte loads of instance and slot), scattered 4-byte stores.
-__global__ void k_bucket(const int32_t* __restrict__ instance, const int32_t* __restrict__ slot, int64_t N,
-                         const int32_t* __restrict__ off, int32_t* __restrict__ prompts) {
-  pdl_entry();
-  __shared__ int32_t soff[NCLS + 1];
-  if (threadIdx.x <= NCLS) soff[threadIdx.x] = off[threadIdx.x];
-  __syncthreads();
-  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (p0 + 3 < N) {
-    const int4 in = __ldg(reinterpret_cast<const int4*>(instance + p0));
-    const int4 sl = __ldg(reinterpret_cast<const int4*>(slot + p0));
-    prompts[soff[in.x] + sl.x] = (int32_t)p0;
-    prompts[soff[in.y] + sl.y] = (int32_t)(p0 + 1);
-    prompts[soff[in.z] + sl.z] = (int32_t)(p0 + 2);
-    prompts[soff[in.w] + sl.w] = (int32_t)(p0 + 3);
-  } else {
-    for (int64_t p = p0; p < N; ++p) prompts[soff[instance[p]] + slot[p]] = (int32_t)p;
+    if (prompts) prompts[ioff[inst] + sl] = (int32_t)p;   // the batch lists (counting-sort scatter)
   }
 }
 
@@ -244,12 +227,8 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
   cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, nclasses * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
   launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot,
-             w.offsets, bucket_offsets);
+             bucket_prompts, bucket_offsets);
   *launches += 2;
-  if (bucket_prompts) {
-    launch_pdl(k_bucket, (unsigned)((p.N + 1023) / 1024), 256, 0, st, instance, slot, p.N, w.offsets, bucket_prompts);
-    *launches += 1;
-  }
   return cudaGetLastError();
 }
 

@@ -103,7 +103,9 @@ __device__ __forceinline__ void select_one(float s1, float s2, int32_t g1, int64
     if ((lvl > 0 && s1 - P.thr[lvl - 1] < 2e-2f) || (lvl < P.nK - 1 && P.thr[lvl] - s1 < 2e-2f))
       fl |= PAS_FLAG_NEAR_THRESHOLD;
   }
-  if (P.lru_stamp && !invalid && !cold && g1 >= 0) P.lru_stamp[g1] = P.lru_tick;   // f2: top-1 reused (R26)
+  // f2: the top-1 entry is the one whose state is reused (R26); gids outside the store (e.g. from a
+  // caller's candidate lists) are ignored
+  if (P.lru_stamp && !invalid && !cold && g1 >= 0 && g1 < P.M_total) P.lru_stamp[g1] = P.lru_tick;
   o.level[p] = (uint8_t)lvl;
   o.K[p] = P.grid[lvl];
   if (o.flags) o.flags[p] = fl;

@@ -25,10 +25,9 @@ def algorithmic_bytes(N, S, k, d, W, M):
         "k_merge_select_thr": N * (S * k * 8 + k * 8 + 4 + 1 + 1),
         "k_keys": N * (1 + 8 + 4),
         "k_scatter": N * (4 + 4),
-        "k_rank": N * (4 + 8 + 1 + 4 + 4 + 4 + 4 + 8),
-        "k_cls_count": N * 4,
-        "k_cls_rank": N * (4 + 4 + 4),
-        "k_bucket": N * (4 + 4 + 4),
+        "k_rank": N * (8 + 4 + 1 + 4),        # read the entry, K' (int32) + class byte written (+ in-bucket reads)
+        "k_cls_count": N * 1,                  # class byte
+        "k_cls_rank": N * (1 + 4 + 4 + 4),     # class byte; instance, slot, bucket-list entry
     }
 
 

@@ -25,7 +25,9 @@
 //                offsets[instance] + slot (the counting sort's scatter; block 0 publishes the offsets).
 // Measured alternatives (64M prompts, profiles/r01_stream): match.any counting is ADU-bound (98 %);
 // one ballot per class bit is slower still; the column scheme ranks slower than match.any (262 vs
-// 207 us); a single-pass decoupled look-back is 60 % slower than count + scan + rank.
+// 207 us); 16 consecutive prompts per thread with register-packed counters and a shuffle scan
+// ranks without votes but scatters the batch lists far worse (463 vs 305 us with the scatter); a
+// single-pass decoupled look-back is 60 % slower than count + scan + rank.
 // HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 4 B written.
 #include "pas_internal.cuh"
 

@@ -6,11 +6,11 @@
 // owns one prompt row of the accumulator and keeps the k best (score desc, gid asc; R10) over the
 // cache range of its work unit.
 //
-// Two tile organisations share one source (compile-time PAS_K2_PAIR; DESIGN.md section 8 records the
-// A/B on one B200 under its 1 kW power cap):
-//   single CTA (default)  tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
+// Two tile organisations share one source (template parameter), dispatched by batch size
+// (simtopk_pair; DESIGN.md section 8 records the A/B on one B200):
+//   single CTA (N > 2048) tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
 //                         instruction; per stage A 128x64 + B 256x64 bf16 (48 KB), 4 stages.
-//   CTA pair              tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
+//   CTA pair (N <= 2048)  tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
 //                         128..255 in CTA 1; the 256 cache rows of B split 128/128 between the two
 //                         CTAs' smem (32 KB / stage, 6 stages); TMA bytes of both CTAs land on the
 //                         leader's mbarrier; commits multicast to both CTAs.
@@ -23,8 +23,8 @@
 // range in the same wave re-use each tile from L2 only while they stay within L2's reach of each
 // other; free-running, they drift apart by more than that over a range of thousands of tiles and
 // tiles are fetched from DRAM again and again (C4: 491 GB of DRAM reads per launch for a 15.4 GB
-// cache).  So each producer warp publishes its tile
-// count (epoch-tagged, one 8-B word per CTA) and, before issuing a tile, waits until it is at most
+// cache).  So each producer warp publishes its tile count (epoch-tagged, one 8-B word per CTA or
+// pair) and, before issuing a tile, waits until it is at most
 // `slack` tiles ahead of the slowest CTA still working; slack is sized so that the tiles between
 // the slowest and the fastest CTA of every concurrently streamed range fit in a share of L2.
 //
@@ -43,32 +43,39 @@
 #include "pas_internal.cuh"
 #include "ptx_sm100.cuh"
 
-#ifndef PAS_K2_PAIR
-#define PAS_K2_PAIR 0
+// Shape-dispatched tile: the CTA pair (cta_group::2) for N <= PAS_K2_PAIR_MAX_TILES x 128 prompts,
+// the single-CTA tile above that (A/B in DESIGN.md 8: the pair is faster where K2 is latency- and
+// L2-bound, the single CTA where it is power-bound).  0 disables the pair; a huge value forces it.
+#ifndef PAS_K2_PAIR_MAX_TILES
+#define PAS_K2_PAIR_MAX_TILES 16
 #endif
 
 namespace pas {
 namespace {
 
-constexpr bool PAIR = PAS_K2_PAIR != 0;
-constexpr int CTAS = PAIR ? 2 : 1;
 constexpr int BM = 128;                 // prompt rows per CTA
 constexpr int BN = 256;                 // cache rows per tile (MMA N)
-constexpr int BN_CTA = BN / CTAS;       // cache rows staged per CTA
 constexpr int BK = 64;                  // one 128-B swizzle row of bf16
-constexpr int STAGES = PAIR ? 6 : 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN_CTA * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
 constexpr int EPI_WARPS = 8;                     // 2 per TMEM lane quarter: column halves
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_WORKERS = kNumSMs / CTAS;      // persistent CTAs (or pairs)
-constexpr int UNIT_ROWS = BM * CTAS;             // prompt rows per work unit
 constexpr int LIST_BYTES = BM * 16 * 8;             // hand-over of the upper half's lists (KMAX <= 16)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + LIST_BYTES;
 constexpr int WARMUP_TILES = 24;
 
+template <bool P>
+struct Tile {
+  static constexpr int CTAS = P ? 2 : 1;
+  static constexpr int BN_CTA = BN / CTAS;           // cache rows staged per CTA
+  static constexpr int STAGES = P ? 6 : 4;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
+  static constexpr int NUM_WORKERS = kNumSMs / CTAS;      // persistent CTAs (or pairs)
+  static constexpr int UNIT_ROWS = BM * CTAS;             // prompt rows per work unit
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + LIST_BYTES;
+};
+
+template <int STAGES>
 struct __align__(8) Bars {
   uint64_t full[STAGES];    // TMA bytes landed (leader's barrier in pair mode)
   uint64_t empty[STAGES];   // MMA finished reading the stage
@@ -178,16 +185,19 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
 
-template <int KMAX, bool DUMP>
+template <int KMAX, bool DUMP, bool PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack) {
+  using TL = Tile<PAIR>;
+  constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
+                B_BYTES = TL::B_BYTES, STAGE_BYTES = TL::STAGE_BYTES, UNIT_ROWS = TL::UNIT_ROWS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  Bars<STAGES>* bars = reinterpret_cast<Bars<STAGES>*>(smem + STAGES * STAGE_BYTES);
   float* list_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [BM][KMAX]
   int32_t* list_g = reinterpret_cast<int32_t*>(list_s + BM * KMAX);            // [BM][KMAX]
 
@@ -601,12 +611,14 @@ cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream
   return cudaGetLastError();
 }
 
-template <int KMAX, bool DUMP>
+template <int KMAX, bool DUMP, bool PAIR>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
+  using TL = Tile<PAIR>;
+  constexpr int CTAS = TL::CTAS;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = TL::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -617,7 +629,8 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP>, *a.tmap_q, *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR>, *a.tmap_q, PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N,
+                            a.M_local, a.d / BK, a.k, a.G,
                             a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack);
 }
 
@@ -626,11 +639,12 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
 #ifndef PAS_K2_ATMEM   // A-in-TMEM variant: correct, but 29 % slower under the power cap
 #define PAS_K2_ATMEM 0
 #endif
-bool simtopk_uses_tmem_a(int d) { return PAS_K2_ATMEM && !PAIR && d <= 2 * TA_ACC_COL; }
-size_t simtopk_smem_bytes() { return SMEM_BYTES; }
-int simtopk_prompt_rows() { return UNIT_ROWS; }
+bool simtopk_uses_tmem_a(int d) { return PAS_K2_ATMEM && d <= 2 * TA_ACC_COL; }
+bool simtopk_pair(int64_t N, int d) { return !simtopk_uses_tmem_a(d) && (N + BM - 1) / BM <= PAS_K2_PAIR_MAX_TILES; }
+int simtopk_prompt_rows() { return Tile<true>::UNIT_ROWS; }   // prompt buffers are padded to whole pair tiles
 int simtopk_box_q() { return BM; }
-int simtopk_box_c(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : BN_CTA; }
+int simtopk_box_c(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : Tile<false>::BN_CTA; }
+int simtopk_box_c_pair() { return Tile<true>::BN_CTA; }
 static int tile_rows(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : BN; }
 
 // Opt the kernel variants into > 48 KB dynamic shared memory on the current device.
@@ -639,9 +653,12 @@ cudaError_t simtopk_init() {
   if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk_ta<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES))) return e;
-  return cudaFuncSetAttribute(k_simtopk<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const int ss = Tile<false>::SMEM_BYTES, pr = Tile<true>::SMEM_BYTES;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
+  return cudaFuncSetAttribute(k_simtopk<16, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
 }
 
 // Pick the number of cache ranges R so that (prompt tiles x R) units fill the persistent workers with
@@ -650,6 +667,9 @@ cudaError_t simtopk_init() {
 // nearly every 32-column chunk of some lane takes the insert path (P(insert) ~ 32 k / columns seen),
 // which makes the first ~8k columns of a unit epilogue-bound rather than MMA-bound.
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d) {
+  const bool pair = simtopk_pair(N, d);
+  const int UNIT_ROWS = pair ? Tile<true>::UNIT_ROWS : Tile<false>::UNIT_ROWS;
+  const int NUM_WORKERS = pair ? Tile<true>::NUM_WORKERS : Tile<false>::NUM_WORKERS;
   const int64_t MT = (N + UNIT_ROWS - 1) / UNIT_ROWS;
   const int64_t NT = (M_local + tile_rows(d) - 1) / tile_rows(d);
   const double warmup = (double)WARMUP_TILES * BN / tile_rows(d);
@@ -689,6 +709,10 @@ uint32_t simtopk_leash_slack(int MT, int NT, int R, int workers) {
 }
 
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
+  const bool pair = !a.dump && simtopk_pair(a.N, a.d);
+  const int UNIT_ROWS = pair ? Tile<true>::UNIT_ROWS : Tile<false>::UNIT_ROWS;
+  const int NUM_WORKERS = pair ? Tile<true>::NUM_WORKERS : Tile<false>::NUM_WORKERS;
+  const int CTAS = pair ? 2 : 1;
   const int MT = (int)((a.N + UNIT_ROWS - 1) / UNIT_ROWS);
   const int NT = (int)((a.M_local + tile_rows(a.d) - 1) / tile_rows(a.d));
   if (MT == 0 || NT == 0) return cudaSuccess;
@@ -700,10 +724,14 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
     if (a.k <= 8) return launch_ta<8, false>(a, MT, NT, grid, st);
     return launch_ta<16, false>(a, MT, NT, grid, st);
   }
-  const uint32_t slack = a.progress ? simtopk_leash_slack(MT, NT, a.R, grid / CTAS) : 0;
-  if (a.dump) return launch_variant<8, true>(a, MT, NT, grid, slack, st);
-  if (a.k <= 8) return launch_variant<8, false>(a, MT, NT, grid, slack, st);
-  return launch_variant<16, false>(a, MT, NT, grid, slack, st);
+  const uint32_t slack = a.progress ? simtopk_leash_slack(MT, NT, a.R, workers) : 0;
+  if (a.dump) return launch_variant<8, true, false>(a, MT, NT, grid, slack, st);
+  if (pair) {
+    if (a.k <= 8) return launch_variant<8, false, true>(a, MT, NT, grid, slack, st);
+    return launch_variant<16, false, true>(a, MT, NT, grid, slack, st);
+  }
+  if (a.k <= 8) return launch_variant<8, false, false>(a, MT, NT, grid, slack, st);
+  return launch_variant<16, false, false>(a, MT, NT, grid, slack, st);
 }
 
 }  // namespace pas

@@ -12,9 +12,6 @@
 
 #include "pas_internal.cuh"
 
-#ifndef PAS_K2_PAIR
-#define PAS_K2_PAIR 0
-#endif
 
 using namespace pas;
 
@@ -131,7 +128,7 @@ struct pas_ctx {
   float* s_tsc = nullptr;
   uint8_t* s_flags = nullptr;
   // tensor maps
-  CUtensorMap tm_q{}, tm_c{};
+  CUtensorMap tm_q{}, tm_c{}, tm_c2{};
   // comm
   ncclComm_t comm = nullptr;
   // timing
@@ -284,7 +281,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
       if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
     }
     if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
-    SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
+    SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
                   ctx->qhat, ctx->cand_local, nullptr, getenv("PAS_K2_NOLEASH") ? nullptr : ctx->k2_progress,
                   ctx->k2_epoch};
     CUDA_TRY(ctx, launch_simtopk(a, st));
@@ -358,7 +355,9 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
 // ----------------------------------------------------------------------------------------------
 extern "C" {
 
-const char* pas_version(void) { return PAS_K2_PAIR ? "libpas 0.3 (sm_100a, tcgen05 K2 cta_group::2 256x256)" : "libpas 0.3 (sm_100a, tcgen05 K2 cta_group::1 128x256)"; }
+const char* pas_version(void) {
+  return "libpas 0.4 (sm_100a; K2 tcgen05 cta_group::1 128x256, cta_group::2 256x256 for small batches)";
+}
 
 const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
 
@@ -471,7 +470,8 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
     }
-  if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c((int)d))) {
+  if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c((int)d)) ||
+      !encode_map(&ctx->tm_c2, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c_pair())) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed");
   }
@@ -951,7 +951,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
-  SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
+  SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
                 ctx->qhat, ctx->cand_local, scores_dev, nullptr, 0};
   CUDA_TRY(ctx, launch_simtopk(a, st));
   return PAS_OK;

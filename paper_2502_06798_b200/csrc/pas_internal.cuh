@@ -106,6 +106,7 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
 struct SimTopkArgs {
   const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x simtopk_box_q(), SW128
   const CUtensorMap* tmap_c;      // [rows_c x d] bf16, box 64 x simtopk_box_c(), SW128
+  const CUtensorMap* tmap_c_pair; // the same store, box 64 x simtopk_box_c_pair() (CTA-pair tile)
   int64_t N;                      // prompts
   int64_t M_local;                // valid store rows on this rank
   int d, k, G, rank, R;           // R cache ranges per prompt tile
@@ -118,11 +119,12 @@ struct SimTopkArgs {
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 bool simtopk_uses_tmem_a(int d);
-size_t simtopk_smem_bytes();
+bool simtopk_pair(int64_t N, int d);   // the CTA-pair tile serves this batch size
 cudaError_t simtopk_init();
 int simtopk_prompt_rows();   // prompt rows per work unit (pair tile)
 int simtopk_box_q();         // TMA box rows of the prompt map
 int simtopk_box_c(int d);    // TMA box rows of the cache map
+int simtopk_box_c_pair();    // TMA box rows of the cache map for the CTA-pair tile
 
 // K3 (+K4 when final): merge [S][N][k] -> [N][k]
 cudaError_t launch_merge(const Cand* in, int S, int64_t N, int k, Cand* out, cudaStream_t st);

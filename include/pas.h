@@ -60,6 +60,9 @@ typedef enum { PAS_GREEDY = 0, PAS_UNIFORM = 1 } pas_mode;  /* P:104 high / low 
 #define PAS_T_TOTAL 50           /* total denoising steps */
 #define PAS_MAX_FORECAST_WINDOW (1 << 22)   /* f1 predictor window (paper: 1000) */
 #define PAS_MAX_TOPK 16
+#define PAS_NEVER_BUSY (-(INT64_C(1) << 62))  /* f3: busy-until of an instance that never fired */
+#define PAS_MAX_TIME_US (INT64_C(1) << 52)    /* f3: clock and timeout range (us) */
+#define PAS_MAX_SERVICE_US (INT64_C(1) << 26) /* f3: batch service time range (us, ~67 s) */
 #define PAS_NCCL_ID_BYTES 128
 
 /* Flags per prompt (pas_route_out.flags), informational; the oracle grades with its own. */
@@ -125,6 +128,13 @@ typedef struct {
   int64_t n_unforecast;                         /* prompts of a level the forecast gave no mass (R23) */
   uint64_t fc_Hc[PAS_MAX_LEVELS + 1];           /* cumulative forecast mass, units of 2^-32 */
   uint64_t fc_Fc[PAS_MAX_LEVELS + 1];           /* cumulative F, units of 2^-32 */
+  /* stateful dispatcher (pas_set_dispatcher; all zero when off): the state AFTER the last batch */
+  int dispatcher;                               /* 1 if the last batch went through the stateful dispatcher */
+  int64_t now_us;                               /* its arrival time */
+  int64_t queue_len[PAS_MAX_INSTANCES];         /* prompts waiting per instance */
+  int64_t busy_until_us[PAS_MAX_INSTANCES];     /* PAS_NEVER_BUSY if the instance never fired */
+  int64_t fired_prompts[PAS_MAX_INSTANCES];     /* cumulative since pas_set_dispatcher */
+  int64_t fired_batches[PAS_MAX_INSTANCES];
 } pas_stats;
 
 /* Library and build identification ("sm_100a", version). Never fails. */
@@ -219,6 +229,40 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
  * Errors: PAS_ERR_ARG (window outside [0, PAS_MAX_FORECAST_WINDOW], replan_every < 1), PAS_ERR_STATE,
  * PAS_ERR_CUDA. */
 pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every);
+
+/* NEXT f3, the stateful load-aware dispatcher (
+ * DESIGN.md R28-R32).  service_us != NULL switches route-and-batch (a8) from the stateless packing
+ * (R13 / R14) to per-instance queues kept on the device across batches: waiting prompts Q_w,
+ * busy-until B_w, service time s_w per batch (service_us[w], 1..PAS_MAX_SERVICE_US), batch timeout
+ * timeout_us (Delta, 0..PAS_MAX_TIME_US; SPEC's default 250000).  Time is integer microseconds.
+ * Each routed batch arrives at the clock set by pas_set_clock (R28) and is dispatched atomically:
+ *   - the form_batch events since the previous batch happen first (R30: an idle instance fires
+ *     min(Q, b*) prompts when Q >= b* or its oldest prompt has waited Delta; busy for s_w);
+ *   - greedy (R29): the longest queue below b* (ties: lowest id), else the instance whose next batch
+ *     starts soonest, max(B_w, now) + floor(Q_w / b*) s_w (ties: lowest id); uniform: as R14;
+ *   - slot (pas_route_out.slot) = the prompt's position in its instance's queue, counting the prompts
+ *     still waiting from earlier batches (R31); batch lists: this batch's prompts per instance;
+ *   - then idle instances fire at `now`.
+ * W must equal pas_set_fractions' W and b* <= 64 while the dispatcher is on.  Resets the state
+ * (empty queues, never busy, clock 0).  service_us == NULL turns it off.  Synchronous.
+ * Errors: PAS_ERR_STATE (no fractions), PAS_ERR_ARG, PAS_ERR_CUDA. */
+pas_status pas_set_dispatcher(pas_ctx* ctx, const int64_t* service_us, int W, int64_t timeout_us);
+
+/* Arrival time (us) of the next routed batch: >= the previous batch's, <= PAS_MAX_TIME_US.  Batches
+ * routed without a new pas_set_clock arrive at the same instant as the previous one.
+ * Errors: PAS_ERR_STATE (dispatcher off), PAS_ERR_ARG. */
+pas_status pas_set_clock(pas_ctx* ctx, int64_t now_us);
+
+/* Load-mode switch (R32): utilisation u = lambda_rps / capacity with capacity =
+ * sum_w bstar_high / s_w; uniform -> greedy when u > 0.8, greedy -> uniform when u < 0.7.  Sets the
+ * mode and b* (bstar_high or 1) for the next batches; F and the instance levels are kept.
+ * mode_out (optional) receives the mode.  Errors: PAS_ERR_STATE (dispatcher off), PAS_ERR_ARG. */
+pas_status pas_set_load(pas_ctx* ctx, double lambda_rps, int bstar_high, pas_mode* mode_out);
+
+/* Current dispatcher state (host arrays of W entries, each optional).  Synchronises the device.
+ * Errors: PAS_ERR_STATE (dispatcher off), PAS_ERR_CUDA. */
+pas_status pas_dispatcher_state(pas_ctx* ctx, int64_t* queue_len, int64_t* busy_until_us, int64_t* fired_prompts,
+                                int64_t* fired_batches);
 
 /* Reset the Philox key and the batch sequence number (R18). */
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);

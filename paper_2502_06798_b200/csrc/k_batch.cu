@@ -29,7 +29,7 @@
 // ranks without votes but scatters the batch lists far worse (463 vs 305 us with the scatter); a
 // single-pass decoupled look-back is 60 % slower than count + scan + rank.
 // HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 4 B written.
-#include "pas_internal.cuh"
+#include "dispatch.cuh"
 
 namespace pas {
 namespace {
@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
   }
 }
 
+template <bool DISP>   // DISP: the f3 stateful dispatcher picks (a separate instantiation keeps R13 lean)
 __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
@@ -136,7 +137,9 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
     const int64_t end = cc + 1 < nC ? scanned[(int64_t)(cc + 1) * ntiles] : P.N;
     const int total = (int)(end - start);
     int cnt = total;
-    if (P.mode != PAS_UNIFORM) {
+    if (DISP) {
+      cnt = P.dplan->cnt[i];   // f3: counted by k_disp_prep from the same class totals
+    } else if (P.mode != PAS_UNIFORM) {
       int m = 0, nj = 0;   // position of i among the instances of its level, their number
       for (int q = 0; q < P.W; ++q) {
         m += (P.inst_level[q] == cc && q < i) ? 1 : 0;
@@ -187,8 +190,18 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
     const int64_t p = base + 32 * j + lane;
     if (c[j] < 0) continue;
     const int t = tile_off[c[j]] + wcnt[w][c[j]] + r[j];
-    int inst, sl;
-    if (P.mode == PAS_UNIFORM) {
+    int inst, sl, pos;
+    if (DISP) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
+      int64_t sl64;
+      if (P.mode == PAS_UNIFORM) {
+        inst = c[j];
+        sl64 = P.dplan->Q0[inst] + t;
+      } else {
+        disp_pick_greedy(P.dplan, ilist_s[c[j]], ninst_s[c[j]], c[j], t, P.bstar, inst, sl64);
+      }
+      sl = (int)sl64;
+      pos = (int)(sl64 - P.dplan->Q0[inst]);
+    } else if (P.mode == PAS_UNIFORM) {
       inst = c[j];
       sl = t;
     } else {
@@ -200,9 +213,10 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
       inst = ilist_s[c[j]][q1 - q2 * (uint32_t)ninst_s[c[j]]];
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
+    if (!DISP) pos = sl;
     instance[p] = inst;
     slot[p] = sl;
-    if (prompts) prompts[ioff[inst] + sl] = (int32_t)p;   // the batch lists (counting-sort scatter)
+    if (prompts) prompts[ioff[inst] + pos] = (int32_t)p;   // the batch lists (counting-sort scatter)
   }
 }
 
@@ -228,8 +242,13 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
   launch_pdl(k_cls_count, ntiles, THREADS, smem, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
   cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, nclasses * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
-  launch_pdl(k_cls_rank, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot,
-             bucket_prompts, bucket_offsets);
+  if (p.disp) {   // f3: queue events since the last batch, pick tables, counts, state after
+    e = launch_disp_prep(p, ntiles, nclasses, w.blk_off, st);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+  }
+  launch_pdl(p.disp ? k_cls_rank<true> : k_cls_rank<false>, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses,
+             w.blk_off, plan, instance, slot, bucket_prompts, bucket_offsets);
   *launches += 2;
   return cudaGetLastError();
 }

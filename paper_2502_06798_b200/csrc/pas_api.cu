@@ -109,6 +109,13 @@ struct pas_ctx {
   FcState* fc_state = nullptr;
   bool fc_stats_valid = false;
   uint32_t k2_epoch = 0;
+  // f3 stateful dispatcher (R28-R32); off = the stateless packing R13 / R14
+  bool disp_on = false, disp_stats_valid = false;
+  int disp_W = 0, disp_bstar_prev = 1, load_mode = PAS_UNIFORM;
+  int64_t disp_now = 0, disp_last = 0, disp_timeout = 0;
+  int64_t disp_svc[kMaxInst] = {};
+  DispState* dstate = nullptr;
+  DispPlan* dplan = nullptr;
   // f2 LRU maintenance: stamps of every global slot (replicated on all ranks) + insert workspace
   uint32_t* stamps = nullptr;
   uint32_t lru_tick = 0;
@@ -218,6 +225,12 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
   p.lru_stamp = ctx->stamps;
   p.lru_tick = ctx->lru_tick;
+  p.disp = ctx->disp_on ? 1 : 0;
+  p.bstar_prev = ctx->disp_bstar_prev;
+  p.now_us = ctx->disp_now;
+  p.timeout_us = ctx->disp_timeout;
+  p.dstate = ctx->dstate;
+  p.dplan = ctx->dplan;
   return p;
 }
 
@@ -345,6 +358,11 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   ctx->last_stream = st;
   ctx->last_N = N;
   ctx->batch_seq++;
+  ctx->disp_stats_valid = ctx->disp_on;
+  if (ctx->disp_on) {   // R28: the events until the next batch follow this batch's policy
+    ctx->disp_bstar_prev = ctx->bstar;
+    ctx->disp_last = ctx->disp_now;
+  }
   return PAS_OK;
 }
 
@@ -382,6 +400,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
     else g_nccl.CommDestroy(ctx->comm);
   }
   void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all, ctx->k2_progress, ctx->fc_ring, ctx->fc_state,
+                  ctx->dstate, ctx->dplan,
                   ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
                   ctx->ins_idx, ctx->ins_count,
                   ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
@@ -751,11 +770,15 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
   for (int j = 0; j < ctx->nK; ++j)
     if (F[j] > 0.0 && !has[j])
       return fail(ctx, PAS_ERR_NO_INSTANCE, "F[%d] > 0 but no instance runs level %d (S:309)", j, j);
+  if (ctx->disp_on && (W != ctx->disp_W || bstar > kArrRing))
+    return fail(ctx, PAS_ERR_ARG, "the stateful dispatcher needs W = %d (as set) and bstar <= %d", ctx->disp_W,
+                kArrRing);
   for (int j = 0; j < kMaxLevels; ++j) ctx->F[j] = j < ctx->nK ? F[j] : 0.0;
   for (int w = 0; w < kMaxInst; ++w) ctx->inst_level[w] = w < W ? instance_level[w] : 0;
   ctx->W = W;
   ctx->bstar = bstar;
   ctx->mode = mode;
+  ctx->load_mode = mode;
   ctx->fractions_set = true;
   return PAS_OK;
 }
@@ -765,6 +788,97 @@ pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq) {
   if (s) return s;
   ctx->seed = seed;
   ctx->batch_seq = batch_seq;
+  return PAS_OK;
+}
+
+pas_status pas_set_dispatcher(pas_ctx* ctx, const int64_t* service_us, int W, int64_t timeout_us) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!service_us) {   // back to the stateless packing
+    ctx->disp_on = false;
+    ctx->disp_stats_valid = false;
+    return PAS_OK;
+  }
+  if (!ctx->fractions_set) return fail(ctx, PAS_ERR_STATE, "pas_set_fractions must precede pas_set_dispatcher");
+  if (W != ctx->W) return fail(ctx, PAS_ERR_ARG, "W = %d differs from the W = %d of pas_set_fractions", W, ctx->W);
+  if (ctx->bstar > kArrRing) return fail(ctx, PAS_ERR_ARG, "the stateful dispatcher needs bstar <= %d", kArrRing);
+  if (timeout_us < 0 || timeout_us > PAS_MAX_TIME_US) return fail(ctx, PAS_ERR_ARG, "timeout_us outside [0, 2^52]");
+  for (int w = 0; w < W; ++w)
+    if (service_us[w] < 1 || service_us[w] > PAS_MAX_SERVICE_US)
+      return fail(ctx, PAS_ERR_ARG, "service_us[%d] outside [1, 2^26]", w);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if (!ctx->dstate) {
+    cudaError_t e = dmalloc(&ctx->dstate, 1);
+    if (e == cudaSuccess) e = dmalloc(&ctx->dplan, 1);
+    CUDA_TRY(ctx, e);
+  }
+  DispState* h = new DispState();   // ~40 KB: not on the stack
+  for (int w = 0; w < kMaxInst; ++w) {
+    h->B[w] = kNeverBusy;
+    h->svc[w] = w < W ? service_us[w] : 1;
+  }
+  cudaError_t e = cudaMemcpy(ctx->dstate, h, sizeof(DispState), cudaMemcpyHostToDevice);
+  delete h;
+  CUDA_TRY(ctx, e);
+  for (int w = 0; w < kMaxInst; ++w) ctx->disp_svc[w] = w < W ? service_us[w] : 0;
+  ctx->disp_on = true;
+  ctx->disp_stats_valid = false;
+  ctx->disp_W = W;
+  ctx->disp_timeout = timeout_us;
+  ctx->disp_now = ctx->disp_last = 0;
+  ctx->disp_bstar_prev = ctx->bstar;
+  return PAS_OK;
+}
+
+pas_status pas_set_clock(pas_ctx* ctx, int64_t now_us) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->disp_on) return fail(ctx, PAS_ERR_STATE, "pas_set_clock needs pas_set_dispatcher");
+  if (now_us < ctx->disp_last || now_us > PAS_MAX_TIME_US)
+    return fail(ctx, PAS_ERR_ARG, "now_us = %lld must be in [last batch = %lld, 2^52]", (long long)now_us,
+                (long long)ctx->disp_last);
+  ctx->disp_now = now_us;
+  return PAS_OK;
+}
+
+pas_status pas_set_load(pas_ctx* ctx, double lambda_rps, int bstar_high, pas_mode* mode_out) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->disp_on) return fail(ctx, PAS_ERR_STATE, "pas_set_load needs pas_set_dispatcher (service times)");
+  if (!(lambda_rps >= 0.0) || !std::isfinite(lambda_rps)) return fail(ctx, PAS_ERR_ARG, "lambda must be finite, >= 0");
+  if (bstar_high < 1 || bstar_high > kArrRing) return fail(ctx, PAS_ERR_ARG, "bstar_high outside [1, %d]", kArrRing);
+  // R32: capacity at the optimal batch size; low -> high above 0.8, high -> low below 0.7
+  double cap = 0.0;
+  for (int w = 0; w < ctx->W; ++w) cap += (double)bstar_high / ((double)ctx->disp_svc[w] * 1e-6);
+  const double u = lambda_rps / cap;
+  int mode = ctx->load_mode;
+  if (mode == PAS_UNIFORM) mode = u > 0.8 ? PAS_GREEDY : PAS_UNIFORM;
+  else mode = u < 0.8 - 0.1 ? PAS_UNIFORM : PAS_GREEDY;
+  ctx->load_mode = mode;
+  ctx->mode = mode;
+  ctx->bstar = mode == PAS_GREEDY ? bstar_high : 1;
+  if (mode_out) *mode_out = (pas_mode)mode;
+  return PAS_OK;
+}
+
+pas_status pas_dispatcher_state(pas_ctx* ctx, int64_t* queue_len, int64_t* busy_until_us, int64_t* fired_prompts,
+                                int64_t* fired_batches) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->disp_on) return fail(ctx, PAS_ERR_STATE, "the stateful dispatcher is off");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  DispState* h = new DispState();
+  cudaError_t e = cudaMemcpy(h, ctx->dstate, sizeof(DispState), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    for (int w = 0; w < ctx->disp_W; ++w) {
+      if (queue_len) queue_len[w] = h->Q[w];
+      if (busy_until_us) busy_until_us[w] = h->B[w];
+      if (fired_prompts) fired_prompts[w] = h->fired_prompts[w];
+      if (fired_batches) fired_batches[w] = h->fired_batches[w];
+    }
+  delete h;
+  CUDA_TRY(ctx, e);
   return PAS_OK;
 }
 
@@ -930,6 +1044,13 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
       out->fc_Hc[i] = f.Hc[i];
       out->fc_Fc[i] = f.Fc[i];
     }
+  }
+  if (ctx->disp_stats_valid) {
+    out->dispatcher = 1;
+    out->now_us = ctx->disp_last;
+    if ((s = pas_dispatcher_state(ctx, out->queue_len, out->busy_until_us, out->fired_prompts,
+                                  out->fired_batches)))
+      return s;
   }
   for (int i = 0; i < 6; ++i) {
     float ms = 0.f;

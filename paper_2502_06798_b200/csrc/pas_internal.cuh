@@ -62,6 +62,31 @@ __host__ __device__ __forceinline__ bool cand_better(const Cand& a, const Cand& 
   return a.s > b.s || (a.s == b.s && (unsigned)a.g < (unsigned)b.g);
 }
 
+// f3 stateful dispatcher (R28-R32): per-instance queue state, kept on the device across
+// batches, and the per-batch pick tables the prep kernel derives from it.
+constexpr int kArrRing = 64;                         // arrival times kept per instance (b* <= 64, R30)
+constexpr int64_t kNeverBusy = PAS_NEVER_BUSY;
+struct DispState {
+  int64_t Q[kMaxInst];                 // waiting prompts
+  int64_t B[kMaxInst];                 // busy-until (us), kNeverBusy before the first batch
+  int64_t E[kMaxInst];                 // prompts ever enqueued (arrival ring index)
+  int64_t fired_prompts[kMaxInst], fired_batches[kMaxInst];
+  int64_t svc[kMaxInst];               // batch service time (us)
+  int64_t arr[kMaxInst][kArrRing];     // arrival time of enqueue number e at arr[w][e % 64]
+};
+struct DispPlan {
+  int64_t Q0[kMaxInst];                // queue the batch found (after the events since the last batch)
+  int64_t Q1[kMaxInst];                // queue after phase 1 (max(Q0, b*))
+  int64_t Bp[kMaxInst];                // max(busy-until, now)
+  int64_t svc[kMaxInst];
+  double inv_svc[kMaxInst];
+  int32_t p1_w[kMaxInst];              // phase-1 fill order, grouped by level: [p1_beg[j], p1_beg[j+1])
+  int32_t p1_cum[kMaxInst];            // prompts of the level placed before this entry
+  int32_t p1_beg[kMaxLevels + 1];
+  int32_t p1_total[kMaxLevels];        // phase-1 capacity of the level
+  int32_t cnt[kMaxInst];               // this batch's prompts per instance
+};
+
 // Per-batch parameters, passed BY VALUE to the kernels that need them (no upload, no host sync).
 struct RouteParams {
   int nK, W, bstar, mode, topk, G, rank, d;
@@ -76,6 +101,12 @@ struct RouteParams {
   int inst_level[kMaxInst];      // level index of each serving instance
   uint32_t* lru_stamp;           // f2: [global slots] last-use ticks (K4 stamps each usable top-1)
   uint32_t lru_tick;             // this batch's tick
+  // f3 stateful dispatcher (disp == 0: the stateless packing of R13 / R14)
+  int disp;
+  int bstar_prev;                // b* in force since the last batch (events in between, R28)
+  int64_t now_us, timeout_us;
+  DispState* dstate;
+  DispPlan* dplan;
 };
 
 // Device-side plan + counters of one batch (K5 writes, pas_plan_stats reads).
@@ -211,6 +242,8 @@ struct BatchWs {
 };
 int batch_tiles(int64_t N);
 cudaError_t batch_init();   // kernel attributes (once per device)
+// f3: events since the last batch, the pick tables, per-instance counts and the state after the batch
+cudaError_t launch_disp_prep(const RouteParams& p, int ntiles, int nC, const int32_t* scanned, cudaStream_t st);
 cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan,
                                    const BatchWs& w, int32_t* instance, int32_t* slot,
                                    int32_t* bucket_offsets, int32_t* bucket_prompts,

@@ -23,6 +23,7 @@ PAS_GREEDY, PAS_UNIFORM = 0, 1
 PAS_MAX_LEVELS, PAS_MAX_INSTANCES, PAS_T_TOTAL, PAS_MAX_TOPK = 16, 64, 50, 16
 PAS_MAX_FORECAST_WINDOW = 1 << 22
 PAS_NCCL_ID_BYTES = 128
+PAS_NEVER_BUSY = -(1 << 62)
 FLAG_INVALID, FLAG_COLD, FLAG_NEAR_TOP1, FLAG_NEAR_THRESHOLD = 1, 2, 4, 8
 
 
@@ -49,7 +50,11 @@ class PasStats(C.Structure):
                 ("forecast", C.c_int), ("fc_replanned", C.c_int), ("fc_plan_n", C.c_int64),
                 ("fc_plan_counts", C.c_int64 * PAS_MAX_LEVELS), ("fc_window_n", C.c_int64),
                 ("fc_l2_error", C.c_double), ("n_unforecast", C.c_int64),
-                ("fc_Hc", C.c_uint64 * (PAS_MAX_LEVELS + 1)), ("fc_Fc", C.c_uint64 * (PAS_MAX_LEVELS + 1))]
+                ("fc_Hc", C.c_uint64 * (PAS_MAX_LEVELS + 1)), ("fc_Fc", C.c_uint64 * (PAS_MAX_LEVELS + 1)),
+                ("dispatcher", C.c_int), ("now_us", C.c_int64),
+                ("queue_len", C.c_int64 * PAS_MAX_INSTANCES), ("busy_until_us", C.c_int64 * PAS_MAX_INSTANCES),
+                ("fired_prompts", C.c_int64 * PAS_MAX_INSTANCES),
+                ("fired_batches", C.c_int64 * PAS_MAX_INSTANCES)]
 
 
 class PasError(RuntimeError):
@@ -80,6 +85,11 @@ _SIG = {
     "pas_set_fractions": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int]),
     "pas_set_seed": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
     "pas_set_forecast": (C.c_int, [_P, C.c_int, C.c_int]),
+    "pas_set_dispatcher": (C.c_int, [_P, C.POINTER(C.c_int64), C.c_int, C.c_int64]),
+    "pas_set_clock": (C.c_int, [_P, C.c_int64]),
+    "pas_set_load": (C.c_int, [_P, C.c_double, C.c_int, C.POINTER(C.c_int)]),
+    "pas_dispatcher_state": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64)]),
     "pas_route_batch": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_batch_host": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_local": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
@@ -213,6 +223,32 @@ def pas_set_forecast(ctx, window, replan_every=1):
     _check(ctx, lib.pas_set_forecast(ctx, window, replan_every))
 
 
+def pas_set_dispatcher(ctx, service_us, timeout_us=250_000):
+    """service_us: per-instance batch service times (us), or None to turn the dispatcher off."""
+    if service_us is None:
+        _check(ctx, lib.pas_set_dispatcher(ctx, None, 0, 0))
+        return
+    arr = (C.c_int64 * len(service_us))(*service_us)
+    _check(ctx, lib.pas_set_dispatcher(ctx, arr, len(service_us), timeout_us))
+
+
+def pas_set_clock(ctx, now_us):
+    _check(ctx, lib.pas_set_clock(ctx, now_us))
+
+
+def pas_set_load(ctx, lambda_rps, bstar_high) -> int:
+    m = C.c_int(0)
+    _check(ctx, lib.pas_set_load(ctx, float(lambda_rps), bstar_high, C.byref(m)))
+    return m.value
+
+
+def pas_dispatcher_state(ctx, W) -> dict:
+    arrs = [(C.c_int64 * W)() for _ in range(4)]
+    _check(ctx, lib.pas_dispatcher_state(ctx, *arrs))
+    return dict(queue=list(arrs[0]), busy_until=list(arrs[1]), fired_prompts=list(arrs[2]),
+                fired_batches=list(arrs[3]))
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -257,7 +293,10 @@ def pas_plan_stats(ctx) -> dict:
                 forecast=s.forecast, fc_replanned=s.fc_replanned, fc_plan_n=s.fc_plan_n,
                 fc_plan_counts=list(s.fc_plan_counts[:nK]), fc_window_n=s.fc_window_n,
                 fc_l2_error=s.fc_l2_error, n_unforecast=s.n_unforecast,
-                fc_Hc=list(s.fc_Hc[:nK + 1]), fc_Fc=list(s.fc_Fc[:nK + 1]))
+                fc_Hc=list(s.fc_Hc[:nK + 1]), fc_Fc=list(s.fc_Fc[:nK + 1]),
+                dispatcher=s.dispatcher, now_us=s.now_us, queue_len=list(s.queue_len[:W]),
+                busy_until_us=list(s.busy_until_us[:W]), fired_prompts=list(s.fired_prompts[:W]),
+                fired_batches=list(s.fired_batches[:W]))
 
 
 def pas_last_launch_count(ctx) -> int:
@@ -320,6 +359,18 @@ class Router:
 
     def set_forecast(self, window, replan_every=1):
         pas_set_forecast(self.ctx, window, replan_every)
+
+    def set_dispatcher(self, service_us, timeout_us=250_000):
+        pas_set_dispatcher(self.ctx, service_us, timeout_us)
+
+    def set_clock(self, now_us):
+        pas_set_clock(self.ctx, now_us)
+
+    def set_load(self, lambda_rps, bstar_high) -> int:
+        return pas_set_load(self.ctx, lambda_rps, bstar_high)
+
+    def dispatcher_state(self) -> dict:
+        return pas_dispatcher_state(self.ctx, self.W)
 
     def alloc_out(self, N, optional=True, device=None):
         t = self.torch

@@ -264,6 +264,33 @@ pas_status pas_set_load(pas_ctx* ctx, double lambda_rps, int bstar_high, pas_mod
 pas_status pas_dispatcher_state(pas_ctx* ctx, int64_t* queue_len, int64_t* busy_until_us, int64_t* fired_prompts,
                                 int64_t* fired_batches);
 
+/* NEXT f4, the Resource Controller's Model Cache Assigner + Query Fraction Solver (PAPER.md P:88, P:207,
+ * P:223; R33-R36), solved exactly on the GPU by enumerating all
+ * C(W + nK - 1, nK - 1) assignments of W instances to the nK levels of pas_set_bands (11.2M for
+ * W = 64, 6 levels; at most PAS_MAX_ASSIGNMENTS).  Inputs: lambda_rps arrival rate (>= 0), H[nK] the
+ * forecast H_K (fractions; NULL = the f1 predictor window, which needs pas_set_forecast), service_us[nK]
+ * the batch service time of a level-k instance at batch size bstar (us).  rate_k = bstar 1e6 / s_k;
+ * a_k = 1 - sum_{K_i < K_k} H_i c(K_k - K_i) (the degradation of pas_set_degradation).  For each
+ * assignment: served S = min(1, sum n_k rate_k / lambda), F = greedy fill of S by a_k descending,
+ * quality q = sum F_k a_k; the optimum maximises (S, q) lexicographically (2^-40 grid), then prefers
+ * the lexicographically largest n (instances at the slower, better levels).  out: host struct.  Uses the
+ * context's last stream; synchronises.  Errors: PAS_ERR_STATE (no bands / no forecast for H == NULL),
+ * PAS_ERR_ARG. */
+#define PAS_MAX_ASSIGNMENTS (INT64_C(1) << 34)
+typedef struct {
+  int nK, W;
+  int32_t n[PAS_MAX_LEVELS];                    /* instances per level */
+  double F[PAS_MAX_LEVELS];                     /* load fractions, sum = served */
+  double F_route[PAS_MAX_LEVELS];               /* F / served: the input of pas_set_fractions */
+  double H[PAS_MAX_LEVELS];                     /* the forecast used */
+  double served, quality;                       /* S and q of the optimum (R34) */
+  int32_t instance_level[PAS_MAX_INSTANCES];    /* level of instance w (levels ascending) */
+  int64_t candidates;                           /* assignments enumerated */
+  float solve_ms;                               /* device time of the solve */
+} pas_assignment;
+pas_status pas_solve_assignment(pas_ctx* ctx, int W, double lambda_rps, const double* H, const int64_t* service_us,
+                                int bstar, pas_assignment* out);
+
 /* Reset the Philox key and the batch sequence number (R18). */
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
 

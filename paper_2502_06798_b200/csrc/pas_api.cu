@@ -116,6 +116,9 @@ struct pas_ctx {
   int64_t disp_svc[kMaxInst] = {};
   DispState* dstate = nullptr;
   DispPlan* dplan = nullptr;
+  // f4 controller solver workspace
+  void* asg_keys = nullptr;
+  AssignOut* asg_out = nullptr;
   // f2 LRU maintenance: stamps of every global slot (replicated on all ranks) + insert workspace
   uint32_t* stamps = nullptr;
   uint32_t lru_tick = 0;
@@ -400,7 +403,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
     else g_nccl.CommDestroy(ctx->comm);
   }
   void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all, ctx->k2_progress, ctx->fc_ring, ctx->fc_state,
-                  ctx->dstate, ctx->dplan,
+                  ctx->dstate, ctx->dplan, ctx->asg_keys, ctx->asg_out,
                   ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
                   ctx->ins_idx, ctx->ins_count,
                   ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
@@ -879,6 +882,72 @@ pas_status pas_dispatcher_state(pas_ctx* ctx, int64_t* queue_len, int64_t* busy_
     }
   delete h;
   CUDA_TRY(ctx, e);
+  return PAS_OK;
+}
+
+pas_status pas_solve_assignment(pas_ctx* ctx, int W, double lambda_rps, const double* H,
+                                const int64_t* service_us, int bstar, pas_assignment* out) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->bands_set) return fail(ctx, PAS_ERR_STATE, "pas_set_bands must precede pas_solve_assignment");
+  if (!service_us || !out) return fail(ctx, PAS_ERR_ARG, "null argument");
+  if (W < 1 || W > kMaxInst) return fail(ctx, PAS_ERR_ARG, "W must be in [1, %d]", kMaxInst);
+  if (bstar < 1) return fail(ctx, PAS_ERR_ARG, "bstar must be >= 1");
+  if (!(lambda_rps >= 0.0) || !std::isfinite(lambda_rps)) return fail(ctx, PAS_ERR_ARG, "lambda must be finite, >= 0");
+  if (!H && ctx->fc_window == 0)
+    return fail(ctx, PAS_ERR_STATE, "H == NULL takes the forecast window: pas_set_forecast first");
+  AssignParams p{};
+  p.nK = ctx->nK;
+  p.W = W;
+  p.bstar = bstar;
+  p.lam = lambda_rps;
+  const int64_t total = assign_count(W, ctx->nK);
+  if (total > PAS_MAX_ASSIGNMENTS)
+    return fail(ctx, PAS_ERR_ARG, "C(W + nK - 1, nK - 1) = %lld assignments exceed %lld", (long long)total,
+                (long long)PAS_MAX_ASSIGNMENTS);
+  for (int k = 0; k < ctx->nK; ++k) {
+    if (service_us[k] < 1 || service_us[k] > PAS_MAX_SERVICE_US)
+      return fail(ctx, PAS_ERR_ARG, "service_us[%d] outside [1, 2^26]", k);
+    if (H && (!std::isfinite(H[k]) || H[k] < 0.0)) return fail(ctx, PAS_ERR_ARG, "H must be finite and >= 0");
+    p.grid[k] = ctx->grid[k];
+    p.service_us[k] = service_us[k];
+    p.H[k] = H ? H[k] : 0.0;
+  }
+  for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
+  p.fc = H ? nullptr : ctx->fc_state;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  constexpr int kMaxBlocks = kNumSMs * 8;
+  if (!ctx->asg_keys) {
+    cudaError_t e = cudaMalloc(&ctx->asg_keys, assign_key_bytes() * kMaxBlocks);
+    if (e == cudaSuccess) e = dmalloc(&ctx->asg_out, 1);
+    CUDA_TRY(ctx, e);
+  }
+  cudaStream_t st = ctx->last_stream;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[7], st));
+  CUDA_TRY(ctx, launch_assign(p, ctx->asg_keys, kMaxBlocks, ctx->asg_out, st));
+  cudaEvent_t done;
+  CUDA_TRY(ctx, cudaEventCreate(&done));
+  CUDA_TRY(ctx, cudaEventRecord(done, st));
+  AssignOut h;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->asg_out, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[7], done);
+  cudaEventDestroy(done);
+  memset(out, 0, sizeof(*out));
+  out->nK = ctx->nK;
+  out->W = W;
+  for (int k = 0; k < ctx->nK; ++k) {
+    out->n[k] = h.n[k];
+    out->F[k] = h.F[k];
+    out->F_route[k] = h.F_route[k];
+    out->H[k] = h.H[k];
+  }
+  for (int w = 0; w < W; ++w) out->instance_level[w] = h.instance_level[w];
+  out->served = h.served;
+  out->quality = h.quality;
+  out->candidates = total;
+  out->solve_ms = ms;
   return PAS_OK;
 }
 

@@ -249,6 +249,26 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
                                    int32_t* bucket_offsets, int32_t* bucket_prompts,
                                    cudaStream_t st, int* launches);
 
+// f4 controller: exact assignment solver by enumeration (R33-R36)
+struct AssignParams {
+  int nK, W, bstar;
+  double lam;                      // prompts / s
+  int grid[kMaxLevels];
+  int64_t service_us[kMaxLevels];  // batch service time at b*
+  double H[kMaxLevels];            // forecast H_K (ignored when fc != nullptr)
+  double c[kTTotal];               // degradation c(dK)
+  const FcState* fc;               // f1 predictor window: H_i = cnt_i / n (uniform when empty)
+};
+struct AssignOut {
+  int32_t n[kMaxLevels];
+  double F[kMaxLevels], F_route[kMaxLevels], H[kMaxLevels];
+  double served, quality;
+  int32_t instance_level[kMaxInst];
+};
+int64_t assign_count(int W, int nK);
+size_t assign_key_bytes();
+cudaError_t launch_assign(const AssignParams& p, void* block_best, int max_blocks, AssignOut* out, cudaStream_t st);
+
 cudaError_t launch_fill_sentinel(Cand* out, int64_t n, cudaStream_t st);
 
 // device-wide exclusive scan of n int32 (tmp: scan_tmp_ints(n) ints)

@@ -57,6 +57,14 @@ class PasStats(C.Structure):
                 ("fired_batches", C.c_int64 * PAS_MAX_INSTANCES)]
 
 
+class PasAssignment(C.Structure):
+    _fields_ = [("nK", C.c_int), ("W", C.c_int), ("n", C.c_int32 * PAS_MAX_LEVELS),
+                ("F", C.c_double * PAS_MAX_LEVELS), ("F_route", C.c_double * PAS_MAX_LEVELS),
+                ("H", C.c_double * PAS_MAX_LEVELS), ("served", C.c_double), ("quality", C.c_double),
+                ("instance_level", C.c_int32 * PAS_MAX_INSTANCES), ("candidates", C.c_int64),
+                ("solve_ms", C.c_float)]
+
+
 class PasError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
@@ -90,6 +98,8 @@ _SIG = {
     "pas_set_load": (C.c_int, [_P, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "pas_dispatcher_state": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int64)]),
+    "pas_solve_assignment": (C.c_int, [_P, C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                       C.c_int, C.POINTER(PasAssignment)]),
     "pas_route_batch": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_batch_host": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_local": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
@@ -249,6 +259,18 @@ def pas_dispatcher_state(ctx, W) -> dict:
                 fired_batches=list(arrs[3]))
 
 
+def pas_solve_assignment(ctx, W, lambda_rps, H, service_us, bstar) -> dict:
+    """H: per-level forecast, or None for the f1 predictor window."""
+    a = PasAssignment()
+    Ha = None if H is None else (C.c_double * len(H))(*H)
+    sv = (C.c_int64 * len(service_us))(*service_us)
+    _check(ctx, lib.pas_solve_assignment(ctx, W, float(lambda_rps), Ha, sv, bstar, C.byref(a)))
+    nK = a.nK
+    return dict(n=list(a.n[:nK]), F=list(a.F[:nK]), F_route=list(a.F_route[:nK]), H=list(a.H[:nK]),
+                S=a.served, q=a.quality, instance_level=list(a.instance_level[:W]),
+                candidates=a.candidates, solve_ms=a.solve_ms)
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -359,6 +381,9 @@ class Router:
 
     def set_forecast(self, window, replan_every=1):
         pas_set_forecast(self.ctx, window, replan_every)
+
+    def solve_assignment(self, W, lambda_rps, H, service_us, bstar) -> dict:
+        return pas_solve_assignment(self.ctx, W, lambda_rps, H, service_us, bstar)
 
     def set_dispatcher(self, service_us, timeout_us=250_000):
         pas_set_dispatcher(self.ctx, service_us, timeout_us)

@@ -63,7 +63,6 @@ EncodeTiledFn get_encode_fn() {
 
 thread_local std::string g_global_err;
 
-constexpr int kMaxKb = 20;   // K6 buckets <= 16 << 20
 
 int ceil_log2(int64_t v) {
   int b = 0;
@@ -215,10 +214,7 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   p.M_total = ctx->M_total;
   p.seed = ctx->seed;
   p.batch_seq = ctx->batch_seq;
-  // K6 buckets: nK << kb with kb = ceil(log2 N) - 4, so a class holding all N prompts averages
-  // <= 16 prompts per bucket (the in-bucket rank loop) and the bucket scan stays small.
-  int kb = ceil_log2(N > 1 ? N : 1) - 4;
-  p.kb = kb < 0 ? 0 : (kb > kMaxKb ? kMaxKb : kb);
+  p.kb = redirect_kb(N);   // K6 buckets per class: 2^kb
   for (int i = 0; i < kMaxLevels; ++i) {
     p.grid[i] = ctx->grid[i];
     p.thr[i] = i + 1 < ctx->nK ? ctx->thr[i] : INFINITY;   // +inf padding: level by binary search
@@ -406,9 +402,9 @@ pas_status pas_destroy(pas_ctx* ctx) {
                   ctx->dstate, ctx->dplan, ctx->asg_keys, ctx->asg_out,
                   ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
                   ctx->ins_idx, ctx->ins_count,
-                  ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.bucket,
-                  ctx->rw.bcount, ctx->rw.bstart, ctx->rw.bfill,  ctx->rw.sorted,    ctx->rw.cls7,
-                  ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp, ctx->rw.scan_tmp,
+                  ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.hist,
+                  ctx->rw.used, ctx->rw.csum, ctx->rw.bnd, ctx->rw.lists,  ctx->rw.cand,    ctx->rw.cls7,
+                  ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp,
                   ctx->stage_emb, ctx->s_K, ctx->s_Kp,
                   ctx->s_inst,  ctx->s_slot,    ctx->s_tid,      ctx->s_boff,       ctx->s_bpr,     ctx->s_tsc,
                   ctx->s_flags};
@@ -455,9 +451,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->cap_rows = cfg->max_rows_per_rank;
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
   ctx->cand_cap = 4 * mb > 592 * qt ? 4 * mb : 592 * qt;
-  int kbm = ceil_log2(mb > 1 ? mb : 1) - 4;
-  kbm = kbm < 0 ? 0 : (kbm > kMaxKb ? kMaxKb : kbm);
-  const int64_t nb = (int64_t)kMaxLevels << kbm;
+  const int64_t nb = (int64_t)kMaxLevels << redirect_kb(mb);
   const int64_t ncls = 64 * (int64_t)batch_tiles(mb);
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, n) \
@@ -471,13 +465,13 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ALLOC(ctx->invalid_count, 1);
   ALLOC(ctx->plan, 1);
   ALLOC(ctx->rw.key, mb);
-  ALLOC(ctx->rw.bucket, mb);
-  ALLOC(ctx->rw.bcount, nb);
-  ALLOC(ctx->rw.bstart, nb);
-  ALLOC(ctx->rw.bfill, nb);
-  ALLOC(ctx->rw.sorted, mb);
+  ALLOC(ctx->rw.hist, nb);
+  ALLOC(ctx->rw.used, 2);
+  ALLOC(ctx->rw.csum, kMaxLevels * 256);
+  ALLOC(ctx->rw.bnd, 1);
+  ALLOC(ctx->rw.lists, kMaxLevels * kMaxLevels);
+  ALLOC(ctx->rw.cand, mb);
   ALLOC(ctx->rw.cls7, mb);
-  ALLOC(ctx->rw.scan_tmp, scan_tmp_ints(nb));
   ALLOC(ctx->bw.blk_counts, ncls);
   ALLOC(ctx->bw.blk_off, ncls);
   ALLOC(ctx->bw.offsets, kMaxInst + 1);

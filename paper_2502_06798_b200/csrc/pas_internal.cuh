@@ -177,20 +177,30 @@ cudaError_t launch_plan(const int* hist, const RouteParams& p, DevPlan* plan, cu
 
 // K6 redirection
 struct __align__(16) KeyEntry {
-  uint64_t key;           // (class << 60) | kappa
+  uint64_t key;           // kappa (60-bit Philox key)
   int32_t p;              // prompt index
   int32_t pad;
 };
-struct RedirectWs {
-  uint64_t* key;          // [N]
-  int32_t* bucket;        // [N]
-  int32_t* bcount;        // [nK << kb]   zeroed
-  int32_t* bstart;        // [nK << kb]
-  int32_t* bfill;         // [nK << kb]   zeroed
-  KeyEntry* sorted;       // [N] bucket order
-  uint8_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
-  int32_t* scan_tmp;      // scan_tmp_ints(nK << kb)
+constexpr int kMaxK6Bits = 18;      // K6 buckets per class <= 2^18
+struct K6Bounds {                   // per class i, split j: the bucket holding split rank X_i[j] (INT32_MAX:
+  int32_t bucket[kMaxLevels][kMaxLevels];   // none), the split's rank inside it, its candidate list
+  int32_t off[kMaxLevels][kMaxLevels];
+  int32_t list[kMaxLevels][kMaxLevels];
 };
+struct K6List {                     // one bucket holding one or more splits of a class
+  int32_t cls, bucket, cnt, base, fill, below;
+};
+struct RedirectWs {
+  uint64_t* key;          // [N] kappa
+  int32_t* hist;          // [kMaxLevels << kMaxK6Bits] (class, bucket) counts, zeroed per batch
+  int32_t* used;          // [2] lists, candidate entries (zeroed per batch)
+  int32_t* csum;          // [kMaxLevels * 256] chunk sums of the bucket counts
+  K6Bounds* bnd;
+  K6List* lists;          // [kMaxLevels * kMaxLevels]
+  KeyEntry* cand;         // [N] entries of the split buckets
+  uint8_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
+};
+int redirect_kb(int64_t N);
 cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan,
                             const RedirectWs& w, int32_t* K_prime, cudaStream_t st, int* launches);
 

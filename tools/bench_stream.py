@@ -23,9 +23,8 @@ def algorithmic_bytes(N, S, k, d, W, M):
     return {
         "k_normalize (cache insert, fp32 in)": M * d * (4 + 2),
         "k_merge_select_thr": N * (S * k * 8 + k * 8 + 4 + 1 + 1),
-        "k_keys": N * (1 + 8 + 4),
-        "k_scatter": N * (4 + 4),
-        "k_rank": N * (8 + 4 + 1 + 4),        # read the entry, K' (int32) + class byte written (+ in-bucket reads)
+        "k6_hist": N * (1 + 8 + 4),           # level byte, kappa written, one (class, bucket) count
+        "k6_assign": N * (1 + 8 + 4 + 1),     # level byte + kappa read; K' (int32) + K7 class byte written
         "k_cls_count": N * 1,                  # class byte
         "k_cls_rank": N * (1 + 4 + 4 + 4),     # class byte; instance, slot, bucket-list entry
     }

@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample-prompts", type=int, default=32)
+    ap.add_argument("--dispatcher", action="store_true",
+                    help="route-and-batch through the f3 stateful dispatcher (queues carried across steps)")
     ap.add_argument("--force-collective", action="store_true",
                     help="use the NCCL all-gather path even with one rank (transport self-test)")
     return ap.parse_args()
@@ -204,6 +206,22 @@ def main():
                         rank=rank, world=G, nccl_id=nccl_id, seed=cfg.route_seed)
     router.set_bands(cfg.grid, cfg.thresholds)
     router.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
+    gap_us = 0
+    if args.dispatcher:
+        # SPEC S:75 service model per instance at b*: (T - K) x 100 ms x (1 + 0.3 (b* - 1)); batches
+        # arrive at 90 % of the instances' capacity, so queues stay short but non-empty
+        svc = [int(round((50 - cfg.grid[lv]) * 100_000 * (1 + 0.3 * (cfg.bstar - 1)))) for lv in cfg.instance_level]
+        router.set_dispatcher(svc, 250_000)
+        cap = sum(cfg.bstar / (s_ * 1e-6) for s_ in svc)
+        gap_us = int(N / (0.9 * cap) * 1e6)
+    clock = [0]
+
+    def route_step():
+        if args.dispatcher:
+            clock[0] += gap_us
+            router.set_clock(clock[0])
+        router.route(P, out)
+
     w = Workload(cfg, device=dev, M=M)
     t_load = time.perf_counter()
     for b in range(w.n_blocks()):
@@ -225,7 +243,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        router.route(P, out)
+        route_step()
     barrier()
 
     clocks = ClockSampler(local)
@@ -243,7 +261,7 @@ def main():
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-        router.route(P, out)
+        route_step()
         launches += pas.pas_last_launch_count(router.ctx)
         if flush is not None:
             s1.record(stream)
@@ -296,7 +314,8 @@ def main():
         "config": {"workload": f"{args.config}: {N:,} prompts vs {M:,}-entry cache ({cfg.note})", "N": N, "M": M,
                    "G": G, "M_per_gpu": M_local, "d": cfg.d, "topk": cfg.topk, "levels": len(cfg.grid),
                    "instances": len(cfg.instance_level), "mode": "uniform" if cfg.mode else "greedy",
-                   "bstar": cfg.bstar, "parallelism": f"cache row-sharded x{G}" + (" + NCCL all-gather" if G > 1 else ""),
+                   "bstar": cfg.bstar, "dispatcher": "stateful (f3)" if args.dispatcher else "stateless (R13)",
+                   "parallelism": f"cache row-sharded x{G}" + (" + NCCL all-gather" if G > 1 else ""),
                    "l2": l2_note},
         "roofline": {"kernel": "k_simtopk (K2: tcgen05 similarity GEMM + fused top-k)", "bound": "tensor",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,

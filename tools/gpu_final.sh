@@ -12,7 +12,7 @@ timeout 900 python bench.py --dispatcher --no-cpu-baseline --no-e2e > $O/bench_c
 timeout 900 python bench.py --config C3 --no-cpu-baseline > $O/bench_c3_g1.json 2> $O/bench_c3_g1.err
 timeout 600 python tools/bench_controller.py > $O/controller.jsonl 2> $O/controller.err
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_|k6_" -s 20 -c 80 --csv --log-file $O/c4_g1_launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu1 rc=$?" >> $O/ncu_launch.log
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_|k6_" -s 153 -c 60 --csv --log-file $O/c4_g1_launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu1 rc=$?" >> $O/ncu_launch.log
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_simtopk -c 1 -o $O/k2_c4_g1 $CMD > $O/ncu_full.log 2>&1; echo "ncu2 rc=$?" >> $O/ncu_full.log
 timeout 600 python tools/bench_stream.py > $O/stream_64M.json 2> $O/stream.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_|k6_" --csv --log-file $O/stream_launches_64M.csv python tools/bench_stream.py --reps 1 > $O/stream_ncu.log 2>&1; echo "ncu3 rc=$?" >> $O/stream_ncu.log

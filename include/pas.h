@@ -135,6 +135,10 @@ typedef struct {
   int64_t busy_until_us[PAS_MAX_INSTANCES];     /* PAS_NEVER_BUSY if the instance never fired */
   int64_t fired_prompts[PAS_MAX_INSTANCES];     /* cumulative since pas_set_dispatcher */
   int64_t fired_batches[PAS_MAX_INSTANCES];
+  /* K2 schedule of the last batch: cache ranges per prompt tile (the S of the merge),
+   * and for the dynamic schedule the cache tiles per chunk and the chunk steps per range (0, 0: the
+   * static schedule, one unit per (prompt tile, range)) */
+  int k2_ranges, k2_chunk_tiles, k2_chunk_steps;
 } pas_stats;
 
 /* Library and build identification ("sm_100a", version). Never fails. */

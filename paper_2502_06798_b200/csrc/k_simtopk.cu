@@ -39,6 +39,7 @@
 //               bubble insert (strict >, columns ascending, so equal scores keep the lower column).
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "pas_internal.cuh"
 #include "ptx_sm100.cuh"
@@ -75,14 +76,20 @@ struct Tile {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + LIST_BYTES;
 };
 
+constexpr int UNIT_RING = 4;   // dynamic schedule: work units fetched ahead by the producer
+
 template <int STAGES>
 struct __align__(8) Bars {
   uint64_t full[STAGES];    // TMA bytes landed (leader's barrier in pair mode)
   uint64_t empty[STAGES];   // MMA finished reading the stage
   uint64_t tfull[2];        // accumulator ready
   uint64_t tempty[2];       // epilogue(s) drained the accumulator
+  uint64_t ufull[UNIT_RING];    // dynamic schedule: unit id published by the producer
+  uint64_t uempty[UNIT_RING];   // ... read by the MMA issuer and every epilogue warp
+  int32_t unit[UNIT_RING];
   uint32_t tmem_base;
 };
+static_assert(sizeof(Bars<6>) <= 256, "barrier block overflows its 256-byte slot");
 
 // Opaque copy: stops the compiler from strength-reducing per-element column ids across chunks.
 __device__ __forceinline__ int opaque(int x) {
@@ -181,15 +188,45 @@ __device__ __noinline__ void leash_wait(uint64_t* progress, int worker, int nwor
   }
 }
 
+// Dynamic schedule (DESIGN.md 8 "K2 schedule"): unit u = (chunk step c, range r, prompt tile m), m
+// fastest, then r, then c; chunk c of range r = its tiles [t0 + cT, t0 + (c+1)T) (possibly empty).
+__device__ __forceinline__ void dyn_decode(int u, int MT, int R, int NT, int T, int& c, int& j, int& ta, int& tb) {
+  const int P = MT * R;
+  c = u / P;
+  j = u - c * P;
+  const int r = j / MT;
+  const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+  ta = min(t1, t0 + c * T);
+  tb = min(t1, ta + T);
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin until the lists of (r, m) after chunk c - 1 are published.  Bounded: a broken protocol traps
+// (a reported launch failure) instead of hanging the device.
+__device__ __noinline__ void dyn_wait_state(const uint64_t* done, uint64_t want) {
+  for (uint32_t spin = 0;; ++spin) {
+    if (ld_acquire_u64(done) == want) return;
+    if (spin > (1u << 26)) __trap();
+    __nanosleep(256);
+  }
+}
+
 __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
 
-template <int KMAX, bool DUMP, bool PAIR>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
-              float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack) {
+              float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack,
+              const DynSched dyn) {
+  static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
   using TL = Tile<PAIR>;
   constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
                 B_BYTES = TL::B_BYTES, STAGE_BYTES = TL::STAGE_BYTES, UNIT_ROWS = TL::UNIT_ROWS;
@@ -207,7 +244,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool leader = crank == 0;
   const int worker = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int nworkers = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int units = MT * R;
+  const int units = DYN ? dyn.CS * MT * R : MT * R;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmQ);
@@ -215,6 +252,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&bars->full[s], 1);
       ptx::mbar_init(&bars->empty[s], 1);
+    }
+    for (int s = 0; s < UNIT_RING; ++s) {
+      ptx::mbar_init(&bars->ufull[s], 1);
+      ptx::mbar_init(&bars->uempty[s], 1 + EPI_WARPS);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&bars->tfull[a], 1);
@@ -241,7 +282,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------- TMA producer -------------------------------
     // Lane 0 waits on the ring and issues TMA; with the leash on, the whole warp walks the schedule
     // (the look-up of the other CTAs' progress is warp-parallel).
-    if (slack || lane == 0) {
+    if (DYN) {
+      // dynamic schedule: lane 0 takes the next unit from the global counter, publishes it to the
+      // MMA issuer and the epilogue through the unit ring, then streams its chunk
+      if (lane == 0) {
+        int stage = 0, us = 0;
+        uint32_t phase = 0, uph = 0;
+        for (;;) {
+          const int u = (int)atomicAdd(dyn.sched, 1u);
+          ptx::mbar_wait(&bars->uempty[us], uph ^ 1);
+          bars->unit[us] = u < units ? u : -1;
+          ptx::mbar_arrive(&bars->ufull[us]);
+          if (++us == UNIT_RING) { us = 0; uph ^= 1; }
+          if (u >= units) break;
+          int c, j, ta, tb;
+          dyn_decode(u, MT, R, NT, dyn.T, c, j, ta, tb);
+          const int qrow = (j % MT) * BM;
+          for (int t = ta; t < tb; ++t) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+              ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
+              ptx::mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
+              ptx::tma_load_2d(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
+              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN, ptx::kEvictNormal);
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+        // every worker has taken its last unit once all have arrived here: the last one out re-arms
+        // the counter for the next launch (kernel boundaries order this against the next K2)
+        if (atomicAdd(dyn.sched + 1, 1u) == (uint32_t)nworkers - 1) {
+          dyn.sched[0] = 0;
+          dyn.sched[1] = 0;
+        }
+      }
+    } else if (slack || lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t issued = 0;
@@ -285,9 +359,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = worker; u < units; u += nworkers) {
-        const int r = u / MT;
-        const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+      int us = 0;
+      uint32_t uph = 0;
+      for (int u = worker; DYN || u < units; u += nworkers) {
+        int t0, t1;
+        if (DYN) {
+          ptx::mbar_wait(&bars->ufull[us], uph);
+          u = bars->unit[us];
+          ptx::mbar_arrive(&bars->uempty[us]);
+          if (++us == UNIT_RING) { us = 0; uph ^= 1; }
+          if (u < 0) break;
+          int c, j;
+          dyn_decode(u, MT, R, NT, dyn.T, c, j, t0, t1);
+        } else {
+          const int r = u / MT;
+          t0 = (int)((int64_t)r * NT / R);
+          t1 = (int)((int64_t)(r + 1) * NT / R);
+        }
         for (int t = t0; t < t1; ++t) {
           ptx::mbar_wait(&bars->tempty[acc], acc_phase ^ 1);
           ptx::tc_fence_after();
@@ -324,14 +412,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int Ml = (int)M_local;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = worker; u < units; u += nworkers) {
-      const int m = u % MT, r = u / MT;
-      const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
+    int us = 0;
+    uint32_t uph = 0;
+    for (int u = worker; DYN || u < units; u += nworkers) {
+      int m, r, t0, t1, c = 0, j = 0;
+      if (DYN) {
+        ptx::mbar_wait(&bars->ufull[us], uph);
+        u = bars->unit[us];
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars->uempty[us]);
+        if (++us == UNIT_RING) { us = 0; uph ^= 1; }
+        if (u < 0) break;
+        dyn_decode(u, MT, R, NT, dyn.T, c, j, t0, t1);
+        m = j % MT;
+        r = j / MT;
+      } else {
+        m = u % MT;
+        r = u / MT;
+        t0 = (int)((int64_t)r * NT / R);
+        t1 = (int)((int64_t)(r + 1) * NT / R);
+      }
       const int64_t prompt = (int64_t)m * UNIT_ROWS + crank * BM + row;
       float s[KMAX];
       int32_t gl[KMAX];
 #pragma unroll
       for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; gl[i] = -1; }
+      // dynamic schedule: resume the lists this (range, prompt tile) had after chunk c - 1
+      const int64_t st_off = ((int64_t)(j * 2 + half) * KMAX) * BM + row;
+      if (DYN && c > 0) {
+        if (warp == 2 && lane == 0) dyn_wait_state(dyn.done + j, ((uint64_t)epoch << 32) | (uint32_t)c);
+        epi_barrier();
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) {
+          s[i] = __ldcg(dyn.st_s + st_off + i * BM);
+          gl[i] = __ldcg(dyn.st_g + st_off + i * BM);
+        }
+      }
       for (int t = t0; t < t1; ++t) {
         ptx::mbar_wait(&bars->tfull[acc], acc_phase);
         ptx::tc_fence_after();
@@ -363,7 +479,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
-      if (!DUMP) {
+      if (DYN && c + 1 < dyn.CS) {
+        // not the range's last chunk: park both half-lists (coalesced [j][half][i][row]) and publish
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) {
+          __stcg(dyn.st_s + st_off + i * BM, s[i]);
+          __stcg(dyn.st_g + st_off + i * BM, gl[i]);
+        }
+        epi_barrier();
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(dyn.done + j),
+                       "l"(((uint64_t)epoch << 32) | (uint32_t)(c + 1)) : "memory");
+        }
+      } else if (!DUMP) {
         // the upper-half warps hand their lists over; the lower half merges and writes
         if (half == 1) {
 #pragma unroll
@@ -611,7 +740,7 @@ cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream
   return cudaGetLastError();
 }
 
-template <int KMAX, bool DUMP, bool PAIR>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN = false>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
   using TL = Tile<PAIR>;
   constexpr int CTAS = TL::CTAS;
@@ -629,9 +758,9 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR>, *a.tmap_q, PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N,
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN>, *a.tmap_q, PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N,
                             a.M_local, a.d / BK, a.k, a.G,
-                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack);
+                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack, a.dyn);
 }
 
 }  // namespace
@@ -654,11 +783,64 @@ cudaError_t simtopk_init() {
   if ((e = cudaFuncSetAttribute(k_simtopk_ta<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   const int ss = Tile<false>::SMEM_BYTES, pr = Tile<true>::SMEM_BYTES;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
-  return cudaFuncSetAttribute(k_simtopk<16, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
+  return cudaFuncSetAttribute(k_simtopk<16, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
+}
+
+// Dynamic schedule.  Static units (prompt tile, whole range) let the 148 CTAs drift apart over a range
+// of thousands of tiles, so L2 stops covering the spread and tiles come from DRAM again (C4: 418 GB
+// read per launch for a 15.4 GB cache); a leash that holds CTAs together costs more than it saves.
+// Here units are short (T tiles of one range for one prompt tile), handed out by a global counter in
+// (chunk step, range, prompt tile) order: whatever their speed, the CTAs stay within one chunk step of
+// each other, so the cache crosses HBM about once, and fast SMs simply take more units.  Top-k lists
+// are parked in global memory (L2-resident, 32 KB per unit for k <= 8) between a tile's chunks.
+// Conditions: the single-CTA tile; at least PAS_K2_DYN_MIN_PAIRS x 148 (range, prompt tile) pairs, so
+// the unit that resumes (r, m) is handed out that many units after the one that parks it (it almost
+// never waits); R * N within the candidate buffer and R * MT within the parked-list buffer.
+#ifndef PAS_K2_DYN_MB
+#define PAS_K2_DYN_MB 80          // L2 budget for the chunks streamed concurrently
+#endif
+#ifndef PAS_K2_DYN_TMAX
+#define PAS_K2_DYN_TMAX 64        // longest chunk (tiles)
+#endif
+#ifndef PAS_K2_DYN_MIN_PAIRS
+#define PAS_K2_DYN_MIN_PAIRS 2
+#endif
+#ifndef PAS_K2_DYN_MIN_STEPS
+#define PAS_K2_DYN_MIN_STEPS 8    // fewer chunk steps: short ranges, the static schedule is faster (C2)
+#endif
+static int env_int(const char* name, int dflt) {   // A/B experiments only
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R_out,
+                          int* T_out, int* CS_out) {
+  const int budget_mb = env_int("PAS_K2_DYN_MB", PAS_K2_DYN_MB);
+  if (budget_mb <= 0 || simtopk_uses_tmem_a(d) || simtopk_pair(N, d)) return false;
+  const int64_t MT = (N + BM - 1) / BM;
+  const int64_t NT = (M_local + BN - 1) / BN;
+  if (MT <= 0 || NT <= 0) return false;
+  const int64_t want = (int64_t)env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS) * Tile<false>::NUM_WORKERS;
+  const int64_t R = (want + MT - 1) / MT;
+  if (R > NT || R * N > cand_rows || R * MT > state_tiles || R > 128) return false;
+  // chunks in flight: the ranges one window of 148 consecutive units spans, plus the next step's
+  const int64_t in_flight = (Tile<false>::NUM_WORKERS + MT - 1) / MT + 1;
+  const int64_t tile_bytes = (int64_t)BN * d * 2;
+  int64_t T = ((int64_t)budget_mb << 20) / (in_flight * tile_bytes);
+  if (T < 4) T = 4;
+  const int tmax = env_int("PAS_K2_DYN_TMAX", PAS_K2_DYN_TMAX);
+  if (T > tmax) T = tmax;
+  const int64_t L = (NT + R - 1) / R;             // tiles of the longest range
+  if (L < env_int("PAS_K2_DYN_MIN_STEPS", PAS_K2_DYN_MIN_STEPS) * T) return false;   // too short to chunk
+  *R_out = (int)R;
+  *T_out = (int)T;
+  *CS_out = (int)((L + T - 1) / T);
+  return true;
 }
 
 // Pick the number of cache ranges R so that (prompt tiles x R) units fill the persistent workers with
@@ -723,6 +905,11 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
     if (a.dump) return launch_ta<8, true>(a, MT, NT, grid, st);
     if (a.k <= 8) return launch_ta<8, false>(a, MT, NT, grid, st);
     return launch_ta<16, false>(a, MT, NT, grid, st);
+  }
+  if (a.dyn.T > 0 && !pair && !a.dump) {
+    const int g = NUM_WORKERS;   // every SM: units are handed out dynamically
+    if (a.k <= 8) return launch_variant<8, false, false, true>(a, MT, NT, g, 0, st);
+    return launch_variant<16, false, false, true>(a, MT, NT, g, 0, st);
   }
   const uint32_t slack = a.progress ? simtopk_leash_slack(MT, NT, a.R, workers) : 0;
   if (a.dump) return launch_variant<8, true, false>(a, MT, NT, grid, slack, st);

@@ -99,6 +99,13 @@ struct pas_ctx {
   Cand* cand_rank = nullptr;
   Cand* cand_all = nullptr;
   uint64_t* k2_progress = nullptr;   // K2 leash words [kNumSMs]
+  // K2 dynamic schedule: parked top-k lists, per-(range, prompt tile) chunk counters, unit counter
+  float* k2_st_s = nullptr;
+  int32_t* k2_st_g = nullptr;
+  uint64_t* k2_done = nullptr;
+  uint32_t* k2_sched = nullptr;
+  int64_t k2_state_tiles = 0;
+  int k2_last_R = 0, k2_last_T = 0, k2_last_CS = 0;   // schedule of the last K2 launch (pas_plan_stats)
   // f1 forecast-driven mode (0 = exact per-batch plan)
   int fc_window = 0, fc_replan_every = 1;
   int64_t fc_tick = 0;
@@ -267,6 +274,15 @@ pas_status ensure_prompt_ws(pas_ctx* ctx) {
   if (e == cudaSuccess) e = dmalloc(&ctx->pflags, (size_t)mb);
   if (e == cudaSuccess) e = dmalloc(&ctx->k2_progress, (size_t)kNumSMs);
   if (e == cudaSuccess) e = cudaMemset(ctx->k2_progress, 0, sizeof(uint64_t) * kNumSMs);   // epoch 0 = none
+  // parked lists of the K2 dynamic schedule: one slot per (range, prompt tile), R * MT <= cand_cap / 128 + 8
+  ctx->k2_state_tiles = ctx->cand_cap / simtopk_box_q() + 8;
+  const size_t st_elems = (size_t)ctx->k2_state_tiles * simtopk_box_q() * 2 * (k <= 8 ? 8 : 16);
+  if (e == cudaSuccess) e = dmalloc(&ctx->k2_st_s, st_elems);
+  if (e == cudaSuccess) e = dmalloc(&ctx->k2_st_g, st_elems);
+  if (e == cudaSuccess) e = dmalloc(&ctx->k2_done, (size_t)ctx->k2_state_tiles);
+  if (e == cudaSuccess) e = cudaMemset(ctx->k2_done, 0, sizeof(uint64_t) * (size_t)ctx->k2_state_tiles);
+  if (e == cudaSuccess) e = dmalloc(&ctx->k2_sched, (size_t)2);
+  if (e == cudaSuccess) e = cudaMemset(ctx->k2_sched, 0, sizeof(uint32_t) * 2);
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_local, (size_t)(ctx->cand_cap * k));
   if (e == cudaSuccess) e = dmalloc(&ctx->cand_rank, (size_t)(mb * k));
   if (e == cudaSuccess && (ctx->cfg.world > 1 || ctx->comm))
@@ -287,17 +303,34 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
   int R = 1;
   if (ctx->M_local > 0) {
-    R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap, ctx->cfg.d);
-    if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
-      const int r = atoi(ov);
-      if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
+    DynSched dyn;
+    const char* sched = getenv("PAS_K2_SCHED");    // "static": A/B experiments only
+    const bool dyn_ok = !(sched && !strcmp(sched, "static")) &&
+                        simtopk_plan_dynamic(N, ctx->M_local, ctx->cand_cap, ctx->k2_state_tiles, ctx->cfg.d, &R,
+                                             &dyn.T, &dyn.CS);
+    if (dyn_ok) {
+      dyn.st_s = ctx->k2_st_s;
+      dyn.st_g = ctx->k2_st_g;
+      dyn.done = ctx->k2_done;
+      dyn.sched = ctx->k2_sched;
+    } else {
+      R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap, ctx->cfg.d);
+      if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
+        const int r = atoi(ov);
+        if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
+      }
     }
     if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
                   ctx->qhat, ctx->cand_local, nullptr, getenv("PAS_K2_NOLEASH") ? nullptr : ctx->k2_progress,
-                  ctx->k2_epoch};
+                  ctx->k2_epoch, dyn};
     CUDA_TRY(ctx, launch_simtopk(a, st));
+    ctx->k2_last_R = R;
+    ctx->k2_last_T = dyn.T;
+    ctx->k2_last_CS = dyn.CS;
   } else {
+    ctx->k2_last_R = 1;
+    ctx->k2_last_T = ctx->k2_last_CS = 0;
     CUDA_TRY(ctx, launch_fill_sentinel(ctx->cand_local, N * k, st));
   }
   ctx->launches++;
@@ -399,6 +432,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
     else g_nccl.CommDestroy(ctx->comm);
   }
   void* ptrs[] = {ctx->store,   ctx->qhat,      ctx->pflags,     ctx->cand_local,   ctx->cand_rank, ctx->cand_all, ctx->k2_progress, ctx->fc_ring, ctx->fc_state,
+                  ctx->k2_st_s, ctx->k2_st_g, ctx->k2_done, ctx->k2_sched,
                   ctx->dstate, ctx->dplan, ctx->asg_keys, ctx->asg_out,
                   ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
                   ctx->ins_idx, ctx->ins_count,
@@ -1093,6 +1127,9 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
   out->n_near_top1 = p.n_near_top1;
   out->n_near_threshold = p.n_near_threshold;
   for (int w = 0; w < ctx->W; ++w) out->bucket_count[w] = p.inst_count[w];
+  out->k2_ranges = ctx->k2_last_R;
+  out->k2_chunk_tiles = ctx->k2_last_T;
+  out->k2_chunk_steps = ctx->k2_last_CS;
   if (ctx->fc_stats_valid) {
     FcState f;
     CUDA_TRY(ctx, cudaMemcpy(&f, ctx->fc_state, sizeof f, cudaMemcpyDeviceToHost));

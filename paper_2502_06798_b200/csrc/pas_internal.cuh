@@ -133,6 +133,18 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
                              cudaStream_t st);
 
+// K2 dynamic schedule (DESIGN.md 8 "K2 schedule"): units (chunk step, range, prompt tile) handed out
+// in that order by a global counter; each (range, prompt tile) parks its two half top-k lists between
+// chunks and publishes "chunks done" (epoch-tagged) for the unit that resumes them.
+struct DynSched {
+  int T = 0;                    // cache tiles per chunk
+  int CS = 0;                   // chunk steps per range
+  float* st_s = nullptr;        // [R*MT][2][KMAX][128] parked scores
+  int32_t* st_g = nullptr;      // [R*MT][2][KMAX][128] parked local rows
+  uint64_t* done = nullptr;     // [R*MT] epoch << 32 | chunks done
+  uint32_t* sched = nullptr;    // [2] unit counter, workers finished (zero between launches)
+};
+
 // K2: similarity GEMM (tcgen05) + fused running top-k over cache ranges.
 struct SimTopkArgs {
   const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x simtopk_box_q(), SW128
@@ -146,9 +158,14 @@ struct SimTopkArgs {
   float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
   uint64_t* progress;             // [kNumSMs] leash words (epoch << 32 | tiles issued), or null: no leash
   uint32_t epoch;                 // this launch's epoch (never 0: zeroed words read as "not started")
+  DynSched dyn;                   // T > 0: the dynamic schedule (simtopk_plan_dynamic)
 };
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
+// The dynamic schedule's ranges R and chunk T for this batch, or false when the static schedule
+// serves it (CTA-pair tile, too few units, or more parked lists than `state_tiles` prompt tiles).
+bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R,
+                          int* T, int* CS);
 bool simtopk_uses_tmem_a(int d);
 bool simtopk_pair(int64_t N, int d);   // the CTA-pair tile serves this batch size
 cudaError_t simtopk_init();

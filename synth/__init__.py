@@ -87,6 +87,21 @@ CONFIGS = {
 }
 
 
+def c5_fractions(prev_h, prev_N: int, N: int) -> list:
+    """The C5 controller input for a batch of N prompts ("only faster
+    K = 25 variants running at peak loads"): F_b = (1 - l_b) h_{b-1} / N_{b-1} + l_b e_{K=25},
+    l_b = log2(N_b / 256) / 9, renormalised; uniform before the first batch.  A workload recipe
+    (what the controller hands the path), not method arithmetic."""
+    if prev_h is None:
+        n = len(CONFIGS["C5"].grid)
+        return [1.0 / n] * n
+    ell = math.log2(N / 256) / 9
+    F = [(1 - ell) * h / prev_N for h in prev_h]
+    F[-1] += ell
+    s = sum(F)
+    return [f / s for f in F]
+
+
 def n_clusters(M: int) -> int:
     return int(min(max(M // 1000, 16), 50000))
 

@@ -50,6 +50,36 @@ def oracle_topk_streaming(P: np.ndarray, cache_chunks, k: int):
     return O.topk_streaming(P, cache_chunks, k + 1)
 
 
+def oracle_topk_parallel(P: np.ndarray, cache_chunks, k: int, workers: int | None = None):
+    """``oracle_topk_streaming`` with the oracle's per-chunk calls run in a thread pool (NumPy releases
+    the GIL; BLAS held to one thread per worker) and the per-chunk top-(k+1) lists merged in chunk order
+    with the oracle's own ``merge_topk`` (the top-k of a union is the top-k of the parts' top-k).  Test
+    plumbing for a 50M-row cache; the arithmetic is the oracle's, unchanged."""
+    import collections
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+    workers = workers or max(1, min(32, len(os.sched_getaffinity(0))))
+    acc = {}
+
+    def drain(pending, limit):
+        while len(pending) > limit:
+            i, s, v = pending.popleft().result()
+            if not acc:
+                acc.update(ids=i, sc=s, valid=v)
+            else:
+                acc["ids"], acc["sc"] = O.merge_topk(acc["ids"], acc["sc"], i, s, k + 1)
+
+    with threadpool_limits(limits=1, user_api="blas"), ThreadPoolExecutor(workers) as ex:
+        pending = collections.deque()
+        for first, rows in cache_chunks:
+            pending.append(ex.submit(O.topk_streaming, P, [(first, rows)], k + 1))
+            drain(pending, 2 * workers)
+        drain(pending, 0)
+    return acc["ids"], acc["sc"], acc["valid"]
+
+
 def tier_b_scores(P: np.ndarray, rows_of_ids: np.ndarray) -> np.ndarray:
     """s_hat(p, g) for the GPU's ids: rows_of_ids [n, k, d] fp32 cache rows (zeros for -1)."""
     Pq, _ = O.quantize(P)

@@ -146,6 +146,61 @@ def test_c4_parity_sampled_full_size(pas):
     print(rep.summary(), st["stage_ms"])
 
 
+@pytest.mark.slow
+def test_c5_load_sweep_parity_full_size(pas):
+    """BASELINE configs[4] with the full 50M-entry cache on one GPU: batches of 256, 2,048, 16,384 and
+    131,072 prompts routed in sequence (batch_seq 0..3), F(K) recomputed before every batch from the
+    previous batch's H_K (synth.c5_fractions, the controller recipe of SURVEY 8(d)).  Eight sampled
+    prompts per batch against the whole cache (one oracle pass for all of them), H_K, plan, K',
+    instances, slots and batch lists on all N of every batch."""
+    from .parity import oracle_topk_parallel
+    from synth import c5_fractions
+    cfg = CONFIGS["C5"]
+    Ns = [256, 2048, 16384, 131072]
+    w = Workload(cfg, device=DEV)
+    rng = np.random.default_rng(5)
+    batches, idx = [], []
+    for b, N in enumerate(Ns):
+        batches.append(w.prompts(N, batch=b))
+        idx.append(np.sort(rng.choice(N, 8, replace=False)))
+    Ps = np.concatenate([batches[b][torch.from_numpy(idx[b])].cpu().numpy() for b in range(len(Ns))])
+    r = _router(pas, cfg, Ns[-1], cfg.M)
+
+    def chunks():
+        for b in range(w.n_blocks()):
+            rows = w.cache_block(b).contiguous()
+            r.load_cache(rows)
+            yield b * BLOCK, rows.cpu().numpy()
+
+    o_ids_all, o_sc_all, valid_all = oracle_topk_parallel(Ps, chunks(), cfg.topk)
+    k = cfg.topk
+    prev_h = prev_N = None
+    for b, N in enumerate(Ns):
+        F = c5_fractions(prev_h, prev_N, N)
+        r.set_fractions(F, cfg.instance_level, cfg.bstar, cfg.mode)
+        out = r.route(batches[b])
+        torch.cuda.synchronize()
+        st = r.stats()
+        g = _host(out)
+        sl = slice(8 * b, 8 * b + 8)
+        o_ids, o_sc, valid = o_ids_all[sl], o_sc_all[sl], valid_all[sl]
+        gid = g["topk_id"].reshape(N, k)[idx[b]]
+        gsc = g["topk_score"].reshape(N, k)[idx[b]]
+        rep = Report()
+        rows = w.rows_at(torch.from_numpy(np.maximum(gid, 0).reshape(-1))).cpu().numpy().reshape(8, k, -1)
+        check_topk(gid, gsc, o_ids, o_sc, rep, Ps[sl], rows)
+        glev = _levels(cfg, g["K"])
+        o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid)
+        check_levels(glev[idx[b]], o_sc[:, 0], o_lev, valid, cfg.thresholds, rep)
+        setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=F, instance_level=cfg.instance_level,
+                        bstar=cfg.bstar, mode=cfg.mode, topk=k, seed=cfg.route_seed, batch_seq=b)
+        check_downstream(g, glev, setup, st, rep, len(cfg.instance_level))
+        print(f"C5 N={N}", rep.summary(), "F", [round(f, 4) for f in F], "h", st["h"], "D_Q", st["D_Q"])
+        prev_h, prev_N = st["h"], N
+    assert st["D_Q"] >= 0 and F[-1] > 0.5     # the peak-load batch leans on K = 25 (P:199)
+    r.close()
+
+
 # ------------------------------------------------------------------------------------------------
 def _small(pas, cache: torch.Tensor, P: torch.Tensor, topk=8, mode=0, bstar=4, name="C1"):
     cfg = CONFIGS[name]
@@ -419,3 +474,46 @@ def test_nccl_collective_path_single_rank(pas):
     for key in ("K", "K_prime", "instance", "slot", "topk_id", "topk_score", "bucket_prompts"):
         assert np.array_equal(got[key], ref[key]), key
     r.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# K2 dynamic schedule (DESIGN.md 8 "K2 schedule"): chunked units handed out by a global counter with
+# the top-k lists parked between chunks.
+def test_k2_dynamic_schedule_full_oracle_k16(pas, monkeypatch):
+    """Ragged N = 2,200 (18 prompt tiles: the single-CTA tile, 17 ranges, chunks of 10 tiles) against a
+    ragged 90,017-row cache with k = 16 (the KMAX = 16 parked lists): full oracle parity.  The ranges
+    are short, so the dynamic schedule is forced down to 2 chunk steps (PAS_K2_DYN_MIN_STEPS)."""
+    monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "2")
+    monkeypatch.setenv("PAS_K2_DYN_MB", "40")
+    rep, st = _full_parity(pas, CONFIGS["C2"], N=2200, M=90_017, topk=16)
+    assert st["k2_chunk_tiles"] > 0 and st["k2_chunk_steps"] >= 2, st
+    print(rep.summary(), "R", st["k2_ranges"], "T", st["k2_chunk_tiles"], "CS", st["k2_chunk_steps"])
+
+
+@pytest.mark.parametrize("N,M,topk", [(16384, 400_003, 8), (4097, 250_000, 3)])
+def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, monkeypatch):
+    """Every output of the dynamic schedule byte-identical to the static one (same MMA sums, exact
+    top-k with the same tie rule, whatever the split into ranges and chunks), over three batches so
+    the epoch-tagged chunk counters and the re-armed unit counter are exercised across launches."""
+    cfg = CONFIGS["C3"]
+    monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "2")
+    w = Workload(cfg, device=DEV, M=M)
+    C_ = w.cache_rows(0, M).contiguous()
+    res = {}
+    for sched in ("dynamic", "static"):
+        if sched == "static":
+            monkeypatch.setenv("PAS_K2_SCHED", "static")
+        r = _router(pas, cfg, N, M, topk=topk)
+        r.load_cache(C_)
+        outs = []
+        for b in range(3):
+            outs.append(_host(r.route(w.prompts(N, batch=b))))
+            torch.cuda.synchronize()
+            st = r.stats()
+            assert (st["k2_chunk_tiles"] > 0) == (sched == "dynamic"), st
+        res[sched] = outs
+        r.close()
+    monkeypatch.delenv("PAS_K2_SCHED")
+    for a, b in zip(res["dynamic"], res["static"]):
+        for key in a:
+            assert np.array_equal(a[key], b[key]), key

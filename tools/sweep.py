@@ -12,7 +12,6 @@ JSON object per line.  The cache is generated on the GPU block by block (synth-v
 """
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -35,7 +34,7 @@ def main():
     import torch
 
     from paper_2502_06798_b200 import pas
-    from synth import CONFIGS, Workload
+    from synth import CONFIGS, Workload, c5_fractions
 
     dev = torch.device("cuda", 0)
     if args.kind == "cache":
@@ -97,16 +96,12 @@ def main():
         for N in Ns:
             P = Pall[:N].contiguous()
             out = r.alloc_out(N)
-            ell = math.log2(N / 256) / 9
             ms = []
             for i in range(args.warmup + args.steps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 if prev_h is not None:          # controller update from the previous batch's H_K
-                    F = [(1 - ell) * h / prev_N for h in prev_h]
-                    F[-1] += ell
-                    s = sum(F)
-                    F = [f / s for f in F]
+                    F = c5_fractions(prev_h, prev_N, N)
                     r.set_fractions(F, cfg.instance_level, cfg.bstar, cfg.mode)
                 r.route(P, out)
                 e1.record()

@@ -40,6 +40,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 #include "pas_internal.cuh"
 #include "ptx_sm100.cuh"
@@ -48,7 +49,14 @@
 // the single-CTA tile above that (A/B in DESIGN.md 8: the pair is faster where K2 is latency- and
 // L2-bound, the single CTA where it is power-bound).  0 disables the pair; a huge value forces it.
 #ifndef PAS_K2_PAIR_MAX_TILES
-#define PAS_K2_PAIR_MAX_TILES 16
+#define PAS_K2_PAIR_MAX_TILES 4
+#endif
+
+#ifndef PAS_K2_EPI_ARGMAX
+#define PAS_K2_EPI_ARGMAX 1   // top-k insert path: repeated chunk max + knock-out (0: column-order scan)
+#endif
+#ifndef PAS_K2_EPI_VOTE
+#define PAS_K2_EPI_VOTE 0     // with ARGMAX=0: a warp vote per column before its insert (measured slower)
 #endif
 
 namespace pas {
@@ -97,9 +105,35 @@ __device__ __forceinline__ int opaque(int x) {
   return x;
 }
 
+__device__ __forceinline__ float max32(const uint32_t (&v)[32]) {
+  float mx = __uint_as_float(v[0]);
+#pragma unroll
+  for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+  return mx;
+}
+
+template <int KMAX>
+__device__ __forceinline__ void bubble_insert(float x, int32_t g, float (&s)[KMAX], int32_t (&gl)[KMAX]) {
+  s[KMAX - 1] = x;
+  gl[KMAX - 1] = g;
+#pragma unroll
+  for (int i = KMAX - 1; i > 0; --i) {
+    if (s[i] > s[i - 1]) {
+      const float ts = s[i]; s[i] = s[i - 1]; s[i - 1] = ts;
+      const int32_t tg = gl[i]; gl[i] = gl[i - 1]; gl[i - 1] = tg;
+    }
+  }
+}
+
 // Epilogue over one accumulator: 32-column chunks (tcgen05.ld), chain max (FMNMX3), the column id
-// materialised only inside the (rare) insert path, the tail mask only on the last partial tile.
-// (A double-buffered tcgen05.ld + tree-max variant was 7 % slower under the power cap: DESIGN.md 8.)
+// materialised only inside the insert path, the tail mask only on the last partial tile.
+// Insert path (PAS_K2_EPI_ARGMAX, default): while the chunk max beats the k-th best, insert it and knock
+// it out (lowest column among equal values), so a lane pays per candidate, not per column; a warp pays
+// the most candidates of any lane.  Inserting in value order (ties: column ascending) with a strict >
+// keeps the list the top-k under (score desc, column asc), exactly as the column-order scan does.
+// Measured alternatives: the column-order scan of all 32 columns (PAS_K2_EPI_ARGMAX=0;
+// a warp pays 32 bubble inserts whenever any lane has a candidate), a warp-vote per column on top of it
+// (PAS_K2_EPI_VOTE=1, slower still), a double-buffered tcgen05.ld + tree max (7 % slower).
 template <int KMAX, bool PARTIAL, int NCH = BN / 64>
 __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_local, float (&s)[KMAX],
                                             int32_t (&gl)[KMAX]) {
@@ -114,26 +148,39 @@ __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_loc
       for (int j = 0; j < 32; ++j)
         if (base + j >= M_local) v[j] = __float_as_uint(-INFINITY);
     }
-    float mx = __uint_as_float(v[0]);
+    float mx = max32(v);
+#if PAS_K2_EPI_ARGMAX
+    while (mx > s[KMAX - 1]) {
+      int col = 0;
+      bool hit = false;
 #pragma unroll
-    for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
+      for (int j = 0; j < 32; ++j) {
+        const bool h = !hit && __uint_as_float(v[j]) == mx;
+        col = h ? j : col;
+        v[j] = h ? __float_as_uint(-INFINITY) : v[j];
+        hit = hit || h;
+      }
+      bubble_insert<KMAX>(mx, base + col, s, gl);
+      mx = max32(v);
+    }
+#elif PAS_K2_EPI_VOTE
+    if (__any_sync(0xffffffffu, mx > s[KMAX - 1])) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = __uint_as_float(v[j]);
+        if (!__any_sync(0xffffffffu, x > s[KMAX - 1])) continue;
+        if (x > s[KMAX - 1]) bubble_insert<KMAX>(x, base + j, s, gl);
+      }
+    }
+#else
     if (mx > s[KMAX - 1]) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float x = __uint_as_float(v[j]);
-        if (x > s[KMAX - 1]) {
-          s[KMAX - 1] = x;
-          gl[KMAX - 1] = base + j;
-#pragma unroll
-          for (int i = KMAX - 1; i > 0; --i) {
-            if (s[i] > s[i - 1]) {
-              const float ts = s[i]; s[i] = s[i - 1]; s[i - 1] = ts;
-              const int32_t tg = gl[i]; gl[i] = gl[i - 1]; gl[i - 1] = tg;
-            }
-          }
-        }
+        if (x > s[KMAX - 1]) bubble_insert<KMAX>(x, base + j, s, gl);
       }
     }
+#endif
   }
 }
 
@@ -188,16 +235,24 @@ __device__ __noinline__ void leash_wait(uint64_t* progress, int worker, int nwor
   }
 }
 
-// Dynamic schedule (DESIGN.md 8 "K2 schedule"): unit u = (chunk step c, range r, prompt tile m), m
-// fastest, then r, then c; chunk c of range r = its tiles [t0 + cT, t0 + (c+1)T) (possibly empty).
-__device__ __forceinline__ void dyn_decode(int u, int MT, int R, int NT, int T, int& c, int& j, int& ta, int& tb) {
-  const int P = MT * R;
-  c = u / P;
-  j = u - c * P;
-  const int r = j / MT;
+// Dynamic schedule (DESIGN.md 8 "K2 schedule"): prompt tiles in groups of MTg; within a group, unit
+// u = (chunk step c, range r, prompt tile m), m fastest, then r, then c; chunk c of range r = its tiles
+// [t0 + cT, t0 + (c+1)T) (possibly empty).  j = r * MT + m is the (range, prompt tile) slot.
+__device__ __forceinline__ void dyn_decode(int u, int MT, int R, int NT, const DynSched& dy, int& c, int& j,
+                                           int& ta, int& tb) {
+  const int per_group = dy.CS * R * dy.MTg;
+  const int g = u / per_group;
+  const int ui = u - g * per_group;
+  const int m0 = g * dy.MTg;
+  const int mg = min(dy.MTg, MT - m0);
+  const int P = mg * R;
+  c = ui / P;
+  const int ji = ui - c * P;
+  const int r = ji / mg;
+  j = r * MT + m0 + (ji - r * mg);
   const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-  ta = min(t1, t0 + c * T);
-  tb = min(t1, ta + T);
+  ta = min(t1, t0 + c * dy.T);
+  tb = min(t1, ta + dy.T);
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
@@ -296,7 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
           if (u >= units) break;
           int c, j, ta, tb;
-          dyn_decode(u, MT, R, NT, dyn.T, c, j, ta, tb);
+          dyn_decode(u, MT, R, NT, dyn, c, j, ta, tb);
           const int qrow = (j % MT) * BM;
           for (int t = ta; t < tb; ++t) {
             for (int kb = 0; kb < kblocks; ++kb) {
@@ -370,7 +425,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
           if (u < 0) break;
           int c, j;
-          dyn_decode(u, MT, R, NT, dyn.T, c, j, t0, t1);
+          dyn_decode(u, MT, R, NT, dyn, c, j, t0, t1);
         } else {
           const int r = u / MT;
           t0 = (int)((int64_t)r * NT / R);
@@ -423,7 +478,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) ptx::mbar_arrive(&bars->uempty[us]);
         if (++us == UNIT_RING) { us = 0; uph ^= 1; }
         if (u < 0) break;
-        dyn_decode(u, MT, R, NT, dyn.T, c, j, t0, t1);
+        dyn_decode(u, MT, R, NT, dyn, c, j, t0, t1);
         m = j % MT;
         r = j / MT;
       } else {
@@ -769,7 +824,13 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
 #define PAS_K2_ATMEM 0
 #endif
 bool simtopk_uses_tmem_a(int d) { return PAS_K2_ATMEM && d <= 2 * TA_ACC_COL; }
-bool simtopk_pair(int64_t N, int d) { return !simtopk_uses_tmem_a(d) && (N + BM - 1) / BM <= PAS_K2_PAIR_MAX_TILES; }
+bool simtopk_pair(int64_t N, int d) {
+  static const int max_tiles = [] {   // A/B experiments: PAS_K2_PAIR_MAX_TILES in the environment
+    const char* v = getenv("PAS_K2_PAIR_MAX_TILES");
+    return v ? atoi(v) : PAS_K2_PAIR_MAX_TILES;
+  }();
+  return !simtopk_uses_tmem_a(d) && (N + BM - 1) / BM <= max_tiles;
+}
 int simtopk_prompt_rows() { return Tile<true>::UNIT_ROWS; }   // prompt buffers are padded to whole pair tiles
 int simtopk_box_q() { return BM; }
 int simtopk_box_c(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : Tile<false>::BN_CTA; }
@@ -803,10 +864,13 @@ cudaError_t simtopk_init() {
 // the unit that resumes (r, m) is handed out that many units after the one that parks it (it almost
 // never waits); R * N within the candidate buffer and R * MT within the parked-list buffer.
 #ifndef PAS_K2_DYN_MB
-#define PAS_K2_DYN_MB 80          // L2 budget for the chunks streamed concurrently
+#define PAS_K2_DYN_MB 100         // L2 budget for the chunks streamed concurrently
+#endif
+#ifndef PAS_K2_DYN_AMB
+#define PAS_K2_DYN_AMB 4096       // L2 budget for one group's prompt tiles (MB; default: one group)
 #endif
 #ifndef PAS_K2_DYN_TMAX
-#define PAS_K2_DYN_TMAX 64        // longest chunk (tiles)
+#define PAS_K2_DYN_TMAX 128       // longest chunk (tiles)
 #endif
 #ifndef PAS_K2_DYN_MIN_PAIRS
 #define PAS_K2_DYN_MIN_PAIRS 2
@@ -819,17 +883,28 @@ static int env_int(const char* name, int dflt) {   // A/B experiments only
   return v ? atoi(v) : dflt;
 }
 bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R_out,
-                          int* T_out, int* CS_out) {
+                          int* T_out, int* CS_out, int* MTg_out) {
   const int budget_mb = env_int("PAS_K2_DYN_MB", PAS_K2_DYN_MB);
   if (budget_mb <= 0 || simtopk_uses_tmem_a(d) || simtopk_pair(N, d)) return false;
   const int64_t MT = (N + BM - 1) / BM;
   const int64_t NT = (M_local + BN - 1) / BN;
   if (MT <= 0 || NT <= 0) return false;
   const int64_t want = (int64_t)env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS) * Tile<false>::NUM_WORKERS;
-  const int64_t R = (want + MT - 1) / MT;
-  if (R > NT || R * N > cand_rows || R * MT > state_tiles || R > 128) return false;
+  // prompt-tile groups: every chunk step of a group re-reads all of its prompt tiles (A, kept in L2
+  // with evict_last), so a group's A must leave L2 room for the chunks; each group streams the cache
+  // once.  Never split below `want` (range, prompt tile) pairs per group.
+  const int64_t a_bytes = (int64_t)MT * BM * d * 2;
+  const int64_t a_budget = (int64_t)std::max(env_int("PAS_K2_DYN_AMB", PAS_K2_DYN_AMB), 1) << 20;
+  int64_t groups = std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, MT), MTg, R;
+  for (;; --groups) {   // fewer groups (more ranges per group) until the candidate buffers hold R ranges
+    MTg = (MT + groups - 1) / groups;
+    R = std::min<int64_t>((want + MTg - 1) / MTg, 128);   // the S-way merge takes S <= 128 sources
+    if (groups == 1 || (R <= NT && R * N <= cand_rows && R * MT <= state_tiles)) break;
+  }
+  if (R > NT || R * N > cand_rows || R * MT > state_tiles) return false;
+  if (R * MTg < Tile<false>::NUM_WORKERS) return false;      // less than one unit per SM per chunk step
   // chunks in flight: the ranges one window of 148 consecutive units spans, plus the next step's
-  const int64_t in_flight = (Tile<false>::NUM_WORKERS + MT - 1) / MT + 1;
+  const int64_t in_flight = (Tile<false>::NUM_WORKERS + MTg - 1) / MTg + 1;
   const int64_t tile_bytes = (int64_t)BN * d * 2;
   int64_t T = ((int64_t)budget_mb << 20) / (in_flight * tile_bytes);
   if (T < 4) T = 4;
@@ -840,6 +915,7 @@ bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t
   *R_out = (int)R;
   *T_out = (int)T;
   *CS_out = (int)((L + T - 1) / T);
+  *MTg_out = (int)MTg;
   return true;
 }
 

@@ -307,7 +307,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
     const char* sched = getenv("PAS_K2_SCHED");    // "static": A/B experiments only
     const bool dyn_ok = !(sched && !strcmp(sched, "static")) &&
                         simtopk_plan_dynamic(N, ctx->M_local, ctx->cand_cap, ctx->k2_state_tiles, ctx->cfg.d, &R,
-                                             &dyn.T, &dyn.CS);
+                                             &dyn.T, &dyn.CS, &dyn.MTg);
     if (dyn_ok) {
       dyn.st_s = ctx->k2_st_s;
       dyn.st_g = ctx->k2_st_g;

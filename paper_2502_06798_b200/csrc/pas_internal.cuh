@@ -139,6 +139,7 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
 struct DynSched {
   int T = 0;                    // cache tiles per chunk
   int CS = 0;                   // chunk steps per range
+  int MTg = 0;                  // prompt tiles per group (each group streams the cache once)
   float* st_s = nullptr;        // [R*MT][2][KMAX][128] parked scores
   int32_t* st_g = nullptr;      // [R*MT][2][KMAX][128] parked local rows
   uint64_t* done = nullptr;     // [R*MT] epoch << 32 | chunks done
@@ -165,7 +166,7 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 // The dynamic schedule's ranges R and chunk T for this batch, or false when the static schedule
 // serves it (CTA-pair tile, too few units, or more parked lists than `state_tiles` prompt tiles).
 bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R,
-                          int* T, int* CS);
+                          int* T, int* CS, int* MTg);
 bool simtopk_uses_tmem_a(int d);
 bool simtopk_pair(int64_t N, int d);   // the CTA-pair tile serves this batch size
 cudaError_t simtopk_init();

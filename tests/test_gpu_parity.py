@@ -304,6 +304,37 @@ def test_virtual_shards_match_single_gpu(pas):
             r.close()
 
 
+def test_virtual_shards_dynamic_schedule(pas, monkeypatch):
+    """The sharded data path where K2 runs its dynamic schedule on each shard (4,097 prompts vs a
+    400,003-row cache, forced down to 2 chunk steps): G = 2 and 4 byte-identical to G = 1."""
+    monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "2")
+    cfg = CONFIGS["C3"]
+    N, M = 4097, 400_003
+    w = Workload(cfg, device=DEV, M=M)
+    C_ = w.cache_rows(0, M).contiguous()
+    P = w.prompts(N)
+    r1 = _router(pas, cfg, N, M)
+    r1.load_cache(C_)
+    ref = _host(r1.route(P))
+    torch.cuda.synchronize()
+    assert r1.stats()["k2_chunk_tiles"] > 0
+    r1.close()
+    for G in (2, 4):
+        ctxs = [_router(pas, cfg, N, (M + G - 1) // G, world=G, rank=r) for r in range(G)]
+        cands = torch.empty(G, N * cfg.topk, dtype=torch.int64, device=DEV)
+        for rk, r in enumerate(ctxs):
+            r.load_cache(C_)
+            pas.pas_route_local(r.ctx, P, cands[rk])
+        out = ctxs[0].alloc_out(N)
+        pas.pas_route_from_candidates(ctxs[0].ctx, cands, G, N, out)
+        torch.cuda.synchronize()
+        got = _host(out)
+        for key in ("K", "K_prime", "instance", "slot", "topk_id", "topk_score", "bucket_prompts"):
+            assert np.array_equal(got[key], ref[key]), (G, key)
+        for r in ctxs:
+            r.close()
+
+
 def test_determinism_and_batch_seq(pas):
     cfg = CONFIGS["C2"]
     w = Workload(cfg, device=DEV, M=3000)

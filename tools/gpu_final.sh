@@ -21,3 +21,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_simtopk -c 1 -o $O/k2_c4_g1 $CMD > $O/ncu_full.log 2>&1; echo "ncu2 rc=$?" >> $O/ncu_full.log
 timeout 600 python tools/bench_stream.py > $O/stream_64M.json 2> $O/stream.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_|k6_" --csv --log-file $O/stream_launches_64M.csv python tools/bench_stream.py --reps 1 > $O/stream_ncu.log 2>&1; echo "ncu3 rc=$?" >> $O/stream_ncu.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_normalize|k_select_s1|k_cls_rank" -c 3 -o $O/stream_k1k3k7 python tools/bench_stream.py --reps 1 > $O/ncu_stream_full.log 2>&1; echo "ncu4 rc=$?" >> $O/ncu_stream_full.log

@@ -342,6 +342,14 @@ int pas_last_launch_count(const pas_ctx* ctx);
 pas_status pas_debug_scores(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N, float* scores_dev,
                             pas_stream stream);
 
+/* The K2 work schedule a batch of N prompts against M_local rows of width d would get in a context of
+ * max_batch prompts (host logic only, no device; DESIGN.md 8 "K2 schedule").  out[8] receives:
+ * R (cache ranges per prompt tile = sources of the merge), T (cache tiles per chunk; 0 = static
+ * schedule), CS (chunk steps per range), MTg (prompt tiles per group), pair (1 = CTA-pair tile),
+ * MT (prompt tiles of 128), NT (cache tiles of 256), cand_cap (candidate rows: R * N <= cand_cap).
+ * Errors: PAS_ERR_ARG. */
+pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_batch, int* out);
+
 #ifdef __cplusplus
 }
 #endif

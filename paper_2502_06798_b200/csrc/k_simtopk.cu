@@ -8,35 +8,34 @@
 //
 // Two tile organisations share one source (template parameter), dispatched by batch size
 // (simtopk_pair; DESIGN.md section 8 records the A/B on one B200):
-//   single CTA (N > 2048) tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
+//   single CTA (N > 512)  tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
 //                         instruction; per stage A 128x64 + B 256x64 bf16 (48 KB), 4 stages.
-//   CTA pair (N <= 2048)  tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
+//   CTA pair (N <= 512)   tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
 //                         128..255 in CTA 1; the 256 cache rows of B split 128/128 between the two
 //                         CTAs' smem (32 KB / stage, 6 stages); TMA bytes of both CTAs land on the
 //                         leader's mbarrier; commits multicast to both CTAs.
 //
-// Work unit = (prompt tile m, cache range r of whole 256-row tiles).  Persistent CTAs / pairs walk
-// units u = id + i*count with m fastest, so concurrently running CTAs stream the SAME cache tiles
-// (L2 reuse of the big operand) against different prompt tiles.
-//
-// Progress leash (used only for small N, see simtopk_leash_slack).  CTAs that stream the same cache
-// range in the same wave re-use each tile from L2 only while they stay within L2's reach of each
-// other; free-running, they drift apart by more than that over a range of thousands of tiles and
-// tiles are fetched from DRAM again and again (C4: 491 GB of DRAM reads per launch for a 15.4 GB
-// cache).  So each producer warp publishes its tile count (epoch-tagged, one 8-B word per CTA or
-// pair) and, before issuing a tile, waits until it is at most
-// `slack` tiles ahead of the slowest CTA still working; slack is sized so that the tiles between
-// the slowest and the fastest CTA of every concurrently streamed range fit in a share of L2.
+// Two schedules:
+//   dynamic (single-CTA tile, long ranges; simtopk_plan_dynamic): units (chunk step, range, prompt
+//     tile) of T cache tiles handed out by a global counter, the top-k lists parked in L2 between a
+//     (range, prompt tile)'s chunks -- the CTAs stay within one chunk step of each other whatever
+//     their speed, so the cache crosses HBM about once and fast SMs take more units.
+//   static (CTA pair, short ranges): unit = (prompt tile m, cache range r); persistent CTAs / pairs
+//     walk units u = id + i*count with m fastest, so concurrently running CTAs stream the SAME cache
+//     tiles against different prompt tiles.  Progress leash (small N only, simtopk_leash_slack): free
+//     running, CTAs drift apart over a range of thousands of tiles by more than L2 holds and tiles are
+//     fetched from DRAM again and again, so each producer publishes its tile count (epoch-tagged) and
+//     waits while it is more than `slack` tiles ahead of the slowest CTA still working.
 //
 // Warp roles per CTA (320 threads, 1 CTA/SM):
-//   warp 0      TMA producer (128-B swizzle, mbarrier complete_tx).
+//   warp 0      TMA producer (128-B swizzle, mbarrier complete_tx); in the dynamic schedule it also
+//               takes the units and publishes them through a 4-entry mbarrier ring.
 //   warp 1      TMEM allocation (512 columns = two 256-column fp32 accumulators) and one lane issuing
 //               tcgen05.mma + tcgen05.commit (smem stage released, accumulator ready).
 //   warps 2..9  epilogue over the CTA's 128 TMEM lanes, two warps per lane quarter (column halves
 //               0..127 / 128..255 of every tile, each with its own top-k list, merged by a bitonic
-//               network at the end of the unit): tcgen05.ld of 32 columns, max of the chunk vs the
-//               current k-th score, and only when the chunk can improve the list a branch-free
-//               bubble insert (strict >, columns ascending, so equal scores keep the lower column).
+//               network at the end of the range): tcgen05.ld of 32 columns, max of the chunk vs the
+//               current k-th score, and while it beats it, insert the max and knock it out (epi_tile).
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <climits>
 #include <cstring>
 #include <string>
 
@@ -264,6 +265,30 @@ pas_status ready(pas_ctx* ctx, int64_t N) {
   return PAS_OK;
 }
 
+// K2 candidate and parked-list capacities for a context of max_batch prompts (pas_create).
+int64_t k2_cand_cap(int64_t max_batch) {
+  const int64_t qt = simtopk_prompt_rows();
+  return 4 * max_batch > 592 * qt ? 4 * max_batch : 592 * qt;
+}
+int64_t k2_state_tiles(int64_t cand_cap) { return cand_cap / simtopk_box_q() + 8; }
+
+// The K2 schedule of one batch: the dynamic schedule when simtopk_plan_dynamic takes it (dyn.T > 0),
+// else the static ranges.  Returns R (the S of the merge).  Host only.
+int k2_schedule(int64_t N, int64_t M_local, int d, int64_t cand_cap, DynSched* dyn) {
+  int R = 1;
+  const char* sched = getenv("PAS_K2_SCHED");    // "static": A/B experiments only
+  if (!(sched && !strcmp(sched, "static")) &&
+      simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, &R, &dyn->T, &dyn->CS, &dyn->MTg))
+    return R;
+  dyn->T = dyn->CS = dyn->MTg = 0;
+  R = simtopk_choose_ranges(N, M_local, cand_cap, d);
+  if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
+    const int r = atoi(ov);
+    if (r >= 1 && (int64_t)r * N <= cand_cap) R = r;
+  }
+  return R;
+}
+
 // Prompt-side workspace (Q_hat, validity flags, K2 candidates, NCCL buffers), allocated on the first
 // call that runs a1 + a3, so a context used only through pas_route_from_candidates never holds it.
 pas_status ensure_prompt_ws(pas_ctx* ctx) {
@@ -275,7 +300,7 @@ pas_status ensure_prompt_ws(pas_ctx* ctx) {
   if (e == cudaSuccess) e = dmalloc(&ctx->k2_progress, (size_t)kNumSMs);
   if (e == cudaSuccess) e = cudaMemset(ctx->k2_progress, 0, sizeof(uint64_t) * kNumSMs);   // epoch 0 = none
   // parked lists of the K2 dynamic schedule: one slot per (range, prompt tile), R * MT <= cand_cap / 128 + 8
-  ctx->k2_state_tiles = ctx->cand_cap / simtopk_box_q() + 8;
+  ctx->k2_state_tiles = k2_state_tiles(ctx->cand_cap);
   const size_t st_elems = (size_t)ctx->k2_state_tiles * simtopk_box_q() * 2 * (k <= 8 ? 8 : 16);
   if (e == cudaSuccess) e = dmalloc(&ctx->k2_st_s, st_elems);
   if (e == cudaSuccess) e = dmalloc(&ctx->k2_st_g, st_elems);
@@ -304,21 +329,12 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   int R = 1;
   if (ctx->M_local > 0) {
     DynSched dyn;
-    const char* sched = getenv("PAS_K2_SCHED");    // "static": A/B experiments only
-    const bool dyn_ok = !(sched && !strcmp(sched, "static")) &&
-                        simtopk_plan_dynamic(N, ctx->M_local, ctx->cand_cap, ctx->k2_state_tiles, ctx->cfg.d, &R,
-                                             &dyn.T, &dyn.CS, &dyn.MTg);
-    if (dyn_ok) {
+    R = k2_schedule(N, ctx->M_local, ctx->cfg.d, ctx->cand_cap, &dyn);
+    if (dyn.T > 0) {
       dyn.st_s = ctx->k2_st_s;
       dyn.st_g = ctx->k2_st_g;
       dyn.done = ctx->k2_done;
       dyn.sched = ctx->k2_sched;
-    } else {
-      R = simtopk_choose_ranges(N, ctx->M_local, ctx->cand_cap, ctx->cfg.d);
-      if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
-        const int r = atoi(ov);
-        if (r >= 1 && (int64_t)r * N <= ctx->cand_cap) R = r;
-      }
     }
     if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
@@ -484,7 +500,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->q_rows = (mb + qt - 1) / qt * qt;
   ctx->cap_rows = cfg->max_rows_per_rank;
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
-  ctx->cand_cap = 4 * mb > 592 * qt ? 4 * mb : 592 * qt;
+  ctx->cand_cap = k2_cand_cap(mb);
   const int64_t nb = (int64_t)kMaxLevels << redirect_kb(mb);
   const int64_t ncls = 64 * (int64_t)batch_tiles(mb);
   cudaError_t e = cudaSuccess;
@@ -1163,6 +1179,21 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
 }
 
 // Test hook: K1 + K2 with the epilogue writing every raw score (no top-k); scores_dev [N x M_local].
+pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_batch, int* out) {
+  if (!out || N < 0 || M_local < 0 || d <= 0 || max_batch < N) return PAS_ERR_ARG;
+  DynSched dyn;
+  const int64_t cap = k2_cand_cap(max_batch);
+  out[0] = k2_schedule(N, M_local, d, cap, &dyn);
+  out[1] = dyn.T;
+  out[2] = dyn.CS;
+  out[3] = dyn.MTg;
+  out[4] = simtopk_pair(N, d) ? 1 : 0;
+  out[5] = (int)((N + simtopk_box_q() - 1) / simtopk_box_q());
+  out[6] = (int)((M_local + 255) / 256);
+  out[7] = (int)(cap > INT32_MAX ? INT32_MAX : cap);
+  return PAS_OK;
+}
+
 pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, float* scores_dev,
                             pas_stream stream) {
   pas_status s = check_live(ctx);

@@ -109,6 +109,7 @@ _SIG = {
     "pas_last_error": (C.c_char_p, [_P]),
     "pas_last_launch_count": (C.c_int, [_P]),
     "pas_debug_scores": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
+    "pas_debug_k2_schedule": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int64, _P]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(lib, _name)
@@ -325,6 +326,15 @@ def pas_plan_stats(ctx) -> dict:
 
 def pas_last_launch_count(ctx) -> int:
     return lib.pas_last_launch_count(ctx)
+
+
+def pas_debug_k2_schedule(N, M_local, d=768, max_batch=None) -> dict:
+    """K2's schedule for a batch (host logic, no device): R, T (0 = static), CS, MTg, pair, MT, NT."""
+    out = (C.c_int * 8)()
+    st = lib.pas_debug_k2_schedule(N, M_local, d, N if max_batch is None else max_batch, out)
+    if st != PAS_OK:
+        raise PasError(st, "pas_debug_k2_schedule: bad arguments")
+    return dict(zip(("R", "T", "CS", "MTg", "pair", "MT", "NT", "cand_cap"), list(out)))
 
 
 def pas_debug_scores(ctx, emb, scores, stream=None):

@@ -23,7 +23,7 @@ def lib():
 def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(pas_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(pas_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_calls():

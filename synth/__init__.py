@@ -131,7 +131,11 @@ class Workload:
         self.weights = (w / w.sum()).to(torch.float32)
         self._cent_dev = self.centroids.to(self.device)
         self._tau_dev = self.tau.to(self.device)
-        self._w_dev = self.weights.to(self.device)
+        # cluster draws of cache rows by inverse CDF on a CPU fp64 cumulative sum: regenerating a block
+        # (rows_at) must reproduce it bit for bit, which torch.multinomial on CUDA does not guarantee
+        # (its device cumsum is a decoupled look-back scan whose float summation order varies)
+        cdf = torch.cumsum(w, 0)
+        self._cdf_dev = (cdf / cdf[-1]).to(self.device)
 
     # ---- cache ---------------------------------------------------------------------
     def _gen(self, *key) -> torch.Generator:
@@ -147,7 +151,8 @@ class Workload:
         if rows <= 0:
             return torch.empty(0, self.d, device=self.device)
         g = self._gen(1, b)
-        j = torch.multinomial(self._w_dev, rows, replacement=True, generator=g)
+        u = torch.rand(rows, generator=g, device=self.device, dtype=torch.float64)
+        j = torch.searchsorted(self._cdf_dev, u, right=True).clamp_(max=self.C - 1)
         noise = torch.randn(rows, self.d, generator=g, device=self.device)
         scale = 0.5 + 1.5 * torch.rand(rows, 1, generator=g, device=self.device)
         row = _unit(self._cent_dev[j] + self._tau_dev[j, None] * noise / math.sqrt(self.d))

@@ -2,6 +2,9 @@
 """Sweeps behind BASELINE's metric "prompts scheduled/s vs cache size" on one B200.
 
   --kind cache   N = 16,384 prompts vs M in {1k, 100k, 1M, 10M, 50M} (SURVEY 8(d) "sweep" row)
+  --kind shard   C4 (65,536 prompts) against one rank's share of the 10M cache at G = 1, 2, 4, 8: the K2
+                 work of one router GPU under row sharding, measured on one B200 (the NCCL all-gather of
+                 8 N k G bytes and the G-way merge are NOT included: a per-rank share, not a multi-GPU run)
   --kind load    C5: N = 256 .. 131,072 (x2) vs a 50M-entry cache, F(K) recomputed before every
                  batch from the previous batch's H_K (F_b = (1 - l_b) h_{b-1} / N_{b-1} + l_b e_{K=25},
                  l_b = log2(N_b / 256) / 9), the pas_set_fractions call timed
@@ -23,7 +26,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kind", choices=["cache", "load"], default="cache")
+    ap.add_argument("--kind", choices=["cache", "load", "shard"], default="cache")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--max-cache", type=int, default=50_000_000)
@@ -37,10 +40,13 @@ def main():
     from synth import CONFIGS, Workload, c5_fractions
 
     dev = torch.device("cuda", 0)
-    if args.kind == "cache":
+    if args.kind in ("cache", "shard"):
         cfg = CONFIGS["C4"]
         N = 16384
         sizes = [m for m in (1_000, 100_000, 1_000_000, 10_000_000, 50_000_000) if m <= args.max_cache]
+        if args.kind == "shard":      # one rank's share of C4 at G = 1, 2, 4, 8 (round-robin rows)
+            N = cfg.N
+            sizes = [(cfg.M + g - 1) // g for g in (1, 2, 4, 8)]
         for M in sizes:
             w = Workload(cfg, device=dev, M=M)
             r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=M, device=0, seed=cfg.route_seed)
@@ -65,7 +71,7 @@ def main():
                     k2.append(r.stats()["stage_ms"][1])
             med = statistics.median(ms)
             tf = 2.0 * N * M * cfg.d / (statistics.median(k2) / 1e3) / 1e12
-            print(json.dumps({"kind": "cache", "N": N, "M": M, "prompts_per_s": N / (med / 1e3), "ms_median": med,
+            print(json.dumps({"kind": args.kind, "N": N, "M": M, "prompts_per_s": N / (med / 1e3), "ms_median": med,
                               "ms_p10": sorted(ms)[max(0, len(ms) // 10)], "ms_p90": sorted(ms)[min(len(ms) - 1, (9 * len(ms)) // 10)],
                               "k2_tflops": tf, "cache_load_s": round(load_s, 2)}), flush=True)
             r.close()

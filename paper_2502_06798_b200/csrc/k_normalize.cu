@@ -5,7 +5,11 @@
 // product, which K2 computes on the tensor cores.  A row with a non-finite element or zero norm is
 // invalid (R16): it is written as zeros and flagged (prompts) or counted (cache insert -> rejected).
 //
-// One warp per row, 128-bit loads (4 fp32 / 4 bf16 per lane per step), the row held in registers.
+// One warp per row, 128-bit loads (4 fp32 / 4 bf16 per lane per step); the row's loads are all in
+// flight at once for the fp64 sum of squares, then the row is re-read (an L1 / L2 hit, no HBM bytes)
+// for the quantised stores, so no value is live across the reduction: 40 registers, 6 resident CTAs
+// (48 warps) per SM.  Measured (profiles/r01_k1c): cache insert 5.02 TB/s vs 4.56 with
+// the row held in registers at 3 CTAs/SM (80 registers) and 4.78 at 4 CTAs/SM (64 registers, spills).
 // HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
 // Cache insert applies the shard filter of the round-robin partition (gid g lives on rank g % G at
 // local row g / G) and reads only this rank's rows.
@@ -54,11 +58,20 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
   *reinterpret_cast<uint2*>(dst) = pk;
 }
 
-// One warp per row.  VEC = d / 128 float4 (or 4 x bf16) per lane: the whole row is held in registers
-// so all its loads are in flight at once and the row is read from HBM exactly once; VEC = 0 is the
-// generic two-pass path for d > 1024.
+// One warp per row.  VEC = d / 128 float4 (or 4 x bf16) per lane: all of a row's loads are in flight
+// at once and the row is read from HBM exactly once; VEC = 0 is the generic two-pass path for d > 1024.
+#ifndef PAS_K1_MINB
+#define PAS_K1_MINB 6     // resident CTAs of 256 threads per SM (register budget 65536 / (256 MINB))
+#endif
+#ifndef PAS_K1_RELOAD
+#define PAS_K1_RELOAD 1   // re-read the row for the stores (fewer live registers, more resident warps)
+#endif
+#ifndef PAS_K1_ACC
+#define PAS_K1_ACC 1      // independent fp64 partial sums per lane (shorter DFMA dependency chain)
+#endif
+
 template <typename T, int VEC>
-__global__ void __launch_bounds__(256, 3) k_normalize(const T* __restrict__ in, int64_t rows, int d,
+__global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count) {
   pdl_entry();
@@ -77,20 +90,35 @@ __global__ void __launch_bounds__(256, 3) k_normalize(const T* __restrict__ in, 
       float v[VEC][4];
 #pragma unroll
       for (int c = 0; c < VEC; ++c) load4(src + c * 128 + lane * 4, v[c]);
+      double part[PAS_K1_ACC];
+#pragma unroll
+      for (int a = 0; a < PAS_K1_ACC; ++a) part[a] = 0.0;
 #pragma unroll
       for (int c = 0; c < VEC; ++c)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           finite &= isfinite(v[c][j]);
-          ss += (double)v[c][j] * (double)v[c][j];
+          part[(c * 4 + j) % PAS_K1_ACC] += (double)v[c][j] * (double)v[c][j];
         }
+#pragma unroll
+      for (int a = 0; a < PAS_K1_ACC; ++a) ss += part[a];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       finite = __all_sync(0xffffffffu, finite);
       const double norm = sqrt(ss);
       const bool valid = finite && norm > 0.0;
+#if PAS_K1_RELOAD
+      // the row is re-read (L1 / L2 hit, no HBM traffic) instead of held across the reduction
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        float w[4];
+        load4(src + c * 128 + lane * 4, w);
+        store_row4(dst + c * 128 + lane * 4, w, norm, valid);
+      }
+#else
 #pragma unroll
       for (int c = 0; c < VEC; ++c) store_row4(dst + c * 128 + lane * 4, v[c], norm, valid);
+#endif
       if (lane == 0) {
         if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
         if (!valid && invalid_count) atomicAdd(invalid_count, 1);
@@ -130,7 +158,7 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
   const int vec = d % 128 == 0 && d <= 1024 ? d / 128 : 0;
   // grid = exactly the resident CTAs (3 per SM by the launch bounds): one wave, grid-stride rows
   int64_t blocks = (rows * 32 + threads - 1) / threads;
-  const int64_t cap = (int64_t)kNumSMs * 3;
+  const int64_t cap = (int64_t)kNumSMs * PAS_K1_MINB;
   if (blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
   switch (vec) {

@@ -98,8 +98,12 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
   }
 }
 
+#ifndef PAS_K7_MINB
+#define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers, no spills
+#endif
+
 template <bool DISP>   // DISP: the f3 stateful dispatcher picks (a separate instantiation keeps R13 lean)
-__global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
+__global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
                                                       int32_t* __restrict__ slot, int32_t* __restrict__ prompts,
@@ -164,16 +168,18 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
   }
   // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count
   // per class (bumped by the lowest lane of each group) carries the earlier rows
+  // the rank is packed above the class byte (c[j] = rank << 8 | class, class 0xFF past the end): one
+  // register per row instead of two
   const unsigned lt = (1u << lane) - 1;
-  int r[ROWS];
 #pragma unroll
   for (int j = 0; j < ROWS; ++j) {
     const unsigned m = __match_any_sync(0xffffffffu, c[j]);
     const bool lead = lane == __ffs(m) - 1;
-    r[j] = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
+    const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
     __syncwarp();
     if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
     __syncwarp();
+    c[j] = (r << 8) | (c[j] & 0xFF);
   }
   __syncthreads();
   if (threadIdx.x < nC) {   // exclusive prefix over warps, per class
@@ -188,29 +194,30 @@ __global__ void __launch_bounds__(THREADS) k_cls_rank(const uint8_t* __restrict_
 #pragma unroll
   for (int j = 0; j < ROWS; ++j) {
     const int64_t p = base + 32 * j + lane;
-    if (c[j] < 0) continue;
-    const int t = tile_off[c[j]] + wcnt[w][c[j]] + r[j];
+    const int cj = c[j] & 0xFF, rj = c[j] >> 8;
+    if (cj == 0xFF) continue;
+    const int t = tile_off[cj] + wcnt[w][cj] + rj;
     int inst, sl, pos;
     if (DISP) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
       int64_t sl64;
       if (P.mode == PAS_UNIFORM) {
-        inst = c[j];
+        inst = cj;
         sl64 = P.dplan->Q0[inst] + t;
       } else {
-        disp_pick_greedy(P.dplan, ilist_s[c[j]], ninst_s[c[j]], c[j], t, P.bstar, inst, sl64);
+        disp_pick_greedy(P.dplan, ilist_s[cj], ninst_s[cj], cj, t, P.bstar, inst, sl64);
       }
       sl = (int)sl64;
       pos = (int)(sl64 - P.dplan->Q0[inst]);
     } else if (P.mode == PAS_UNIFORM) {
-      inst = c[j];
+      inst = cj;
       sl = t;
     } else {
       // q1 = t div b*, q2 = q1 div n_j (exact multiply-high, t < 2^26, n_j <= 64):
       // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
       const uint32_t b = (uint32_t)P.bstar;
       const uint32_t q1 = P.bstar_shift >= 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
-      const uint32_t q2 = (uint32_t)(((uint64_t)q1 * magic_s[c[j]]) >> 32);
-      inst = ilist_s[c[j]][q1 - q2 * (uint32_t)ninst_s[c[j]]];
+      const uint32_t q2 = (uint32_t)(((uint64_t)q1 * magic_s[cj]) >> 32);
+      inst = ilist_s[cj][q1 - q2 * (uint32_t)ninst_s[cj]];
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
     if (!DISP) pos = sl;

@@ -155,15 +155,28 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
     icount[i] = cnt;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int i = 0; i <= P.W; ++i) {
-      ioff[i] = run;
-      if (tile == 0) {
-        if (user_off) user_off[i] = run;
-        if (i < P.W) plan->inst_count[i] = icount[i];
+  if (w == 0) {   // batch-list offsets: exclusive scan of the W <= 64 instance counts, two per lane
+    static_assert(kMaxInst <= 64, "two instances per lane");
+    const int i0 = 2 * lane, i1 = 2 * lane + 1;
+    const int a = i0 < P.W ? icount[i0] : 0, b = i1 < P.W ? icount[i1] : 0;
+    int incl = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const int ex = incl - a - b;
+    if (i0 < P.W) ioff[i0] = ex;
+    if (i1 < P.W) ioff[i1] = ex + a;
+    if (lane == 31) ioff[P.W] = incl;   // the total
+    if (tile == 0) {
+      if (user_off) {
+        if (i0 < P.W) user_off[i0] = ex;
+        if (i1 < P.W) user_off[i1] = ex + a;
+        if (lane == 31) user_off[P.W] = incl;
       }
-      if (i < P.W) run += icount[i];
+      if (i0 < P.W) plan->inst_count[i0] = a;
+      if (i1 < P.W) plan->inst_count[i1] = b;
     }
   }
   // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count

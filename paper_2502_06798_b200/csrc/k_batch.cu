@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
 #define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers, no spills
 #endif
 
-template <bool DISP>   // DISP: the f3 stateful dispatcher picks (a separate instantiation keeps R13 lean)
+// DISP: the f3 stateful dispatcher picks (a separate instantiation keeps R13 lean).  MODE (the stateless
+// path; compile-time so the per-row loop carries no mode branches or parameter reloads): 0 greedy with
+// b* a power of two, 1 greedy with any b*, 2 uniform.  The DISP instantiation reads P.mode.
+template <bool DISP, int MODE>
 __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
@@ -118,10 +121,11 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * TILE + w * 32 * ROWS;
+  const bool uniform = DISP ? P.mode == PAS_UNIFORM : MODE == 2;
   int c[ROWS];
   load_rows(cls, base, P.N, c);
   for (int i = threadIdx.x; i < WARPS * NCLS; i += THREADS) (&wcnt[0][0])[i] = 0;
-  if (P.mode != PAS_UNIFORM) {   // the instance lists of the K' levels, staged once per block
+  if (!uniform) {   // the instance lists of the K' levels, staged once per block
     if (threadIdx.x < nC) {
       magic_s[threadIdx.x] = plan->n_inst_magic[threadIdx.x];
       ninst_s[threadIdx.x] = plan->n_inst[threadIdx.x];
@@ -136,14 +140,14 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   if (threadIdx.x < P.W) {
     // class totals (from the scanned counts) -> this instance's count (closed form, R13 / R14)
     const int i = threadIdx.x;
-    const int cc = P.mode == PAS_UNIFORM ? i : P.inst_level[i];
+    const int cc = uniform ? i : P.inst_level[i];
     const int64_t start = scanned[(int64_t)cc * ntiles];
     const int64_t end = cc + 1 < nC ? scanned[(int64_t)(cc + 1) * ntiles] : P.N;
     const int total = (int)(end - start);
     int cnt = total;
     if (DISP) {
       cnt = P.dplan->cnt[i];   // f3: counted by k_disp_prep from the same class totals
-    } else if (P.mode != PAS_UNIFORM) {
+    } else if (!uniform) {
       int m = 0, nj = 0;   // position of i among the instances of its level, their number
       for (int q = 0; q < P.W; ++q) {
         m += (P.inst_level[q] == cc && q < i) ? 1 : 0;
@@ -195,8 +199,8 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
     c[j] = (r << 8) | (c[j] & 0xFF);
   }
   __syncthreads();
-  if (threadIdx.x < nC) {   // exclusive prefix over warps, per class
-    int run = 0;
+  if (threadIdx.x < nC) {   // per class: the tile's offset plus the exclusive prefix over warps
+    int run = tile_off[threadIdx.x];
     for (int v2 = 0; v2 < WARPS; ++v2) {
       const int x = wcnt[v2][threadIdx.x];
       wcnt[v2][threadIdx.x] = run;
@@ -204,16 +208,19 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
     }
   }
   __syncthreads();
+  // per-warp output bases: the unrolled rows below address them with immediate offsets
+  int32_t* const inst_w = instance + base + lane;
+  int32_t* const slot_w = slot + base + lane;
+  const int32_t p_w = (int32_t)(base + lane);   // prompt ids fit int32 (N <= max_batch < 2^31)
 #pragma unroll
   for (int j = 0; j < ROWS; ++j) {
-    const int64_t p = base + 32 * j + lane;
     const int cj = c[j] & 0xFF, rj = c[j] >> 8;
     if (cj == 0xFF) continue;
-    const int t = tile_off[cj] + wcnt[w][cj] + rj;
+    const int t = wcnt[w][cj] + rj;
     int inst, sl, pos;
     if (DISP) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
       int64_t sl64;
-      if (P.mode == PAS_UNIFORM) {
+      if (uniform) {
         inst = cj;
         sl64 = P.dplan->Q0[inst] + t;
       } else {
@@ -221,22 +228,22 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
       }
       sl = (int)sl64;
       pos = (int)(sl64 - P.dplan->Q0[inst]);
-    } else if (P.mode == PAS_UNIFORM) {
+    } else if (uniform) {
       inst = cj;
       sl = t;
     } else {
       // q1 = t div b*, q2 = q1 div n_j (exact multiply-high, t < 2^26, n_j <= 64):
       // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
       const uint32_t b = (uint32_t)P.bstar;
-      const uint32_t q1 = P.bstar_shift >= 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
+      const uint32_t q1 = MODE == 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
       const uint32_t q2 = (uint32_t)(((uint64_t)q1 * magic_s[cj]) >> 32);
       inst = ilist_s[cj][q1 - q2 * (uint32_t)ninst_s[cj]];
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
     if (!DISP) pos = sl;
-    instance[p] = inst;
-    slot[p] = sl;
-    if (prompts) prompts[ioff[inst] + pos] = (int32_t)p;   // the batch lists (counting-sort scatter)
+    inst_w[32 * j] = inst;
+    slot_w[32 * j] = sl;
+    if (prompts) prompts[ioff[inst] + pos] = p_w + 32 * j;   // the batch lists (counting-sort scatter)
   }
 }
 
@@ -267,8 +274,11 @@ cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, De
     if (e != cudaSuccess) return e;
     *launches += 1;
   }
-  launch_pdl(p.disp ? k_cls_rank<true> : k_cls_rank<false>, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses,
-             w.blk_off, plan, instance, slot, bucket_prompts, bucket_offsets);
+  auto kern = p.disp ? k_cls_rank<true, 0>
+              : p.mode == PAS_UNIFORM ? k_cls_rank<false, 2>
+              : p.bstar_shift >= 0 ? k_cls_rank<false, 0> : k_cls_rank<false, 1>;
+  launch_pdl(kern, ntiles, THREADS, 0, st, r.cls7, p, ntiles, nclasses, w.blk_off, plan, instance, slot, bucket_prompts,
+             bucket_offsets);
   *launches += 2;
   return cudaGetLastError();
 }

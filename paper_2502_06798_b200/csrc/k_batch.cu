@@ -98,6 +98,9 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
   }
 }
 
+#ifndef PAS_K7_BALLOT
+#define PAS_K7_BALLOT 0   // 1: in-row ranking by class-bit ballots (<= 32 classes; measured slower: 297 vs 261 us)
+#endif
 #ifndef PAS_K7_MINB
 #define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers, no spills
 #endif
@@ -188,15 +191,41 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   // the rank is packed above the class byte (c[j] = rank << 8 | class, class 0xFF past the end): one
   // register per row instead of two
   const unsigned lt = (1u << lane) - 1;
+  if (PAS_K7_BALLOT && nC <= 32) {
+    // multisplit by class bits: nb ballots per row give every lane the mask of its own class's lanes
+    // and the mask of the lanes of class `lane`; lane L keeps the warp's running count of class L in a
+    // register (no shared memory, no per-row warp syncs)
+    int nb = 0;
+    while ((1 << nb) < nC) ++nb;
+    int run = 0;
 #pragma unroll
-  for (int j = 0; j < ROWS; ++j) {
-    const unsigned m = __match_any_sync(0xffffffffu, c[j]);
-    const bool lead = lane == __ffs(m) - 1;
-    const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
-    __syncwarp();
-    if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
-    __syncwarp();
-    c[j] = (r << 8) | (c[j] & 0xFF);
+    for (int j = 0; j < ROWS; ++j) {
+      const int cj = c[j];
+      unsigned own = __ballot_sync(0xffffffffu, cj >= 0), mine = own;
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        if (b >= nb) break;
+        const unsigned bb = __ballot_sync(0xffffffffu, (cj >> b) & 1);
+        own &= ((cj >> b) & 1) ? bb : ~bb;
+        mine &= ((lane >> b) & 1) ? bb : ~bb;
+      }
+      const int before = __shfl_sync(0xffffffffu, run, cj & 31);
+      run += __popc(mine);
+      const int r = cj >= 0 ? before + __popc(own & lt) : 0;
+      c[j] = (r << 8) | (cj & 0xFF);
+    }
+    if (lane < nC) wcnt[w][lane] = run;
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS; ++j) {
+      const unsigned m = __match_any_sync(0xffffffffu, c[j]);
+      const bool lead = lane == __ffs(m) - 1;
+      const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
+      __syncwarp();
+      if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
+      __syncwarp();
+      c[j] = (r << 8) | (c[j] & 0xFF);
+    }
   }
   __syncthreads();
   if (threadIdx.x < nC) {   // per class: the tile's offset plus the exclusive prefix over warps

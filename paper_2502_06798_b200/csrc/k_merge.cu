@@ -275,6 +275,10 @@ __global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __r
 // pair of candidates 2e, 2e+1 (one 16-byte load, two 8-byte stores, all coalesced); the thread that
 // owns a prompt's first pair also does K4 for it.  Requires even k.
 constexpr int S1_THREADS = 256;
+#ifndef PAS_S1_UNROLL
+#define PAS_S1_UNROLL 1   // 16-byte loads in flight per thread per step (2 and 4 measured equal, 8 slower)
+#endif
+constexpr int S1_UNROLL = PAS_S1_UNROLL;
 template <int HALF>
 __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict__ in,
                                                           const uint8_t* __restrict__ pflags, const RouteParams P,
@@ -285,21 +289,37 @@ __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict
   constexpr uint32_t half = HALF;
   const bool cold = (P.M_total == 0);
   const uint32_t total = (uint32_t)P.N * half;                    // <= 2^30
-  // persistent grid-stride loop: one smem histogram flush per CTA (global atomics stay O(grid))
-  for (uint32_t e = blockIdx.x * S1_THREADS + threadIdx.x; e < total; e += gridDim.x * S1_THREADS) {
-    const uint32_t p = e / half;
-    const int4 v = __ldg(in + e);
-    Cand c0{__int_as_float(v.x), v.y}, c1{__int_as_float(v.z), v.w};
-    const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
-    if (invalid || cold) {
-      c0 = Cand{-INFINITY, -1};
-      c1 = c0;
+  const uint32_t stride = gridDim.x * S1_THREADS;
+  // persistent grid-stride loop: one smem histogram flush per CTA (global atomics stay O(grid)).
+  // S1_UNROLL independent 16-byte loads are issued before any is consumed (memory-level parallelism).
+  for (uint32_t e0 = blockIdx.x * S1_THREADS + threadIdx.x; e0 < total; e0 += S1_UNROLL * stride) {
+    int4 v[S1_UNROLL];
+    uint8_t fl[S1_UNROLL];
+#pragma unroll
+    for (int u = 0; u < S1_UNROLL; ++u) {
+      const uint32_t e = e0 + u * stride;
+      if (e < total) {
+        v[u] = __ldg(in + e);
+        fl[u] = pflags ? __ldg(pflags + e / half) : 0;
+      }
     }
-    if (o.topk_id) reinterpret_cast<int2*>(o.topk_id)[e] = make_int2(c0.g, c1.g);
-    if (o.topk_score) reinterpret_cast<float2*>(o.topk_score)[e] = make_float2(c0.s, c1.s);
-    if (o.cand_out) reinterpret_cast<int4*>(o.cand_out)[e] = make_int4(__float_as_int(c0.s), c0.g,
-                                                                       __float_as_int(c1.s), c1.g);
-    if (e == p * half) select_one(c0.s, c1.s, c0.g, p, invalid, cold, P, o, ty);
+#pragma unroll
+    for (int u = 0; u < S1_UNROLL; ++u) {
+      const uint32_t e = e0 + u * stride;
+      if (e >= total) break;
+      const uint32_t p = e / half;
+      Cand c0{__int_as_float(v[u].x), v[u].y}, c1{__int_as_float(v[u].z), v[u].w};
+      const bool invalid = (fl[u] & PAS_FLAG_INVALID) != 0;
+      if (invalid || cold) {
+        c0 = Cand{-INFINITY, -1};
+        c1 = c0;
+      }
+      if (o.topk_id) reinterpret_cast<int2*>(o.topk_id)[e] = make_int2(c0.g, c1.g);
+      if (o.topk_score) reinterpret_cast<float2*>(o.topk_score)[e] = make_float2(c0.s, c1.s);
+      if (o.cand_out) reinterpret_cast<int4*>(o.cand_out)[e] = make_int4(__float_as_int(c0.s), c0.g,
+                                                                         __float_as_int(c1.s), c1.g);
+      if (e == p * half) select_one(c0.s, c1.s, c0.g, p, invalid, cold, P, o, ty);
+    }
   }
   flush_tally(P, o, ty);
 }
@@ -325,7 +345,13 @@ cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, co
   if (S == 1 && (p.topk & 1) == 0) {
     const int64_t threads = p.N * (p.topk >> 1);
     int64_t blocks = (threads + S1_THREADS - 1) / S1_THREADS;
-    if (blocks > (int64_t)kNumSMs * 8) blocks = (int64_t)kNumSMs * 8;   // one resident wave
+    static const int per_sm = [] {   // resident CTAs per SM at this kernel's register count
+      int n = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_select_s1<4>, S1_THREADS, 0) != cudaSuccess || n < 1)
+        n = 4;
+      return n;
+    }();
+    if (blocks > (int64_t)kNumSMs * per_sm) blocks = (int64_t)kNumSMs * per_sm;   // one resident wave
     const unsigned g = (unsigned)blocks;
     const int4* in4 = reinterpret_cast<const int4*>(in);
     switch (p.topk >> 1) {

@@ -347,7 +347,8 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, 
  * R (cache ranges per prompt tile = sources of the merge), T (cache tiles per chunk; 0 = static
  * schedule), CS (chunk steps per range), MTg (prompt tiles per group), pair (1 = CTA-pair tile),
  * MT (prompt tiles of 128), NT (cache tiles of 256), cand_cap (candidate rows: R * N <= cand_cap).
- * Errors: PAS_ERR_ARG. */
+ * The PAS_K2_* experiment variables are read at each call here; a context reads them
+ * once, at pas_create.  Errors: PAS_ERR_ARG. */
 pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_batch, int* out);
 
 #ifdef __cplusplus

@@ -39,6 +39,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <algorithm>
 
 #include "pas_internal.cuh"
@@ -877,23 +878,36 @@ cudaError_t simtopk_init() {
 #ifndef PAS_K2_DYN_MIN_STEPS
 #define PAS_K2_DYN_MIN_STEPS 8    // fewer chunk steps: short ranges, the static schedule is faster (C2)
 #endif
-static int env_int(const char* name, int dflt) {   // A/B experiments only
+static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
 }
-bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R_out,
-                          int* T_out, int* CS_out, int* MTg_out) {
-  const int budget_mb = env_int("PAS_K2_DYN_MB", PAS_K2_DYN_MB);
+K2Tuning K2Tuning::from_env() {
+  K2Tuning t;
+  const char* sched = getenv("PAS_K2_SCHED");
+  t.force_static = sched && !strcmp(sched, "static");
+  t.ranges = env_int("PAS_K2_RANGES", 0);
+  t.no_leash = getenv("PAS_K2_NOLEASH") != nullptr;
+  t.dyn_mb = env_int("PAS_K2_DYN_MB", PAS_K2_DYN_MB);
+  t.dyn_tmax = env_int("PAS_K2_DYN_TMAX", PAS_K2_DYN_TMAX);
+  t.dyn_min_pairs = env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS);
+  t.dyn_min_steps = env_int("PAS_K2_DYN_MIN_STEPS", PAS_K2_DYN_MIN_STEPS);
+  t.dyn_amb = env_int("PAS_K2_DYN_AMB", PAS_K2_DYN_AMB);
+  return t;
+}
+bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d,
+                          const K2Tuning& tune, int* R_out, int* T_out, int* CS_out, int* MTg_out) {
+  const int budget_mb = tune.dyn_mb;
   if (budget_mb <= 0 || simtopk_uses_tmem_a(d) || simtopk_pair(N, d)) return false;
   const int64_t MT = (N + BM - 1) / BM;
   const int64_t NT = (M_local + BN - 1) / BN;
   if (MT <= 0 || NT <= 0) return false;
-  const int64_t want = (int64_t)env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS) * Tile<false>::NUM_WORKERS;
+  const int64_t want = (int64_t)tune.dyn_min_pairs * Tile<false>::NUM_WORKERS;
   // prompt-tile groups: every chunk step of a group re-reads all of its prompt tiles (A, kept in L2
   // with evict_last), so a group's A must leave L2 room for the chunks; each group streams the cache
   // once.  Never split below `want` (range, prompt tile) pairs per group.
   const int64_t a_bytes = (int64_t)MT * BM * d * 2;
-  const int64_t a_budget = (int64_t)std::max(env_int("PAS_K2_DYN_AMB", PAS_K2_DYN_AMB), 1) << 20;
+  const int64_t a_budget = (int64_t)std::max(tune.dyn_amb, 1) << 20;
   int64_t groups = std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, MT), MTg, R;
   for (;; --groups) {   // fewer groups (more ranges per group) until the candidate buffers hold R ranges
     MTg = (MT + groups - 1) / groups;
@@ -907,10 +921,10 @@ bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t
   const int64_t tile_bytes = (int64_t)BN * d * 2;
   int64_t T = ((int64_t)budget_mb << 20) / (in_flight * tile_bytes);
   if (T < 4) T = 4;
-  const int tmax = env_int("PAS_K2_DYN_TMAX", PAS_K2_DYN_TMAX);
+  const int tmax = tune.dyn_tmax;
   if (T > tmax) T = tmax;
   const int64_t L = (NT + R - 1) / R;             // tiles of the longest range
-  if (L < env_int("PAS_K2_DYN_MIN_STEPS", PAS_K2_DYN_MIN_STEPS) * T) return false;   // too short to chunk
+  if (L < tune.dyn_min_steps * T) return false;   // too short to chunk
   *R_out = (int)R;
   *T_out = (int)T;
   *CS_out = (int)((L + T - 1) / T);

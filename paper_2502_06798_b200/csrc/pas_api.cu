@@ -107,6 +107,7 @@ struct pas_ctx {
   uint32_t* k2_sched = nullptr;
   int64_t k2_state_tiles = 0;
   int k2_last_R = 0, k2_last_T = 0, k2_last_CS = 0;   // schedule of the last K2 launch (pas_plan_stats)
+  K2Tuning k2_tune;                                    // experiment knobs, read at pas_create
   // f1 forecast-driven mode (0 = exact per-batch plan)
   int fc_window = 0, fc_replan_every = 1;
   int64_t fc_tick = 0;
@@ -274,18 +275,14 @@ int64_t k2_state_tiles(int64_t cand_cap) { return cand_cap / simtopk_box_q() + 8
 
 // The K2 schedule of one batch: the dynamic schedule when simtopk_plan_dynamic takes it (dyn.T > 0),
 // else the static ranges.  Returns R (the S of the merge).  Host only.
-int k2_schedule(int64_t N, int64_t M_local, int d, int64_t cand_cap, DynSched* dyn) {
+int k2_schedule(int64_t N, int64_t M_local, int d, int64_t cand_cap, const K2Tuning& tune, DynSched* dyn) {
   int R = 1;
-  const char* sched = getenv("PAS_K2_SCHED");    // "static": A/B experiments only
-  if (!(sched && !strcmp(sched, "static")) &&
-      simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, &R, &dyn->T, &dyn->CS, &dyn->MTg))
+  if (!tune.force_static &&
+      simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, tune, &R, &dyn->T, &dyn->CS, &dyn->MTg))
     return R;
   dyn->T = dyn->CS = dyn->MTg = 0;
   R = simtopk_choose_ranges(N, M_local, cand_cap, d);
-  if (const char* ov = getenv("PAS_K2_RANGES")) {   // tuning experiments only
-    const int r = atoi(ov);
-    if (r >= 1 && (int64_t)r * N <= cand_cap) R = r;
-  }
+  if (tune.ranges >= 1 && (int64_t)tune.ranges * N <= cand_cap) R = tune.ranges;
   return R;
 }
 
@@ -329,7 +326,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   int R = 1;
   if (ctx->M_local > 0) {
     DynSched dyn;
-    R = k2_schedule(N, ctx->M_local, ctx->cfg.d, ctx->cand_cap, &dyn);
+    R = k2_schedule(N, ctx->M_local, ctx->cfg.d, ctx->cand_cap, ctx->k2_tune, &dyn);
     if (dyn.T > 0) {
       dyn.st_s = ctx->k2_st_s;
       dyn.st_g = ctx->k2_st_g;
@@ -338,7 +335,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
     }
     if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
-                  ctx->qhat, ctx->cand_local, nullptr, getenv("PAS_K2_NOLEASH") ? nullptr : ctx->k2_progress,
+                  ctx->qhat, ctx->cand_local, nullptr, ctx->k2_tune.no_leash ? nullptr : ctx->k2_progress,
                   ctx->k2_epoch, dyn};
     CUDA_TRY(ctx, launch_simtopk(a, st));
     ctx->k2_last_R = R;
@@ -501,6 +498,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   ctx->cap_rows = cfg->max_rows_per_rank;
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
   ctx->cand_cap = k2_cand_cap(mb);
+  ctx->k2_tune = K2Tuning::from_env();
   const int64_t nb = (int64_t)kMaxLevels << redirect_kb(mb);
   const int64_t ncls = 64 * (int64_t)batch_tiles(mb);
   cudaError_t e = cudaSuccess;
@@ -1183,7 +1181,7 @@ pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_
   if (!out || N < 0 || M_local < 0 || d <= 0 || max_batch < N) return PAS_ERR_ARG;
   DynSched dyn;
   const int64_t cap = k2_cand_cap(max_batch);
-  out[0] = k2_schedule(N, M_local, d, cap, &dyn);
+  out[0] = k2_schedule(N, M_local, d, cap, K2Tuning::from_env(), &dyn);
   out[1] = dyn.T;
   out[2] = dyn.CS;
   out[3] = dyn.MTg;

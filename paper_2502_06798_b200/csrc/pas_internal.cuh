@@ -146,6 +146,20 @@ struct DynSched {
   uint32_t* sched = nullptr;    // [2] unit counter, workers finished (zero between launches)
 };
 
+// K2 schedule knobs for A/B experiments.  Read from the environment once per context at
+// pas_create (K2Tuning::from_env), never on the routing path; defaults are the measured choices.
+struct K2Tuning {
+  bool force_static = false;   // PAS_K2_SCHED=static: the static ranges even where the dynamic schedule applies
+  int ranges = 0;              // PAS_K2_RANGES: static-schedule ranges (0: chosen by the cost model)
+  bool no_leash = false;       // PAS_K2_NOLEASH: static schedule without the progress leash
+  int dyn_mb = 0;              // PAS_K2_DYN_MB: L2 budget (MB) for the chunks in flight
+  int dyn_tmax = 0;            // PAS_K2_DYN_TMAX: longest chunk (tiles)
+  int dyn_min_pairs = 0;       // PAS_K2_DYN_MIN_PAIRS: (range, prompt tile) pairs per group, in units of 148
+  int dyn_min_steps = 0;       // PAS_K2_DYN_MIN_STEPS: fewest chunk steps for the dynamic schedule
+  int dyn_amb = 0;             // PAS_K2_DYN_AMB: L2 budget (MB) for one group's prompt tiles
+  static K2Tuning from_env();
+};
+
 // K2: similarity GEMM (tcgen05) + fused running top-k over cache ranges.
 struct SimTopkArgs {
   const CUtensorMap* tmap_q;      // [rows_q x d] bf16, box 64 x simtopk_box_q(), SW128
@@ -165,8 +179,8 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 // The dynamic schedule's ranges R and chunk T for this batch, or false when the static schedule
 // serves it (CTA-pair tile, too few units, or more parked lists than `state_tiles` prompt tiles).
-bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d, int* R,
-                          int* T, int* CS, int* MTg);
+bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d,
+                          const K2Tuning& tune, int* R, int* T, int* CS, int* MTg);
 bool simtopk_uses_tmem_a(int d);
 bool simtopk_pair(int64_t N, int d);   // the CTA-pair tile serves this batch size
 cudaError_t simtopk_init();

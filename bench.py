@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--cpu-sample-prompts", type=int, default=32)
     ap.add_argument("--dispatcher", action="store_true",
                     help="route-and-batch through the f3 stateful dispatcher (queues carried across steps)")
+    ap.add_argument("--forecast", type=int, default=0, metavar="W",
+                    help="the f1 forecast-driven mode: an Optimal-K Predictor window of W prompts, the plan "
+                         "rebuilt every batch, i.i.d. Philox K' (0: the exact per-batch plan)")
     ap.add_argument("--force-collective", action="store_true",
                     help="use the NCCL all-gather path even with one rank (transport self-test)")
     return ap.parse_args()
@@ -207,6 +210,8 @@ def main():
     router.set_bands(cfg.grid, cfg.thresholds)
     router.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
     gap_us = 0
+    if args.forecast:
+        router.set_forecast(args.forecast, 1)
     if args.dispatcher:
         # SPEC S:75 service model per instance at b*: (T - K) x 100 ms x (1 + 0.3 (b* - 1)); batches
         # arrive at 90 % of the instances' capacity, so queues stay short but non-empty
@@ -325,6 +330,7 @@ def main():
                    "G": G, "M_per_gpu": M_local, "d": cfg.d, "topk": cfg.topk, "levels": len(cfg.grid),
                    "instances": len(cfg.instance_level), "mode": "uniform" if cfg.mode else "greedy",
                    "bstar": cfg.bstar, "dispatcher": "stateful (f3)" if args.dispatcher else "stateless (R13)",
+                   "plan": f"forecast (f1, window {args.forecast})" if args.forecast else "exact per batch",
                    "parallelism": f"cache row-sharded x{G}" + (" + NCCL all-gather" if G > 1 else ""),
                    "l2": l2_note},
         "roofline": {"kernel": "k_simtopk (K2: tcgen05 similarity GEMM + fused top-k)", "bound": "tensor",

@@ -302,7 +302,9 @@ pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
  * prompts on every rank.
  * out: device arrays, written in full on every rank.  N == 0 is a no-op; N > max_batch ->
  * PAS_ERR_CAPACITY.  Requires bands and fractions (PAS_ERR_STATE).  Enqueue-only (no host sync);
- * batch_seq increments on success.  world > 1 needs the NCCL communicator. */
+ * batch_seq increments on success.  world > 1 needs the NCCL communicator.  One batch in flight per
+ * context (its workspace is reused), and not capturable into a CUDA graph for replay: each call passes
+ * per-call host state to its kernels (batch_seq for the Philox counters, the K2 schedule's epoch tag). */
 pas_status pas_route_batch(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
                            const pas_route_out* out, pas_stream stream);
 

@@ -275,13 +275,18 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
 
-template <int KMAX, bool DUMP, bool PAIR, bool DYN>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN, bool MC = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack,
               const DynSched dyn) {
   static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
+  // MC: clusters of two single-CTA tiles on the dynamic schedule, streaming the same cache chunk for
+  // prompt tiles 2 mp and 2 mp + 1; each CTA TMA-loads half of every B k-block and multicasts it to
+  // both, so a cache tile crosses L2 -> SMEM once per pair instead of once per CTA.  Units hold
+  // prompt-tile PAIRS (MTp of them); the leader takes them from the counter and hands them to the peer.
+  static_assert(!MC || DYN, "B multicast is built on the dynamic schedule");
   using TL = Tile<PAIR>;
   constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
                 B_BYTES = TL::B_BYTES, STAGE_BYTES = TL::STAGE_BYTES, UNIT_ROWS = TL::UNIT_ROWS;
@@ -295,22 +300,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0;
+  const uint32_t crank = (PAIR || MC) ? ptx::cluster_ctarank() : 0;
   const bool leader = crank == 0;
-  const int worker = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int nworkers = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int units = DYN ? dyn.CS * MT * R : MT * R;
+  const int worker = (PAIR || MC) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nworkers = (PAIR || MC) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int MTu = MC ? (MT + 1) / 2 : MT;   // schedule rows: prompt tiles (or pairs of them under MC)
+  const int units = DYN ? dyn.CS * MTu * R : MT * R;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmQ);
     ptx::prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&bars->full[s], 1);
-      ptx::mbar_init(&bars->empty[s], 1);
+      ptx::mbar_init(&bars->empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs read the stage's B halves
     }
     for (int s = 0; s < UNIT_RING; ++s) {
       ptx::mbar_init(&bars->ufull[s], 1);
-      ptx::mbar_init(&bars->uempty[s], 1 + EPI_WARPS);
+      // MC: the leader's slot is released by both CTAs' MMA issuer + epilogue warps and the peer's producer
+      ptx::mbar_init(&bars->uempty[s], MC ? 2 * (1 + EPI_WARPS) + 1 : 1 + EPI_WARPS);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&bars->tfull[a], 1);
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   ptx::tc_fence_before();
-  if (PAIR) ptx::cluster_sync(); else __syncthreads();
+  if (PAIR || MC) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
   pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
@@ -344,28 +351,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int stage = 0, us = 0;
         uint32_t phase = 0, uph = 0;
         for (;;) {
-          const int u = (int)atomicAdd(dyn.sched, 1u);
-          ptx::mbar_wait(&bars->uempty[us], uph ^ 1);
-          bars->unit[us] = u < units ? u : -1;
-          ptx::mbar_arrive(&bars->ufull[us]);
+          int u;
+          if (!MC || leader) {
+            u = (int)atomicAdd(dyn.sched, 1u);
+            if (u >= units) u = -1;
+            ptx::mbar_wait(&bars->uempty[us], uph ^ 1);
+            bars->unit[us] = u;
+            if (MC) {   // the peer's ring slot (released with ours: its consumers arrive on our uempty)
+              ptx::st_cluster_u32(&bars->unit[us], 1, (uint32_t)u);
+              ptx::mbar_arrive_cluster(&bars->ufull[us], 1);
+            }
+            ptx::mbar_arrive(&bars->ufull[us]);
+          } else {
+            ptx::mbar_wait_cluster(&bars->ufull[us], uph);
+            u = bars->unit[us];
+            ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
+          }
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
-          if (u >= units) break;
+          if (u < 0) break;
           int c, j, ta, tb;
-          dyn_decode(u, MT, R, NT, dyn, c, j, ta, tb);
-          const int qrow = (j % MT) * BM;
+          dyn_decode(u, MTu, R, NT, dyn, c, j, ta, tb);
+          const int qrow = (MC ? 2 * (j % MTu) + (int)crank : j % MT) * BM;
           for (int t = ta; t < tb; ++t) {
             for (int kb = 0; kb < kblocks; ++kb) {
               ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
               ptx::mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
               ptx::tma_load_2d(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
-              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN, ptx::kEvictNormal);
+              if (MC)   // this CTA's half of the cache tile, into both CTAs (tmC: 128-row boxes)
+                ptx::tma_load_2d_mcast(&tmC, sB + stage * B_BYTES + crank * (B_BYTES / 2), &bars->full[stage],
+                                       kb * BK, t * BN + (int)crank * (BN / 2), 0x3, ptx::kEvictNormal);
+              else
+                ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN,
+                                 ptx::kEvictNormal);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
           }
         }
         // every worker has taken its last unit once all have arrived here: the last one out re-arms
         // the counter for the next launch (kernel boundaries order this against the next K2)
-        if (atomicAdd(dyn.sched + 1, 1u) == (uint32_t)nworkers - 1) {
+        if ((!MC || leader) && atomicAdd(dyn.sched + 1, 1u) == (uint32_t)nworkers - 1) {
           dyn.sched[0] = 0;
           dyn.sched[1] = 0;
         }
@@ -408,7 +432,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer ---------------------------------
-    if (leader && ptx::elect_one()) {
+    // (CTA pair: the leader issues for both CTAs; every other tile, incl. each CTA of an MC pair, its own)
+    if ((!PAIR || leader) && ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(UNIT_ROWS, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -419,13 +444,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = worker; DYN || u < units; u += nworkers) {
         int t0, t1;
         if (DYN) {
-          ptx::mbar_wait(&bars->ufull[us], uph);
+          if (MC) ptx::mbar_wait_cluster(&bars->ufull[us], uph);
+          else ptx::mbar_wait(&bars->ufull[us], uph);
           u = bars->unit[us];
-          ptx::mbar_arrive(&bars->uempty[us]);
+          if (MC) ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
+          else ptx::mbar_arrive(&bars->uempty[us]);
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
           if (u < 0) break;
           int c, j;
-          dyn_decode(u, MT, R, NT, dyn, c, j, t0, t1);
+          dyn_decode(u, MTu, R, NT, dyn, c, j, t0, t1);
         } else {
           const int r = u / MT;
           t0 = (int)((int64_t)r * NT / R);
@@ -448,6 +475,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               else ptx::umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
             }
             if (PAIR) ptx::umma_commit_pair(&bars->empty[stage], 0x3);
+            else if (MC) ptx::umma_commit_mcast(&bars->empty[stage], 0x3);   // frees the stage in both CTAs
             else ptx::umma_commit(&bars->empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -472,22 +500,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int u = worker; DYN || u < units; u += nworkers) {
       int m, r, t0, t1, c = 0, j = 0;
       if (DYN) {
-        ptx::mbar_wait(&bars->ufull[us], uph);
+        if (MC) ptx::mbar_wait_cluster(&bars->ufull[us], uph);
+        else ptx::mbar_wait(&bars->ufull[us], uph);
         u = bars->unit[us];
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars->uempty[us]);
+        if (lane == 0) {
+          if (MC) ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
+          else ptx::mbar_arrive(&bars->uempty[us]);
+        }
         if (++us == UNIT_RING) { us = 0; uph ^= 1; }
         if (u < 0) break;
-        dyn_decode(u, MT, R, NT, dyn, c, j, t0, t1);
-        m = j % MT;
-        r = j / MT;
+        dyn_decode(u, MTu, R, NT, dyn, c, j, t0, t1);
+        if (MC) {   // j = r MTp + mp -> this CTA's prompt tile 2 mp + crank, its parked-list slot 2 j + crank
+          m = 2 * (j % MTu) + (int)crank;
+          r = j / MTu;
+          j = 2 * j + (int)crank;
+        } else {
+          m = j % MT;
+          r = j / MT;
+        }
       } else {
         m = u % MT;
         r = u / MT;
         t0 = (int)((int64_t)r * NT / R);
         t1 = (int)((int64_t)(r + 1) * NT / R);
       }
-      const int64_t prompt = (int64_t)m * UNIT_ROWS + crank * BM + row;
+      const int64_t prompt = (int64_t)m * UNIT_ROWS + (PAIR ? crank * BM : 0) + row;
       float s[KMAX];
       int32_t gl[KMAX];
 #pragma unroll
@@ -572,8 +610,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  if (PAIR) ptx::cluster_sync(); else __syncthreads();
-  if (warp == 1) {
+  if (PAIR || MC) ptx::cluster_sync(); else __syncthreads();   // MC: no CTA leaves while the peer may
+  if (warp == 1) {                                               // still multicast into it or arrive on it
     ptx::tc_fence_after();
     if (PAIR) ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
     else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -795,10 +833,10 @@ cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream
   return cudaGetLastError();
 }
 
-template <int KMAX, bool DUMP, bool PAIR, bool DYN = false>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN = false, bool MC = false>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
   using TL = Tile<PAIR>;
-  constexpr int CTAS = TL::CTAS;
+  constexpr int CTAS = (PAIR || MC) ? 2 : 1;   // cluster size
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -812,9 +850,10 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = PAIR ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN>, *a.tmap_q, PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N,
-                            a.M_local, a.d / BK, a.k, a.G,
+  cfg.numAttrs = (PAIR || MC) ? 2 : 1;
+  // the CTA pair and the B multicast read the cache through the 128-row box map
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN, MC>, *a.tmap_q,
+                            (PAIR || MC) ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
                             a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack, a.dyn);
 }
 
@@ -848,6 +887,8 @@ cudaError_t simtopk_init() {
   if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
   return cudaFuncSetAttribute(k_simtopk<16, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
@@ -872,6 +913,9 @@ cudaError_t simtopk_init() {
 #ifndef PAS_K2_DYN_TMAX
 #define PAS_K2_DYN_TMAX 128       // longest chunk (tiles)
 #endif
+#ifndef PAS_K2_MCAST
+#define PAS_K2_MCAST 0            // clusters of two sharing B by TMA multicast (dynamic schedule)
+#endif
 #ifndef PAS_K2_DYN_MIN_PAIRS
 #define PAS_K2_DYN_MIN_PAIRS 2
 #endif
@@ -893,6 +937,7 @@ K2Tuning K2Tuning::from_env() {
   t.dyn_min_pairs = env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS);
   t.dyn_min_steps = env_int("PAS_K2_DYN_MIN_STEPS", PAS_K2_DYN_MIN_STEPS);
   t.dyn_amb = env_int("PAS_K2_DYN_AMB", PAS_K2_DYN_AMB);
+  t.mcast = env_int("PAS_K2_MCAST", PAS_K2_MCAST) != 0;
   return t;
 }
 bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d,
@@ -902,22 +947,27 @@ bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t
   const int64_t MT = (N + BM - 1) / BM;
   const int64_t NT = (M_local + BN - 1) / BN;
   if (MT <= 0 || NT <= 0) return false;
-  const int64_t want = (int64_t)tune.dyn_min_pairs * Tile<false>::NUM_WORKERS;
+  // schedule rows: prompt tiles, or pairs of them under the B multicast (one unit per CTA pair)
+  const bool mc = tune.mcast;
+  const int64_t rows = mc ? (MT + 1) / 2 : MT;
+  const int64_t workers = mc ? Tile<false>::NUM_WORKERS / 2 : Tile<false>::NUM_WORKERS;
+  const int64_t want = (int64_t)tune.dyn_min_pairs * workers;
   // prompt-tile groups: every chunk step of a group re-reads all of its prompt tiles (A, kept in L2
   // with evict_last), so a group's A must leave L2 room for the chunks; each group streams the cache
-  // once.  Never split below `want` (range, prompt tile) pairs per group.
+  // once.  Never split below `want` (range, prompt tile) pairs per group.  (Not with the multicast.)
   const int64_t a_bytes = (int64_t)MT * BM * d * 2;
   const int64_t a_budget = (int64_t)std::max(tune.dyn_amb, 1) << 20;
-  int64_t groups = std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, MT), MTg, R;
+  int64_t groups = mc ? 1 : std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, rows), MTg, R;
+  const int64_t slots_per_range = mc ? 2 * rows : MT;   // parked-list slots
   for (;; --groups) {   // fewer groups (more ranges per group) until the candidate buffers hold R ranges
-    MTg = (MT + groups - 1) / groups;
+    MTg = (rows + groups - 1) / groups;
     R = std::min<int64_t>((want + MTg - 1) / MTg, 128);   // the S-way merge takes S <= 128 sources
-    if (groups == 1 || (R <= NT && R * N <= cand_rows && R * MT <= state_tiles)) break;
+    if (groups == 1 || (R <= NT && R * N <= cand_rows && R * slots_per_range <= state_tiles)) break;
   }
-  if (R > NT || R * N > cand_rows || R * MT > state_tiles) return false;
-  if (R * MTg < Tile<false>::NUM_WORKERS) return false;      // less than one unit per SM per chunk step
-  // chunks in flight: the ranges one window of 148 consecutive units spans, plus the next step's
-  const int64_t in_flight = (Tile<false>::NUM_WORKERS + MTg - 1) / MTg + 1;
+  if (R > NT || R * N > cand_rows || R * slots_per_range > state_tiles) return false;
+  if (R * MTg < workers) return false;      // less than one unit per worker per chunk step
+  // chunks in flight: the ranges one window of `workers` consecutive units spans, plus the next step's
+  const int64_t in_flight = (workers + MTg - 1) / MTg + 1;
   const int64_t tile_bytes = (int64_t)BN * d * 2;
   int64_t T = ((int64_t)budget_mb << 20) / (in_flight * tile_bytes);
   if (T < 4) T = 4;
@@ -997,6 +1047,10 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   }
   if (a.dyn.T > 0 && !pair && !a.dump) {
     const int g = NUM_WORKERS;   // every SM: units are handed out dynamically
+    if (a.dyn.mcast) {
+      if (a.k <= 8) return launch_variant<8, false, false, true, true>(a, MT, NT, g, 0, st);
+      return launch_variant<16, false, false, true, true>(a, MT, NT, g, 0, st);
+    }
     if (a.k <= 8) return launch_variant<8, false, false, true>(a, MT, NT, g, 0, st);
     return launch_variant<16, false, false, true>(a, MT, NT, g, 0, st);
   }

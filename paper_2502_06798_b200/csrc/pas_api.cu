@@ -278,9 +278,12 @@ int64_t k2_state_tiles(int64_t cand_cap) { return cand_cap / simtopk_box_q() + 8
 int k2_schedule(int64_t N, int64_t M_local, int d, int64_t cand_cap, const K2Tuning& tune, DynSched* dyn) {
   int R = 1;
   if (!tune.force_static &&
-      simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, tune, &R, &dyn->T, &dyn->CS, &dyn->MTg))
+      simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, tune, &R, &dyn->T, &dyn->CS, &dyn->MTg)) {
+    dyn->mcast = tune.mcast;
     return R;
+  }
   dyn->T = dyn->CS = dyn->MTg = 0;
+  dyn->mcast = false;
   R = simtopk_choose_ranges(N, M_local, cand_cap, d);
   if (tune.ranges >= 1 && (int64_t)tune.ranges * N <= cand_cap) R = tune.ranges;
   return R;

@@ -139,7 +139,9 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
 struct DynSched {
   int T = 0;                    // cache tiles per chunk
   int CS = 0;                   // chunk steps per range
-  int MTg = 0;                  // prompt tiles per group (each group streams the cache once)
+  int MTg = 0;                  // prompt tiles per group (each group streams the cache once); under
+                                // mcast: prompt-tile PAIRS per group
+  bool mcast = false;           // clusters of two CTAs sharing every B k-block by TMA multicast
   float* st_s = nullptr;        // [R*MT][2][KMAX][128] parked scores
   int32_t* st_g = nullptr;      // [R*MT][2][KMAX][128] parked local rows
   uint64_t* done = nullptr;     // [R*MT] epoch << 32 | chunks done
@@ -157,6 +159,7 @@ struct K2Tuning {
   int dyn_min_pairs = 0;       // PAS_K2_DYN_MIN_PAIRS: (range, prompt tile) pairs per group, in units of 148
   int dyn_min_steps = 0;       // PAS_K2_DYN_MIN_STEPS: fewest chunk steps for the dynamic schedule
   int dyn_amb = 0;             // PAS_K2_DYN_AMB: L2 budget (MB) for one group's prompt tiles
+  bool mcast = false;          // PAS_K2_MCAST: B multicast across CTA pairs on the dynamic schedule
   static K2Tuning from_env();
 };
 

@@ -179,6 +179,46 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
       "r"(cta)
       : "memory");
 }
+// Blocking wait with cluster-scope acquire: for barriers whose arrivals come from another CTA of the
+// cluster together with data that CTA wrote into this CTA's shared memory (st.shared::cluster).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+// 32-bit store to the same shared-memory offset in CTA `cta` of the cluster.
+__device__ __forceinline__ void st_cluster_u32(void* p, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(p)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
+// TMA load multicast to the CTAs in cta_mask: the box lands at the same smem offset in each and
+// completes (bytes) on the mbarrier at the same offset in each.
+__device__ __forceinline__ void tma_load_2d_mcast(const CUtensorMap* m, void* smem_dst, uint64_t* bar, int32_t c0,
+                                                  int32_t c1, uint16_t cta_mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask), "l"(cache_hint)
+      : "memory");
+}
+// cta_group::1 commit arriving on the mbarrier at this offset in every CTA of cta_mask.
+__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
 // TMA load by either CTA of a pair, completing on the LEADER's mbarrier (peer bit cleared).
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, void* smem_dst, uint64_t* bar, int32_t c0,

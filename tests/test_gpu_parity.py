@@ -521,17 +521,21 @@ def test_k2_dynamic_schedule_full_oracle_k16(pas, monkeypatch):
     print(rep.summary(), "R", st["k2_ranges"], "T", st["k2_chunk_tiles"], "CS", st["k2_chunk_steps"])
 
 
-@pytest.mark.parametrize("N,M,topk,amb", [(16384, 400_003, 8, None), (4097, 250_000, 3, None),
-                                          (16384, 400_003, 8, "8")])
-def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, monkeypatch):
+@pytest.mark.parametrize("N,M,topk,amb,mcast", [(16384, 400_003, 8, None, None), (4097, 250_000, 3, None, None),
+                                                (16384, 400_003, 8, "8", None), (16384, 400_003, 8, None, "1"),
+                                                (4097, 250_000, 16, None, "1")])
+def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, mcast, monkeypatch):
     """Every output of the dynamic schedule byte-identical to the static one (same MMA sums, exact
     top-k with the same tie rule, whatever the split into groups, ranges and chunks), over three
     batches so the epoch-tagged chunk counters and the re-armed unit counter are exercised across
-    launches.  amb = "8": an 8 MB prompt-tile budget splits the 128 prompt tiles into 3 groups."""
+    launches.  amb = "8": an 8 MB prompt-tile budget splits the 128 prompt tiles into 3 groups; mcast:
+    the B-multicast CTA pairs (k = 16 with 33 prompt tiles: the odd tile's peer computes padding rows)."""
     cfg = CONFIGS["C3"]
     monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "2")
     if amb:
         monkeypatch.setenv("PAS_K2_DYN_AMB", amb)
+    if mcast:   # clusters of two CTAs sharing every B k-block by TMA multicast (odd MT: 33 prompt tiles)
+        monkeypatch.setenv("PAS_K2_MCAST", mcast)
     w = Workload(cfg, device=DEV, M=M)
     C_ = w.cache_rows(0, M).contiguous()
     res = {}

@@ -558,3 +558,38 @@ def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, mcast, monkeyp
         for key in a:
             x, y = (a[key][:W + 1], b[key][:W + 1]) if key == "bucket_offsets" else (a[key], b[key])
             assert np.array_equal(x, y), key           # (only [0, W] of bucket_offsets is written)
+
+
+def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
+    """Random shapes with the dynamic schedule forced into small chunks (T = 4 .. 16, as few as one
+    chunk step, empty trailing chunks in the shorter ranges, odd prompt-tile counts for the multicast
+    pairs): every output byte-identical to the static schedule on the same inputs."""
+    rng = np.random.default_rng(2502)
+    cfg = CONFIGS["C2"]
+    for case in range(10):
+        N = int(rng.integers(513, 6000))
+        M = int(rng.integers(20_000, 160_000))
+        k = int(rng.choice([1, 2, 5, 8, 11, 16]))
+        w = Workload(cfg, device=DEV, M=M)
+        C_ = w.cache_rows(0, M).contiguous()
+        P = w.prompts(N, batch=case)
+        res = {}
+        for sched in ("static", "dynamic"):
+            monkeypatch.setenv("PAS_K2_SCHED", "static" if sched == "static" else "dynamic")
+            monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "1")
+            monkeypatch.setenv("PAS_K2_DYN_MB", str(int(rng.choice([1, 4, 16]))))
+            monkeypatch.setenv("PAS_K2_MCAST", str(case % 2))
+            r = _router(pas, cfg, N, M, topk=k)
+            r.load_cache(C_)
+            res[sched] = _host(r.route(P))
+            torch.cuda.synchronize()
+            st = r.stats()
+            r.close()
+        W = len(cfg.instance_level)
+        for key in res["static"]:
+            a, b = res["static"][key], res["dynamic"][key]
+            if key == "bucket_offsets":
+                a, b = a[:W + 1], b[:W + 1]
+            assert np.array_equal(a, b), (case, N, M, k, key, st["k2_chunk_tiles"], st["k2_chunk_steps"])
+    for v in ("PAS_K2_SCHED", "PAS_K2_DYN_MIN_STEPS", "PAS_K2_DYN_MB", "PAS_K2_MCAST"):
+        monkeypatch.delenv(v)

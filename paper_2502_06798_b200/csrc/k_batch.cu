@@ -118,8 +118,8 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
   __shared__ int32_t icount[kMaxInst], ioff[kMaxInst + 1];   // per-instance counts, batch-list offsets
-  __shared__ uint64_t magic_s[kMaxLevels];
-  __shared__ int32_t ninst_s[kMaxLevels];
+  // per K' level: {32-bit reciprocal of n_j (0 for n_j = 1), n_j} -- one 8-byte shared load per prompt
+  __shared__ uint2 cinfo_s[kMaxLevels];
   __shared__ int32_t ilist_s[kMaxLevels][kMaxInst];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tile = blockIdx.x;
@@ -130,8 +130,10 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   for (int i = threadIdx.x; i < WARPS * NCLS; i += THREADS) (&wcnt[0][0])[i] = 0;
   if (!uniform) {   // the instance lists of the K' levels, staged once per block
     if (threadIdx.x < nC) {
-      magic_s[threadIdx.x] = plan->n_inst_magic[threadIdx.x];
-      ninst_s[threadIdx.x] = plan->n_inst[threadIdx.x];
+      // q div n_j for q < 2^26 and n_j <= 64 as umulhi(q, ceil(2^32 / n_j)): exact since the
+      // reciprocal's error (< n_j) times q stays below 2^32 (n_j = 1: q itself)
+      const uint32_t nj = (uint32_t)plan->n_inst[threadIdx.x];
+      cinfo_s[threadIdx.x] = make_uint2(nj > 1 ? (uint32_t)((0x100000000ull + nj - 1) / nj) : 0u, nj);
     }
     for (int i = threadIdx.x; i < nC * kMaxInst; i += THREADS)
       ilist_s[i / kMaxInst][i % kMaxInst] = plan->inst_list[i / kMaxInst][i % kMaxInst];
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
         inst = cj;
         sl64 = P.dplan->Q0[inst] + t;
       } else {
-        disp_pick_greedy(P.dplan, ilist_s[cj], ninst_s[cj], cj, t, P.bstar, inst, sl64);
+        disp_pick_greedy(P.dplan, ilist_s[cj], (int)cinfo_s[cj].y, cj, t, P.bstar, inst, sl64);
       }
       sl = (int)sl64;
       pos = (int)(sl64 - P.dplan->Q0[inst]);
@@ -265,8 +267,9 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
       // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
       const uint32_t b = (uint32_t)P.bstar;
       const uint32_t q1 = MODE == 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
-      const uint32_t q2 = (uint32_t)(((uint64_t)q1 * magic_s[cj]) >> 32);
-      inst = ilist_s[cj][q1 - q2 * (uint32_t)ninst_s[cj]];
+      const uint2 ci = cinfo_s[cj];
+      const uint32_t q2 = ci.x ? __umulhi(q1, ci.x) : q1;
+      inst = ilist_s[cj][q1 - q2 * ci.y];
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
     if (!DISP) pos = sl;

@@ -422,7 +422,7 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
 extern "C" {
 
 const char* pas_version(void) {
-  return "libpas 0.4 (sm_100a; K2 tcgen05 cta_group::1 128x256, cta_group::2 256x256 for small batches)";
+  return "libpas 0.5 (sm_100a; K2 tcgen05 cta_group::1 128x256 on a dynamic chunked schedule, cta_group::2 256x256 for N <= 512)";
 }
 
 const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }

@@ -29,7 +29,8 @@ def test_schedule_invariants(pas, N, M):
     if T:
         L = math.ceil(NT / R)                                              # tiles of the longest range
         assert not s["pair"] and 4 <= T <= 128
-        assert CS == math.ceil(L / T) and CS >= 8                          # every tile in some chunk
+        assert CS == math.ceil(L / T) and CS >= 2                          # every tile in some chunk
+        assert T <= max(4, math.ceil(L / 6))                               # short ranges: >= ~6 steps
         assert R * s["MTg"] >= WORKERS                                     # >= one unit per SM per step
         assert 1 <= s["MTg"] <= MT
         assert CS * R * MT < 2 ** 31                                       # unit ids are int32
@@ -44,7 +45,8 @@ def test_bench_configs(pas):
     assert (c4["R"], c4["T"], c4["MTg"]) == (1, 128, 512)                 # C4: one range, 128-tile chunks
     c3 = pas.pas_debug_k2_schedule(16384, 1_000_000)
     assert c3["R"] == 3 and c3["T"] > 0                                    # 128 prompt tiles < 148 SMs
-    assert pas.pas_debug_k2_schedule(4096, 100_000)["T"] == 0              # C2: short ranges, static
+    c2 = pas.pas_debug_k2_schedule(4096, 100_000)                          # C2: 40-tile ranges, 6 chunks
+    assert (c2["R"], c2["T"], c2["CS"]) == (10, 7, 6)
     c1 = pas.pas_debug_k2_schedule(64, 1000)
     assert c1["pair"] == 1 and c1["T"] == 0
 

@@ -111,6 +111,22 @@ def measured_peaks():
             "fallback (B200_PROFILING.md)"
 
 
+def select_peak(peaks: dict, clk: dict | None):
+    """Which measured peak bounds K2 (MEASURED_PEAKS.json): the sustained figure (cuBLAS 8192^3 back to
+    back under the 1 kW cap) when this run ran power- or thermally-limited -- the long steps (C4, C5)
+    -- else the burst figure (short steps at full clock, e.g. C2; also the conservative choice without
+    clock samples).  Returns (TFLOP/s, description)."""
+    reasons = set((clk or {}).get("reasons") or [])
+    capped = bool(reasons & {"sw_power_cap", "hw_power_brake_slowdown", "hw_slowdown", "sw_thermal_slowdown",
+                             "hw_thermal_slowdown"})
+    if not capped and clk and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        capped = clk["sm_mhz"] < 0.97 * clk["sm_max_mhz"]
+    sustained = peaks.get("bf16_tflops_sustained")
+    if capped and sustained:
+        return float(sustained), "bf16 sustained (power-capped run)"
+    return float(peaks["bf16_tflops"]), "bf16 burst (full-clock run)"
+
+
 def profiled_traffic(config: str, G: int):
     """dram read+write bytes per K2 launch from the committed ncu --set full capture, if any."""
     try:
@@ -309,17 +325,7 @@ def main():
     peaks, peak_src = measured_peaks()
     flops = 2.0 * N * M_local * cfg.d
     achieved = flops / (k2_ms / 1e3) / 1e12
-    # Which measured peak bounds K2 (MEASURED_PEAKS.json): the sustained figure (cuBLAS 8192^3 back to
-    # back under the 1 kW cap) when this run ran power-capped -- the long steps (C4, C5) -- else the
-    # burst figure (short steps at full clock, e.g. C2; also the conservative choice without clocks).
-    reasons = set((clk or {}).get("reasons") or [])
-    capped = bool(reasons & {"sw_power_cap", "hw_power_brake_slowdown", "hw_slowdown", "sw_thermal_slowdown",
-                             "hw_thermal_slowdown"})
-    if not capped and clk and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
-        capped = clk["sm_mhz"] < 0.97 * clk["sm_max_mhz"]
-    sustained = peaks.get("bf16_tflops_sustained")
-    peak = float(sustained if capped and sustained else peaks["bf16_tflops"])
-    peak_kind = "bf16 sustained (power-capped run)" if capped and sustained else "bf16 burst (full-clock run)"
+    peak, peak_kind = select_peak(peaks, clk)
     traffic = profiled_traffic(args.config, G)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,

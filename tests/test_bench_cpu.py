@@ -1,0 +1,39 @@
+"""bench.py host logic (CPU): which measured peak the roofline divides by, and the committed DRAM
+traffic figure it reports."""
+import importlib.util
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_under_test", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+PEAKS = {"bf16_tflops": 1628.4, "bf16_tflops_sustained": 1374.4}
+
+
+def test_power_capped_run_uses_the_sustained_peak():
+    b = _bench()
+    peak, kind = b.select_peak(PEAKS, {"sm_mhz": 1425.0, "sm_max_mhz": 1965.0, "reasons": ["sw_power_cap"]})
+    assert peak == 1374.4 and "sustained" in kind
+    # clocks well below max with no reason reported also counts as limited
+    peak, _ = b.select_peak(PEAKS, {"sm_mhz": 1500.0, "sm_max_mhz": 1965.0, "reasons": []})
+    assert peak == 1374.4
+
+
+def test_full_clock_or_unknown_uses_the_burst_peak():
+    b = _bench()
+    assert b.select_peak(PEAKS, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []})[0] == 1628.4
+    assert b.select_peak(PEAKS, None)[0] == 1628.4                       # no clock samples: conservative
+    assert b.select_peak({"bf16_tflops": 1628.4}, {"reasons": ["sw_power_cap"]})[0] == 1628.4
+
+
+def test_profiled_traffic_is_the_committed_capture():
+    b = _bench()
+    t = b.profiled_traffic("C4", 1)
+    assert t is None or 1.5e10 < t < 6e11                                 # >= the algorithmic 15.5 GB
+    assert b.profiled_traffic("C4", 8) is None                            # no capture at G = 8

@@ -561,16 +561,17 @@ def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, mcast, monkeyp
 
 
 def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
-    """Random shapes with the dynamic schedule forced into small chunks (T = 4 .. 16, as few as one
-    chunk step, empty trailing chunks in the shorter ranges, odd prompt-tile counts for the multicast
-    pairs): every output byte-identical to the static schedule on the same inputs."""
+    """Random shapes (d in {512, 768, 1024}) with the dynamic schedule forced into small chunks (T = 4 ..
+    16, as few as one chunk step, empty trailing chunks in the shorter ranges, odd prompt-tile counts for
+    the multicast pairs): every output byte-identical to the static schedule on the same inputs."""
+    import dataclasses
     rng = np.random.default_rng(2502)
-    cfg = CONFIGS["C2"]
     for case in range(10):
         N = int(rng.integers(513, 6000))
         M = int(rng.integers(20_000, 160_000))
         k = int(rng.choice([1, 2, 5, 8, 11, 16]))
-        w = Workload(cfg, device=DEV, M=M)
+        cfg = dataclasses.replace(CONFIGS["C2"], d=int(rng.choice([512, 768, 1024])))
+        w = Workload(cfg, device=DEV, M=M, d=cfg.d)
         C_ = w.cache_rows(0, M).contiguous()
         P = w.prompts(N, batch=case)
         res = {}
@@ -590,6 +591,6 @@ def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
             a, b = res["static"][key], res["dynamic"][key]
             if key == "bucket_offsets":
                 a, b = a[:W + 1], b[:W + 1]
-            assert np.array_equal(a, b), (case, N, M, k, key, st["k2_chunk_tiles"], st["k2_chunk_steps"])
+            assert np.array_equal(a, b), (case, N, M, k, cfg.d, key, st["k2_chunk_tiles"], st["k2_chunk_steps"])
     for v in ("PAS_K2_SCHED", "PAS_K2_DYN_MIN_STEPS", "PAS_K2_DYN_MB", "PAS_K2_MCAST"):
         monkeypatch.delenv(v)

@@ -97,13 +97,22 @@ __global__ void __launch_bounds__(RT) k6_bounds(const RouteParams P, const DevPl
   const int i = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int nb = 1 << P.kb, len = (nb + kChunks - 1) / kChunks;
   const int32_t* hc = hist + ((int64_t)i << P.kb);
-  if (t == 0) {
-    int run = 0;
-    for (int c = 0; c < kChunks; ++c) {
-      cex[c] = run;
-      run += csum[i * kChunks + c];
+  {   // exclusive scan of the class's kChunks chunk sums (one per thread: warp scans + warp totals)
+    static_assert(kChunks == RT, "one chunk sum per thread");
+    __shared__ int32_t wtot[RT / 32];
+    const int v = csum[i * kChunks + t];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
-    cex[kChunks] = run;
+    if (lane == 31) wtot[w] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int q = 0; q < w; ++q) before += wtot[q];
+    cex[t] = before + incl - v;
+    if (t == RT - 1) cex[kChunks] = before + incl;
   }
   if (t < kMaxLevels) sb[t] = INT32_MAX;
   __syncthreads();
@@ -111,8 +120,9 @@ __global__ void __launch_bounds__(RT) k6_bounds(const RouteParams P, const DevPl
   for (int j = w; j + 1 < P.nK; j += RT / 32) {   // split rank X_i[j]: the first prompt of group j + 1
     const int X = plan->X[i][j];
     if (X >= h) continue;                          // no such prompt
-    int c = 0;
-    while (cex[c + 1] <= X) ++c;
+    int c = 0;   // the chunk holding rank X: the last c with cex[c] <= X (binary search, cex ascending)
+    for (int step = kChunks / 2; step > 0; step >>= 1)
+      if (c + step < kChunks && cex[c + step] <= X) c += step;
     const int c0 = c * len, c1 = c0 + len < nb ? c0 + len : nb;
     int run = cex[c];
     for (int base = c0; base < c1; base += 32) {   // 32 buckets at a time, warp scan

@@ -53,7 +53,8 @@ def parse():
 
 # ----------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms; only the samples taken between
+    begin() and stop() count (nvidia-smi takes ~1 s to start, longer than a short timed region)."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -63,17 +64,25 @@ class ClockSampler:
         self.rows = []
         self.proc = None
         self.thread = None
+        self.first = 0
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+
+    def begin(self):
+        """Wait (<= 5 s) until nvidia-smi is producing samples, then open the counted window."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < 5.0:
+            time.sleep(0.02)
+        self.first = len(self.rows)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -82,12 +91,14 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
+        last = len(self.rows)
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        self.rows = self.rows[self.first:last]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
@@ -269,6 +280,7 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.begin()
     stage_sum = [0.0] * 8
     launches = 0
     ev0 = torch.cuda.Event(enable_timing=True)

@@ -13,8 +13,10 @@ timeout 900 python bench.py --dispatcher --no-cpu-baseline --no-e2e > $O/bench_c
 timeout 900 python bench.py --config C3 --steps 30 > $O/bench_c3_g1.json 2> $O/bench_c3_g1.err
 timeout 900 python bench.py --config C2 --steps 50 > $O/bench_c2_g1.json 2> $O/bench_c2_g1.err
 timeout 600 python tools/bench_controller.py > $O/controller.jsonl 2> $O/controller.err
+if [ "${SWEEPS:-1}" = 1 ]; then
 timeout 1200 python tools/sweep.py --kind load --steps 4 --warmup 2 > $O/c5_load_sweep_50M_g1.jsonl 2> $O/c5_sweep.err
 timeout 1200 python tools/sweep.py --kind cache --steps 4 --warmup 2 > $O/cache_sweep_n16384.jsonl 2> $O/cache_sweep.err
+fi
 # launch list of the bench command: skip the 2 launches per 65,536-row block of the 10M cache load
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_|k6_" -s 306 -c 60 --csv --log-file $O/c4_g1_launches.csv $CMD > $O/ncu_launch.log 2>&1; echo "ncu1 rc=$?" >> $O/ncu_launch.log

@@ -37,3 +37,15 @@ def test_profiled_traffic_is_the_committed_capture():
     t = b.profiled_traffic("C4", 1)
     assert t is None or 1.5e10 < t < 6e11                                 # >= the algorithmic 15.5 GB
     assert b.profiled_traffic("C4", 8) is None                            # no capture at G = 8
+
+
+def test_clock_sampler_counts_only_the_timed_window():
+    # rows taken before begin() (nvidia-smi start-up, warm-up) and after stop() must not count
+    b = _bench()
+    c = b.ClockSampler(0)
+    row = lambda mhz, cap: [str(mhz), "1965", "900.0", "Not Active", "Not Active", "Not Active", cap]
+    c.rows = [row(1965, "Not Active")] * 3
+    c.first = len(c.rows)
+    c.rows += [row(1400, "Active"), row(1420, "Active")]
+    clk = c.stop()
+    assert clk["samples"] == 2 and clk["sm_mhz"] == 1410.0 and clk["reasons"] == ["sw_power_cap"]

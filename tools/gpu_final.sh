@@ -10,8 +10,8 @@ timeout 2400 python -m pytest tests -m gpu -q -s > $O/gpu_tests.log 2>&1; echo "
 timeout 900 python bench.py > $O/bench_c4_g1.json 2> $O/bench_c4_g1.err; echo "rc=$?" >> $O/bench_c4_g1.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference_c4.json 2> $O/bench_reference_c4.err
 timeout 900 python bench.py --dispatcher --no-cpu-baseline --no-e2e > $O/bench_c4_g1_dispatcher.json 2> $O/bench_c4_g1_dispatcher.err
-timeout 900 python bench.py --config C3 --steps 30 > $O/bench_c3_g1.json 2> $O/bench_c3_g1.err
-timeout 900 python bench.py --config C2 --steps 50 > $O/bench_c2_g1.json 2> $O/bench_c2_g1.err
+timeout 900 python bench.py --config C3 --steps 100 > $O/bench_c3_g1.json 2> $O/bench_c3_g1.err
+timeout 900 python bench.py --config C2 --steps 2000 > $O/bench_c2_g1.json 2> $O/bench_c2_g1.err
 timeout 600 python tools/bench_controller.py > $O/controller.jsonl 2> $O/controller.err
 if [ "${SWEEPS:-1}" = 1 ]; then
 timeout 1200 python tools/sweep.py --kind load --steps 4 --warmup 2 > $O/c5_load_sweep_50M_g1.jsonl 2> $O/c5_sweep.err

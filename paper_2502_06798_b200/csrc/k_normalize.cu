@@ -8,7 +8,8 @@
 // One warp per row, 128-bit loads (4 fp32 / 4 bf16 per lane per step); the row's loads are all in
 // flight at once for the fp64 sum of squares, then the row is re-read (an L1 / L2 hit, no HBM bytes)
 // for the quantised stores, so no value is live across the reduction: 40 registers, 6 resident CTAs
-// (48 warps) per SM.  Measured (profiles/r01_k1c): cache insert 5.02 TB/s vs 4.56 with
+// (48 warps) per SM.  Measured (profiles/r01_k1c, r01_k1g): cache insert 5.43 TB/s (5.02 on
+// a resident-CTA grid) vs 4.56 with
 // the row held in registers at 3 CTAs/SM (80 registers) and 4.78 at 4 CTAs/SM (64 registers, spills).
 // HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
 // Cache insert applies the shard filter of the round-robin partition (gid g lives on rank g % G at
@@ -65,6 +66,11 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
 #endif
 #ifndef PAS_K1_RELOAD
 #define PAS_K1_RELOAD 1   // re-read the row for the stores (fewer live registers, more resident warps)
+#endif
+#ifndef PAS_K1_GRIDCAP
+#define PAS_K1_GRIDCAP 0  // 0: one CTA per 8 rows, the block scheduler balances the tail (64 vs 70 us
+                          // at C4, cache insert 5.43 vs 4.96 TB/s, profiles/r01_k1g/); 1: grid = the
+                          // resident CTAs with grid-stride rows
 #endif
 #ifndef PAS_K1_ACC
 #define PAS_K1_ACC 1      // independent fp64 partial sums per lane (shorter DFMA dependency chain)
@@ -156,10 +162,10 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
                      int rank, int* invalid_count, cudaStream_t st) {
   const int threads = 256;
   const int vec = d % 128 == 0 && d <= 1024 ? d / 128 : 0;
-  // grid = exactly the resident CTAs (3 per SM by the launch bounds): one wave, grid-stride rows
+  // one warp per row, one CTA per 8 rows (PAS_K1_GRIDCAP 1: capped at the resident CTAs, grid-stride)
   int64_t blocks = (rows * 32 + threads - 1) / threads;
   const int64_t cap = (int64_t)kNumSMs * PAS_K1_MINB;
-  if (blocks > cap) blocks = cap;
+  if (PAS_K1_GRIDCAP && blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
   switch (vec) {
     case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;

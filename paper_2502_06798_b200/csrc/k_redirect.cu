@@ -28,9 +28,6 @@ namespace pas {
 namespace {
 
 constexpr int RT = 256;
-#ifndef PAS_K6_ILP
-#define PAS_K6_ILP 1      // k6_assign: prompts per thread per grid step
-#endif
 constexpr int kSmemList = 2048;   // k6_resolve: entries staged in shared memory (else read from L2)
 
 __device__ __forceinline__ bool entry_less(uint64_t ka, int32_t pa, uint64_t kb, int32_t pb) {
@@ -192,37 +189,22 @@ __global__ void __launch_bounds__(RT) k6_assign(const uint8_t* __restrict__ leve
     sl[i][j] = j + 1 < P.nK ? bnd->list[i][j] : -1;
   }
   __syncthreads();
-  // PAS_K6_ILP prompts per thread per step: their loads are issued together (bytes in flight)
-  const int64_t stride = (int64_t)gridDim.x * RT;
-  for (int64_t p0 = (int64_t)blockIdx.x * RT + threadIdx.x; p0 < P.N; p0 += stride * PAS_K6_ILP) {
-    int lv[PAS_K6_ILP];
-    uint64_t kp[PAS_K6_ILP];
-#pragma unroll
-    for (int u = 0; u < PAS_K6_ILP; ++u) {
-      const int64_t p = p0 + u * stride;
-      lv[u] = p < P.N ? level[p] : 0;
-      kp[u] = p < P.N ? key[p] : 0;
+  for (int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x; p < P.N; p += (int64_t)gridDim.x * RT) {
+    const int i = level[p];
+    const uint64_t kappa = key[p];
+    const int b = (int)top_bits(kappa, P.kb);
+    int below = 0, list = -1;
+    for (int j = 0; j + 1 < P.nK; ++j) {
+      below += sb[i][j] < b;
+      if (sb[i][j] == b) list = sl[i][j];
     }
-#pragma unroll
-    for (int u = 0; u < PAS_K6_ILP; ++u) {
-      const int64_t p = p0 + u * stride;
-      if (p >= P.N) break;
-      const int i = lv[u];
-      const uint64_t kappa = kp[u];
-      const int b = (int)top_bits(kappa, P.kb);
-      int below = 0, list = -1;
-      for (int j = 0; j + 1 < P.nK; ++j) {
-        below += sb[i][j] < b;
-        if (sb[i][j] == b) list = sl[i][j];
-      }
-      if (list < 0) {
-        emit(P, grid_s, plan, p, below, K_prime, cls7);
-        continue;
-      }
-      K6List* L = lists + list;
-      const int slot = atomicAdd(&L->fill, 1);
-      cand[L->base + slot] = KeyEntry{kappa, (int32_t)p, 0};
+    if (list < 0) {
+      emit(P, grid_s, plan, p, below, K_prime, cls7);
+      continue;
     }
+    K6List* L = lists + list;
+    const int slot = atomicAdd(&L->fill, 1);
+    cand[L->base + slot] = KeyEntry{kappa, (int32_t)p, 0};
   }
 }
 

@@ -13,6 +13,10 @@
 // non-zero bin.  HBM per prompt: S*k*8 B read, k*8 + 5 B written (+1 flag byte read).
 #include "pas_internal.cuh"
 
+#ifndef PAS_S1_GRIDCAP
+#define PAS_S1_GRIDCAP 1   // k_select_s1: grid = one resident wave (grid-stride); 0: uncapped
+#endif
+
 namespace pas {
 namespace {
 
@@ -351,7 +355,7 @@ cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, co
         n = 4;
       return n;
     }();
-    if (blocks > (int64_t)kNumSMs * per_sm) blocks = (int64_t)kNumSMs * per_sm;   // one resident wave
+    if (PAS_S1_GRIDCAP && blocks > (int64_t)kNumSMs * per_sm) blocks = (int64_t)kNumSMs * per_sm;   // one resident wave
     const unsigned g = (unsigned)blocks;
     const int4* in4 = reinterpret_cast<const int4*>(in);
     switch (p.topk >> 1) {

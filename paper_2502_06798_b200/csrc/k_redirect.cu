@@ -28,6 +28,9 @@ namespace pas {
 namespace {
 
 constexpr int RT = 256;
+#ifndef PAS_K6_GRIDCAP
+#define PAS_K6_GRIDCAP 1   // k6_assign: grid capped at 8 CTAs per SM (grid-stride); 0: uncapped
+#endif
 constexpr int kSmemList = 2048;   // k6_resolve: entries staged in shared memory (else read from L2)
 
 __device__ __forceinline__ bool entry_less(uint64_t ka, int32_t pa, uint64_t kb, int32_t pb) {
@@ -258,7 +261,7 @@ cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const De
   launch_pdl(k6_hist, blocks, RT, 0, st, level, p, w.key, w.hist);
   launch_pdl(k6_chunks, p.nK * kChunks, RT, 0, st, p, w.hist, w.csum);
   launch_pdl(k6_bounds, p.nK, RT, 0, st, p, plan, w.hist, w.csum, w.bnd, w.lists, w.used);
-  const unsigned ablocks = blocks < (unsigned)kNumSMs * 8 ? blocks : (unsigned)kNumSMs * 8;
+  const unsigned ablocks = (!PAS_K6_GRIDCAP || blocks < (unsigned)kNumSMs * 8) ? blocks : (unsigned)kNumSMs * 8;
   launch_pdl(k6_assign, ablocks, RT, 0, st, level, w.key, p, plan, w.bnd, w.lists, w.cand, K_prime, w.cls7);
   launch_pdl(k6_resolve, p.nK * (p.nK - 1) > 0 ? p.nK * (p.nK - 1) : 1, RT, 0, st, p, plan, w.bnd, w.lists, w.used,
              w.cand, K_prime, w.cls7);

@@ -13,7 +13,8 @@
 // the row held in registers at 3 CTAs/SM (80 registers) and 4.78 at 4 CTAs/SM (64 registers, spills).
 // HBM-bound: algorithmic bytes per row = d*(in_bytes + 2) (+1 flag byte).
 // Cache insert applies the shard filter of the round-robin partition (gid g lives on rank g % G at
-// local row g / G) and reads only this rank's rows.
+// local row g / G): it stores only this rank's rows but checks every row's validity, so
+// all ranks accept or reject a load together.
 #include "pas_internal.cuh"
 
 namespace pas {
@@ -86,7 +87,11 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp_global; i < rows; i += nwarps) {
     const int64_t gid = first_gid + i;
-    if (G > 1 && (gid % G) != rank) continue;
+    // A row of another rank's shard is not stored here, but its validity is still checked when the
+    // caller counts invalid rows (cache insert): every rank must accept or reject the same load
+    // (pas.h: "nothing appended"), whichever rank owns the bad row.
+    const bool own = G == 1 || (gid % G) == rank;
+    if (!own && !invalid_count) continue;
     const int64_t orow = (G > 1) ? gid / G : gid;
     const T* src = in + i * (int64_t)d;
     __nv_bfloat16* dst = out + orow * (int64_t)d;
@@ -113,6 +118,10 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       finite = __all_sync(0xffffffffu, finite);
       const double norm = sqrt(ss);
       const bool valid = finite && norm > 0.0;
+      if (!own) {
+        if (lane == 0 && !valid) atomicAdd(invalid_count, 1);
+        continue;
+      }
 #if PAS_K1_RELOAD
       // the row is re-read (L1 / L2 hit, no HBM traffic) instead of held across the reduction
 #pragma unroll
@@ -144,6 +153,10 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       finite = __all_sync(0xffffffffu, finite);
       const double norm = sqrt(ss);
       const bool valid = finite && norm > 0.0;
+      if (!own) {
+        if (lane == 0 && !valid) atomicAdd(invalid_count, 1);
+        continue;
+      }
       for (int c = lane * 4; c < d; c += 128) {
         float v[4];
         load4(src + c, v);

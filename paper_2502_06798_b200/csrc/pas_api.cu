@@ -151,6 +151,7 @@ struct pas_ctx {
   ncclComm_t comm = nullptr;
   // timing
   cudaEvent_t ev[8]{};
+  cudaEvent_t ev_aux = nullptr;   // end event of pas_solve_assignment's timing
   bool ev_valid = false;
   cudaStream_t last_stream = nullptr;
 };
@@ -253,6 +254,16 @@ pas_status validate_out(pas_ctx* ctx, const pas_route_out* out, bool device = tr
       if (reinterpret_cast<uintptr_t>(q) & 15)
         return fail(ctx, PAS_ERR_ARG, "output arrays must be 16-byte aligned (vectorised stores)");
   }
+  return PAS_OK;
+}
+
+// K1 reads rows with 128-bit (fp32) / 64-bit (bf16) vector loads: the base must be aligned to that
+// (d is a multiple of 64, so every row then is).
+pas_status validate_rows(pas_ctx* ctx, const void* rows, pas_dtype dt) {
+  if (dt != PAS_F32 && dt != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
+  const uintptr_t a = reinterpret_cast<uintptr_t>(rows);
+  if (a & (dt == PAS_F32 ? 15 : 7))
+    return fail(ctx, PAS_ERR_ARG, "embedding rows must be %d-byte aligned (vector loads)", dt == PAS_F32 ? 16 : 8);
   return PAS_OK;
 }
 
@@ -372,7 +383,10 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
                             nullptr, 0, st));
   ctx->launches++;
   SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
-  const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;   // else: all prompts valid
+  // the validity flags of the pas_route_local / run_local that produced these candidates; consumed
+  // here, so a later pas_route_from_candidates with the same N never reuses them (else: all valid)
+  const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;
+  ctx->last_local_N = -1;
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
@@ -462,6 +476,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->ev_aux) cudaEventDestroy(ctx->ev_aux);
   delete ctx;
   return PAS_OK;
 }
@@ -537,6 +552,10 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
       pas_destroy(ctx);
       return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
     }
+  if (cudaEventCreate(&ctx->ev_aux) != cudaSuccess) {
+    pas_destroy(ctx);
+    return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
+  }
   if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c((int)d)) ||
       !encode_map(&ctx->tm_c2, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c_pair())) {
     pas_destroy(ctx);
@@ -583,8 +602,8 @@ pas_status pas_cache_load(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64
                           pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
-  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
   if (M < 0 || (M > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / M");
+  if ((s = validate_rows(ctx, rows, dtype))) return s;
   const int G = ctx->cfg.world, rank = ctx->cfg.rank;
   const int64_t new_total = ctx->M_total + M;
   if (new_total >= (1LL << 31)) return fail(ctx, PAS_ERR_CAPACITY, "global ids must stay below 2^31");
@@ -657,8 +676,8 @@ pas_status pas_cache_insert(pas_ctx* ctx, const void* rows, pas_dtype dtype, int
                             pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
-  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
   if (n < 0 || (n > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / n");
+  if ((s = validate_rows(ctx, rows, dtype))) return s;
   if (n > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "n > max_batch (rows are staged like a batch)");
   if (n == 0) return PAS_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -682,8 +701,8 @@ pas_status pas_cache_insert_vanilla(pas_ctx* ctx, const void* emb, pas_dtype dty
   pas_status s = check_live(ctx);
   if (s) return s;
   if (n_inserted) *n_inserted = 0;
-  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "dtype must be PAS_F32 or PAS_BF16");
   if (N < 0 || (N > 0 && (!emb || !K_prime))) return fail(ctx, PAS_ERR_ARG, "bad emb / K_prime / N");
+  if ((s = validate_rows(ctx, emb, dtype))) return s;
   if (N > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "N > max_batch");
   if (N == 0) return PAS_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -739,6 +758,7 @@ pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const fl
   ctx->fractions_set = false;
   if (ctx->fc_window > 0) {   // the window holds level indices of the old bands: start afresh
     CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+    CUDA_TRY(ctx, cudaDeviceSynchronize());   // no batch in flight may still read or write the window
     CUDA_TRY(ctx, cudaMemset(ctx->fc_state, 0, sizeof(FcState)));
     ctx->fc_tick = 0;
     ctx->fc_planned = false;
@@ -958,6 +978,11 @@ pas_status pas_solve_assignment(pas_ctx* ctx, int W, double lambda_rps, const do
     p.service_us[k] = service_us[k];
     p.H[k] = H ? H[k] : 0.0;
   }
+  if (H) {   // a_K = 1 - sum_i H_i c(K - K_i) is SPEC's expected quality only for a distribution
+    double hs = 0.0;
+    for (int k = 0; k < ctx->nK; ++k) hs += H[k];
+    if (std::fabs(hs - 1.0) > 1e-9) return fail(ctx, PAS_ERR_ARG, "sum H = %.12g != 1 (S:35)", hs);
+  }
   for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
   p.fc = H ? nullptr : ctx->fc_state;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
@@ -970,15 +995,13 @@ pas_status pas_solve_assignment(pas_ctx* ctx, int W, double lambda_rps, const do
   cudaStream_t st = ctx->last_stream;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev[7], st));
   CUDA_TRY(ctx, launch_assign(p, ctx->asg_keys, kMaxBlocks, ctx->asg_out, st));
-  cudaEvent_t done;
-  CUDA_TRY(ctx, cudaEventCreate(&done));
+  cudaEvent_t done = ctx->ev_aux;
   CUDA_TRY(ctx, cudaEventRecord(done, st));
   AssignOut h;
   CUDA_TRY(ctx, cudaMemcpyAsync(&h, ctx->asg_out, sizeof h, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[7], done);
-  cudaEventDestroy(done);
   memset(out, 0, sizeof(*out));
   out->nK = ctx->nK;
   out->W = W;
@@ -1001,7 +1024,7 @@ pas_status pas_route_local(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   pas_status s = check_live(ctx);
   if (s) return s;
   if (N < 0 || N > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "N outside [0, max_batch]");
-  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  if ((s = validate_rows(ctx, emb, dtype))) return s;
   if (N > 0 && (!emb || !cand_dev)) return fail(ctx, PAS_ERR_ARG, "null emb / cand");
   ctx->launches = 0;
   if (N == 0) return PAS_OK;
@@ -1036,7 +1059,7 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   pas_status s = check_live(ctx);
   if (s) return s;
   if ((s = ready(ctx, N))) return s;
-  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  if ((s = validate_rows(ctx, emb, dtype))) return s;
   ctx->launches = 0;
   if (N == 0) return PAS_OK;
   if ((s = validate_out(ctx, out))) return s;
@@ -1200,6 +1223,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   pas_status s = check_live(ctx);
   if (s) return s;
   if (N < 1 || N > ctx->cfg.max_batch || !emb || !scores_dev) return fail(ctx, PAS_ERR_ARG, "bad arguments");
+  if ((s = validate_rows(ctx, emb, dtype))) return s;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   if ((s = ensure_prompt_ws(ctx))) return s;

@@ -147,10 +147,12 @@ def pas_create(d=768, topk=8, max_batch=4096, max_rows_per_rank=1 << 20, device=
         cfg.nccl_id = C.cast(keep, C.c_void_p)
     ctx = _P()
     _check(None, lib.pas_create(C.byref(ctx), C.byref(cfg)))
+    _CTX_D[ctx.value] = d
     return ctx
 
 
 def pas_destroy(ctx):
+    _CTX_D.pop(ctx.value, None)
     _check(None, lib.pas_destroy(ctx))
 
 
@@ -161,6 +163,22 @@ def _stream(stream):
     if isinstance(stream, int):
         return _P(stream)
     return _P(stream.cuda_stream)
+
+
+_CTX_D: dict = {}   # embedding width d of each live context (argument checks only)
+
+
+def _rows(ctx, t, device=True):
+    """Embedding rows [n, d] as the C side reads them: contiguous (row stride d), width d, on the
+    device (or the host for pas_route_batch_host).  Raises instead of letting K1 read out of bounds."""
+    d = _CTX_D.get(ctx.value if isinstance(ctx, _P) else ctx)
+    if t.dim() != 2 or (d is not None and t.shape[1] != d):
+        raise ValueError(f"embeddings must be [n, {d}], got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError("embeddings must be contiguous (row-major, stride d)")
+    if t.is_cuda != device:
+        raise ValueError("embeddings must be a CUDA tensor" if device else "embeddings must be a host tensor")
+    return _P(t.data_ptr())
 
 
 def _dtype_code(t) -> int:
@@ -174,9 +192,8 @@ def _dtype_code(t) -> int:
 
 def pas_cache_load(ctx, rows, stream=None) -> int:
     """rows: contiguous CUDA tensor [M, d] (float32 / bfloat16).  Returns the first global id."""
-    assert rows.is_cuda and rows.is_contiguous()
     first = C.c_int64(0)
-    _check(ctx, lib.pas_cache_load(ctx, _P(rows.data_ptr()), _dtype_code(rows), rows.shape[0],
+    _check(ctx, lib.pas_cache_load(ctx, _rows(ctx, rows), _dtype_code(rows), rows.shape[0],
                                    C.byref(first), _stream(stream)))
     return first.value
 
@@ -214,13 +231,13 @@ def pas_set_seed(ctx, seed, batch_seq=0):
 
 
 def pas_cache_insert(ctx, rows, gids_out=None, stream=None):
-    _check(ctx, lib.pas_cache_insert(ctx, _P(rows.data_ptr()), _dtype_code(rows), rows.shape[0],
+    _check(ctx, lib.pas_cache_insert(ctx, _rows(ctx, rows), _dtype_code(rows), rows.shape[0],
                                      _P(gids_out.data_ptr()) if gids_out is not None else None, _stream(stream)))
 
 
 def pas_cache_insert_vanilla(ctx, emb, K_prime, gids_by_prompt=None, stream=None) -> int:
     n = C.c_int64(0)
-    _check(ctx, lib.pas_cache_insert_vanilla(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0],
+    _check(ctx, lib.pas_cache_insert_vanilla(ctx, _rows(ctx, emb), _dtype_code(emb), emb.shape[0],
                                              _P(K_prime.data_ptr()),
                                              _P(gids_by_prompt.data_ptr()) if gids_by_prompt is not None else None,
                                              C.byref(n), _stream(stream)))
@@ -283,20 +300,20 @@ def make_out(**arrays) -> PasRouteOut:
 
 def pas_route_batch(ctx, emb, out: dict, stream=None):
     o = make_out(**out)
-    _check(ctx, lib.pas_route_batch(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0], C.byref(o),
+    _check(ctx, lib.pas_route_batch(ctx, _rows(ctx, emb), _dtype_code(emb), emb.shape[0], C.byref(o),
                                     _stream(stream)))
 
 
 def pas_route_batch_host(ctx, emb, out: dict, stream=None):
     """emb: CPU tensor (pinned for speed); out: dict of CPU tensors."""
     o = make_out(**out)
-    _check(ctx, lib.pas_route_batch_host(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0],
+    _check(ctx, lib.pas_route_batch_host(ctx, _rows(ctx, emb, device=False), _dtype_code(emb), emb.shape[0],
                                          C.byref(o), _stream(stream)))
 
 
 def pas_route_local(ctx, emb, cand, stream=None):
     """cand: CUDA int64/float tensor with N*topk 8-byte elements (pairs {float score, int32 gid})."""
-    _check(ctx, lib.pas_route_local(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0],
+    _check(ctx, lib.pas_route_local(ctx, _rows(ctx, emb), _dtype_code(emb), emb.shape[0],
                                     _P(cand.data_ptr()), _stream(stream)))
 
 
@@ -338,7 +355,7 @@ def pas_debug_k2_schedule(N, M_local, d=768, max_batch=None) -> dict:
 
 
 def pas_debug_scores(ctx, emb, scores, stream=None):
-    _check(ctx, lib.pas_debug_scores(ctx, _P(emb.data_ptr()), _dtype_code(emb), emb.shape[0],
+    _check(ctx, lib.pas_debug_scores(ctx, _rows(ctx, emb), _dtype_code(emb), emb.shape[0],
                                      _P(scores.data_ptr()), _stream(stream)))
 
 

@@ -4,8 +4,18 @@ Graded (north_star): scores within 2e-2 of the fp64 Tier-A similarity; top-k ids
 position whose Tier-A margins to both neighbours are >= 2e-2 (R17); optimal-K bit-exact wherever s1
 is >= 2e-2 from every threshold; everything downstream (H_K, f, x, K', instance, slot, buckets)
 bit-exact, teacher-forced on the GPU's K vector when a flagged near-tie flipped a K; D_Q within 1e-5
-relative.  Internal (tighter): every returned score within TAU_B of the fp64 dot product of the
-bf16-quantised rows of the id the GPU returned (Tier B).
+relative.
+
+Internal (tighter, SURVEY 8(c).6 S1/S2 "internally"): the oracle also scans the WHOLE cache under
+Tier B (s_hat = fp64 dot of the bf16-quantised rows, O1').  The GPU differs from s_hat only by its
+fp32 summation (< TAU_B), so
+  * every returned score is within TAU_B of s_hat of its id, and position-wise within TAU_B of the
+    Tier-B top-k (order statistics are 1-Lipschitz);
+  * the ids are bit-exact at every position whose Tier-B margins to both neighbours are >= 2 TAU_B
+    (nothing else can be reordered into it), and the optimal-K level is bit-exact wherever the Tier-B
+    s1 is >= 2 TAU_B from every threshold.
+On clustered data this grades almost every position (the Tier-A rule grades few: V3), so retrieval is
+checked on ordinary prompts, not only on planted duplicates; the fractions are reported and floored.
 """
 from __future__ import annotations
 
@@ -31,18 +41,32 @@ DELTA = 2 * 2.0 ** -8 + 2.0 ** -16 + TAU_B
 @dataclass
 class Report:
     n: int = 0
-    graded_ids: int = 0
+    positions: int = 0           # finite (non-sentinel) top-k positions checked
+    graded_ids: int = 0          # graded under Tier A (R17, north_star)
+    graded_ids_B: int = 0        # graded under Tier B (margins >= 2 TAU_B)
+    levels_B: int = 0            # prompts whose level is graded under Tier B
+    levels_checked: int = 0
     k_flips: list = field(default_factory=list)
     max_score_err_A: float = 0.0
     max_score_err_B: float = 0.0
     flagged_top1: int = 0
     flagged_threshold: int = 0
+    flagged_B: list = field(default_factory=list)   # (prompt, position, min Tier-B margin) not graded
     notes: list = field(default_factory=list)
 
+    def frac_A(self):
+        return self.graded_ids / max(1, self.positions)
+
+    def frac_B(self):
+        return self.graded_ids_B / max(1, self.positions)
+
     def summary(self):
-        return (f"n={self.n} graded_ids={self.graded_ids} k_flips={len(self.k_flips)} "
-                f"max|s-sA|={self.max_score_err_A:.3g} max|s-sB|={self.max_score_err_B:.3g} "
-                f"flag_top1={self.flagged_top1} flag_thr={self.flagged_threshold}")
+        return (f"n={self.n} positions={self.positions} graded_A={self.graded_ids} ({self.frac_A():.1%}) "
+                f"graded_B={self.graded_ids_B} ({self.frac_B():.1%}) levels_B={self.levels_B}/{self.levels_checked} "
+                f"k_flips={len(self.k_flips)} max|s-sA|={self.max_score_err_A:.3g} max|s-sB|={self.max_score_err_B:.3g} "
+                f"flag_top1={self.flagged_top1} flag_thr={self.flagged_threshold} "
+                f"tierB_flagged={len(self.flagged_B)}"
+                + (f" (min margin {min(m for _, _, m in self.flagged_B):.2g})" if self.flagged_B else ""))
 
 
 def oracle_topk_streaming(P: np.ndarray, cache_chunks, k: int):
@@ -80,6 +104,119 @@ def oracle_topk_parallel(P: np.ndarray, cache_chunks, k: int, workers: int | Non
     return acc["ids"], acc["sc"], acc["valid"]
 
 
+def _topk_tier_b(Pq: np.ndarray, Pvalid: np.ndarray, first: int, Cq: np.ndarray, k: int):
+    """Tier-B top-k of quantised prompts against one quantised cache chunk Cq (the oracle's own
+    quantize, O1'), by the oracle's similarity_B and top-k (O2); invalid prompts get sentinels (R16)."""
+    S = O.similarity_B(Pq, Cq)
+    gids = np.arange(first, first + Cq.shape[0], dtype=np.int64)
+    ids, sc = O.topk_prefiltered(S, gids, k)
+    ids[~Pvalid] = O.SENTINEL_GID
+    sc[~Pvalid] = O.NEG_INF
+    return ids, sc
+
+
+def oracle_topk_ab(P: np.ndarray, cache_chunks, k: int, workers: int | None = None, pblock: int = 1024):
+    """Tier-A AND Tier-B top-(k+1) of prompts P over the whole streamed cache (the (k+1)-th entries are
+    the next neighbours for the margins).  Each chunk is one thread-pool job (NumPy releases the GIL;
+    BLAS held to one thread per worker) that runs the oracle's per-chunk calls over prompt blocks of
+    ``pblock`` (bounded memory); per-chunk lists are merged in chunk order with the oracle's merge_topk.
+    Test plumbing only: the arithmetic is the oracle's, unchanged.
+    Returns dict(ids_A, sc_A, ids_B, sc_B, valid)."""
+    import collections
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+    workers = workers or max(1, min(32, len(os.sched_getaffinity(0))))
+    n = P.shape[0]
+    kk = k + 1
+    Pq, Pvalid = O.quantize(P)
+    blocks = [(lo, min(n, lo + pblock)) for lo in range(0, n, pblock)]
+    acc = {}
+
+    def job(first, rows):
+        Cq, cvalid = O.quantize(rows)
+        if not cvalid.all():
+            raise ValueError("cache rows must be valid")
+        out = []
+        for lo, hi in blocks:
+            ia, sa, va = O.topk_streaming(P[lo:hi], [(first, rows)], kk)
+            ib, sb = _topk_tier_b(Pq[lo:hi], Pvalid[lo:hi], first, Cq, kk)
+            out.append((ia, sa, va, ib, sb))
+        return out
+
+    def merge(res):
+        ia = np.concatenate([r[0] for r in res])
+        sa = np.concatenate([r[1] for r in res])
+        va = np.concatenate([r[2] for r in res])
+        ib = np.concatenate([r[3] for r in res])
+        sb = np.concatenate([r[4] for r in res])
+        if not acc:
+            acc.update(ids_A=ia, sc_A=sa, ids_B=ib, sc_B=sb, valid=va)
+        else:
+            acc["ids_A"], acc["sc_A"] = O.merge_topk(acc["ids_A"], acc["sc_A"], ia, sa, kk)
+            acc["ids_B"], acc["sc_B"] = O.merge_topk(acc["ids_B"], acc["sc_B"], ib, sb, kk)
+
+    def drain(pending, limit):
+        while len(pending) > limit:
+            merge(pending.popleft().result())
+
+    with threadpool_limits(limits=1, user_api="blas"), ThreadPoolExecutor(workers) as ex:
+        pending = collections.deque()
+        for first, rows in cache_chunks:
+            pending.append(ex.submit(job, first, rows))
+            drain(pending, 2 * workers)
+        drain(pending, 0)
+    if not acc:   # empty cache: every prompt cold
+        sent_i = np.full((n, kk), O.SENTINEL_GID, dtype=np.int64)
+        sent_s = np.full((n, kk), O.NEG_INF)
+        acc.update(ids_A=sent_i, sc_A=sent_s, ids_B=sent_i.copy(), sc_B=sent_s.copy(), valid=O.row_valid(P))
+    return acc
+
+
+def check_topk_tier_b(gpu_ids, gpu_sc, ob_ids, ob_sc, rep: Report, floor: float | None = None):
+    """Internal S1: gpu [n, k] vs the Tier-B top-(k+1) of the whole cache.
+    Scores position-wise within TAU_B; ids bit-exact at every position whose Tier-B margins to both
+    neighbours are >= 2 TAU_B; the rest reported with their margins.  ``floor``: minimum fraction of
+    finite positions that must be graded (so the check can never become vacuous)."""
+    n, k = gpu_ids.shape
+    fin = np.isfinite(ob_sc[:, :k])
+    assert np.array_equal(np.isfinite(gpu_sc), fin), "Tier-B sentinel positions differ"
+    if fin.any():
+        eb = np.abs(gpu_sc[fin] - ob_sc[:, :k][fin])
+        rep.max_score_err_B = max(rep.max_score_err_B, float(eb.max()))
+        assert eb.max() <= TAU_B, f"position-wise Tier-B score error {eb.max():.3g} > {TAU_B}"
+    prev = np.concatenate([np.full((n, 1), np.inf), ob_sc[:, :k - 1]], axis=1)
+    cur = ob_sc[:, :k]
+    nxt = ob_sc[:, 1:k + 1]
+    with np.errstate(invalid="ignore"):
+        m_lo = np.where(np.isfinite(nxt), cur - nxt, np.inf)
+        margin = np.minimum(prev - cur, m_lo)
+    graded = fin & (margin >= 2 * TAU_B)
+    bad = graded & (gpu_ids != ob_ids[:, :k])
+    assert not bad.any(), (f"{int(bad.sum())} Tier-B-graded top-k ids differ, e.g. (prompt, pos) "
+                           f"{tuple(np.argwhere(bad)[0])}: gpu {gpu_ids[bad][0]} vs oracle {ob_ids[:, :k][bad][0]}")
+    rep.graded_ids_B += int(graded.sum())
+    for p_, m_ in np.argwhere(fin & ~graded):
+        rep.flagged_B.append((int(p_), int(m_), float(margin[p_, m_])))
+    if floor is not None and fin.any():
+        frac = graded.sum() / fin.sum()
+        assert frac >= floor, f"only {frac:.1%} of top-k positions graded under Tier B (floor {floor:.0%})"
+
+
+def check_levels_tier_b(gpu_level, ob_s1, usable, thresholds, rep: Report):
+    """Internal S2: the level of #{m : s_hat1 >= t_m} wherever the Tier-B s1 is >= 2 TAU_B from every
+    (fp32) threshold -- the GPU's fp32 s1 is within TAU_B of s_hat1, so its comparisons agree."""
+    t = np.asarray(thresholds, dtype=np.float32).astype(np.float64)
+    o_lev = O.optimal_k_level(ob_s1, thresholds, usable)
+    dist = np.min(np.abs(ob_s1[:, None] - t[None, :]), axis=1) if len(t) else np.full(len(ob_s1), np.inf)
+    graded = ~usable | (dist >= 2 * TAU_B)
+    bad = graded & (gpu_level != o_lev)
+    assert not bad.any(), f"{int(bad.sum())} Tier-B-graded optimal-K levels differ, e.g. prompt {np.argwhere(bad)[0]}"
+    rep.levels_B += int(graded.sum())
+    rep.levels_checked += len(gpu_level)
+
+
 def tier_b_scores(P: np.ndarray, rows_of_ids: np.ndarray) -> np.ndarray:
     """s_hat(p, g) for the GPU's ids: rows_of_ids [n, k, d] fp32 cache rows (zeros for -1)."""
     Pq, _ = O.quantize(P)
@@ -96,6 +233,7 @@ def check_topk(gpu_ids, gpu_sc, o_ids, o_sc, rep: Report, P=None, gpu_rows=None)
     assert np.array_equal(np.isfinite(gpu_sc), ~sentinel), "sentinel positions differ"
     assert np.all(gpu_ids[sentinel] == -1)
     fin = ~sentinel
+    rep.positions += int(fin.sum())
     err = np.abs(gpu_sc[fin] - o_sc[:, :k][fin])
     if err.size:
         rep.max_score_err_A = max(rep.max_score_err_A, float(err.max()))

@@ -116,4 +116,7 @@ def test_solver_api_errors(pas):
         r.solve_assignment(65, 1.0, [0.5, 0.5], [1000, 1000], 4)      # W <= 64
     with pytest.raises(pas.PasError):
         r.solve_assignment(8, -1.0, [0.5, 0.5], [1000, 1000], 4)
+    with pytest.raises(pas.PasError) as ei:
+        r.solve_assignment(8, 1.0, [0.5, 0.6], [1000, 1000], 4)       # sum H != 1
+    assert ei.value.status == -1
     r.close()

@@ -69,3 +69,21 @@ def test_binding_fails_loudly_without_library(tmp_path):
     out = subprocess.run([sys.executable, "-c", code % (str(tmp_path / "missing.so"), ROOT)],
                          capture_output=True, text=True)
     assert "raised" in out.stdout, out.stdout + out.stderr
+
+
+def test_binding_rejects_bad_embedding_layouts(lib):
+    """the binding checks the rows K1 will read with vector loads -- width d, contiguous,
+    on the right side of the PCIe bus -- before any pointer crosses the ABI."""
+    import torch
+    fake = ctypes.c_void_p(12345)
+    lib._CTX_D[fake.value] = 768
+    try:
+        with pytest.raises(ValueError):
+            lib._rows(fake, torch.zeros(4, 512), device=False)           # wrong d
+        with pytest.raises(ValueError):
+            lib._rows(fake, torch.zeros(768, 4).t(), device=False)       # strided view
+        with pytest.raises(ValueError):
+            lib._rows(fake, torch.zeros(4, 768), device=True)            # host tensor on a device path
+        assert lib._rows(fake, torch.zeros(4, 768), device=False).value is not None
+    finally:
+        lib._CTX_D.pop(fake.value)

@@ -39,8 +39,6 @@ def parse():
     ap.add_argument("--cache", type=int, default=None, help="override M")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-rows", type=int, default=1 << 20)
-    ap.add_argument("--cpu-sample-prompts", type=int, default=32)
     ap.add_argument("--dispatcher", action="store_true",
                     help="route-and-batch through the f3 stateful dispatcher (queues carried across steps)")
     ap.add_argument("--forecast", type=int, default=0, metavar="W",
@@ -48,6 +46,9 @@ def parse():
                          "rebuilt every batch, i.i.d. Philox K' (0: the exact per-batch plan)")
     ap.add_argument("--force-collective", action="store_true",
                     help="use the NCCL all-gather path even with one rank (transport self-test)")
+    ap.add_argument("--collectives", default="folded", choices=["folded", "explicit"],
+                    help="G > 1: folded (N1 all-gather, every rank merges all N) or explicit (N1 + slice merge + "
+                         "N2 all-reduce of H_K + N3 all-gather), pas_set_collectives")
     return ap.parse_args()
 
 
@@ -149,42 +150,77 @@ def profiled_traffic(config: str, G: int):
 
 
 # ----------------------------------------------------------------------------------------------
-def cpu_baseline(cfg, w, N, M, P_host, n_prompts, n_rows, torch):
-    """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
-    n_prompts prompts against the first n_rows cache rows (Tier-A fp64 similarity + top-k +
-    optimal-K), plus the downstream O4..O10 on all N prompts.  Scaled to the full cache (the
-    similarity cost is linear in M) and expressed in prompts/s."""
-    import numpy as np
+ORACLE_PROMPTS = 32          # the one oracle sampling definition of both legs (cpu_baseline and --impl reference)
+ORACLE_ROWS = 1 << 20
 
-    from oracle import route as O
-    from synth import BLOCK
 
-    n_rows = min(n_rows, M)
-    idx = np.arange(min(n_prompts, N))
-    chunks = []
-    b = 0
-    while b * BLOCK < n_rows:
-        rows = w.cache_block(b)[: n_rows - b * BLOCK].cpu().numpy()
-        chunks.append((b * BLOCK, rows))
-        b += 1
-    threads = torch.get_num_threads()
-    t0 = time.perf_counter()
-    ids, sc, valid = O.topk_streaming(P_host[idx], iter(chunks), cfg.topk)
-    lev_s = O.optimal_k_level(sc[:, 0], cfg.thresholds, valid)
-    t_sim = time.perf_counter() - t0
-    rng = np.random.default_rng(0)
-    levels = rng.integers(0, len(cfg.grid), N)
-    levels[idx] = lev_s
-    setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
-                    bstar=cfg.bstar, mode=cfg.mode, topk=cfg.topk, seed=cfg.route_seed)
-    t1 = time.perf_counter()
-    O.downstream(levels, setup)
-    t_down = time.perf_counter() - t1
-    per_prompt = t_sim / len(idx) * (M / n_rows) + t_down / N
-    return {"value": 1.0 / per_prompt, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": (f"{len(idx)} prompts x first {n_rows:,} of {M:,} cache rows (fp64 Tier-A similarity, "
-                       f"full-sort top-{cfg.topk}, optimal-K; {t_sim:.1f} s, scaled x{M / n_rows:.2f} to the "
-                       f"full cache) + O4..O10 downstream on all {N:,} prompts ({t_down:.1f} s)"),
+class OracleSample:
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload: ORACLE_PROMPTS
+    prompts (a different slice each step) against the first ORACLE_ROWS cache rows -- Tier-A fp64
+    similarity, full-sort top-k, optimal-K (O1..O3) -- plus the downstream O4..O10 on all N prompts.
+    The similarity seconds are scaled to the full cache (linear in M) and per prompt; the downstream is
+    per prompt of the whole batch.  Used unchanged by the cpu_baseline leg and the reference arm, so the
+    two report the same quantity."""
+
+    def __init__(self, cfg, w, N, M, P_host):
+        import numpy as np
+
+        from synth import BLOCK
+        self.cfg, self.N, self.M, self.P = cfg, N, M, P_host
+        self.n_rows = min(ORACLE_ROWS, M)
+        self.n_p = min(ORACLE_PROMPTS, N)
+        self.chunks = []
+        b = 0
+        while b * BLOCK < self.n_rows:
+            self.chunks.append((b * BLOCK, w.cache_block(b)[: self.n_rows - b * BLOCK].cpu().numpy()))
+            b += 1
+        self.levels = np.random.default_rng(0).integers(0, len(cfg.grid), N)
+        self.i = 0
+
+    def step(self):
+        """One bounded sample; returns (seconds per prompt, similarity s, downstream s)."""
+        import numpy as np
+
+        from oracle import route as O
+        cfg = self.cfg
+        idx = (np.arange(self.n_p) + self.i * self.n_p) % self.N
+        self.i += 1
+        t0 = time.perf_counter()
+        ids, sc, valid = O.topk_streaming(self.P[idx], iter(self.chunks), cfg.topk)
+        lev = O.optimal_k_level(sc[:, 0], cfg.thresholds, valid)
+        t_sim = time.perf_counter() - t0
+        levels = self.levels.copy()
+        levels[idx] = lev
+        setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
+                        bstar=cfg.bstar, mode=cfg.mode, topk=cfg.topk, seed=cfg.route_seed)
+        t1 = time.perf_counter()
+        O.downstream(levels, setup)
+        t_down = time.perf_counter() - t1
+        return t_sim / self.n_p * (self.M / self.n_rows) + t_down / self.N, t_sim, t_down
+
+    def describe(self, t_sim, t_down):
+        return (f"per step: {self.n_p} prompts x first {self.n_rows:,} of {self.M:,} cache rows (fp64 Tier-A "
+                f"similarity, full-sort top-{self.cfg.topk}, optimal-K; {t_sim:.1f} s, scaled x{self.M / self.n_rows:.2f} "
+                f"to the full cache) + O4..O10 on all {self.N:,} prompts ({t_down:.1f} s)")
+
+
+def _threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or 1
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(cfg, w, N, M, P_host, steps: int = 2):
+    """The cpu_baseline leg: OracleSample, `steps` samples on rank 0, reported as prompts/s."""
+    smp = OracleSample(cfg, w, N, M, P_host)
+    per = [smp.step() for _ in range(steps)]
+    per_prompt = sum(p[0] for p in per) / len(per)
+    return {"value": 1.0 / per_prompt, "unit": UNIT, "cores": _threads(), "kind": "oracle",
+            "sample": smp.describe(per[-1][1], per[-1][2]) + f"; mean of {steps} steps",
+            "seconds": {"similarity": round(sum(p[1] for p in per) / len(per), 3),
+                        "downstream": round(sum(p[2] for p in per) / len(per), 3)},
             "cpu_model": _cpu_model()}
 
 
@@ -220,6 +256,8 @@ def main():
     dev = torch.device("cuda", local)
     dist = None
     if world > 1 or args.force_collective:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")           # the communicator's init log (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -236,6 +274,9 @@ def main():
                         rank=rank, world=G, nccl_id=nccl_id, seed=cfg.route_seed)
     router.set_bands(cfg.grid, cfg.thresholds)
     router.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
+    if nccl_id is not None:
+        pas.pas_set_collectives(router.ctx, pas.PAS_COLL_EXPLICIT if args.collectives == "explicit"
+                                else pas.PAS_COLL_FOLDED)
     gap_us = 0
     if args.forecast:
         router.set_forecast(args.forecast, 1)
@@ -278,38 +319,40 @@ def main():
         route_step()
     barrier()
 
+    # per-step events on the routing stream and the library's stage-timing ring: nothing in the timed
+    # loop waits on the device (no stats() / host sync between steps)
+    pas.pas_stage_ring(router.ctx, args.steps)
     clocks = ClockSampler(local)
     clocks.start()
     clocks.begin()
-    stage_sum = [0.0] * 8
     launches = 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    step_ms = []
+    s0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    s1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         if flush is not None:
             flush.fill_(1.0)
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
+        s0[i].record(stream)
         route_step()
+        s1[i].record(stream)
         launches += pas.pas_last_launch_count(router.ctx)
-        if flush is not None:
-            s1.record(stream)
-            s1.synchronize()
-            step_ms.append(s0.elapsed_time(s1))
-        st = router.stats()          # syncs on the step's last event; device stage times
-        for i in range(8):
-            stage_sum[i] += st["stage_ms"][i]
     ev1.record(stream)
     barrier()
     clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in zip(s0, s1)]
+    stages = pas.pas_stage_ring_read(router.ctx, args.steps)
+    pas.pas_stage_ring(router.ctx, 0)
+    stage_sum = [sum(r[i] for r in stages) for i in range(7)]
     total_ms = sum(step_ms) if flush is not None else ev0.elapsed_time(ev1)
     total_ms = max_over_ranks(total_ms, dist, dev, torch)
-    k2_ms = max_over_ranks(stage_sum[1] / args.steps, dist, dev, torch)
+    k2_ms = max_over_ranks(stage_sum[1] / len(stages), dist, dev, torch)
     value = N * args.steps / (total_ms / 1e3)
+    q = statistics.quantiles(step_ms, n=10) if len(step_ms) >= 2 else [step_ms[0]] * 9
+    step_stats = {"median": statistics.median(step_ms), "p10": q[0], "p90": q[-1], "min": min(step_ms),
+                  "max": max(step_ms), "note": "device time per pas_route_batch (CUDA events, this rank)"}
 
     # ---- e2e through the host-buffer entry point (H2D of the prompts, D2H of every output)
     e2e = None
@@ -349,14 +392,18 @@ def main():
                    "instances": len(cfg.instance_level), "mode": "uniform" if cfg.mode else "greedy",
                    "bstar": cfg.bstar, "dispatcher": "stateful (f3)" if args.dispatcher else "stateless (R13)",
                    "plan": f"forecast (f1, window {args.forecast})" if args.forecast else "exact per batch",
-                   "parallelism": f"cache row-sharded x{G}" + (" + NCCL all-gather" if G > 1 else ""),
+                   "parallelism": f"cache row-sharded x{G}" + ((" + NCCL all-gather" if args.collectives == "folded" else
+                                                                   " + NCCL all-gather / all-reduce H_K / all-gather (explicit N2)")
+                                                                  if G > 1 else ""),
                    "l2": l2_note},
         "roofline": {"kernel": "k_simtopk (K2: tcgen05 similarity GEMM + fused top-k)", "bound": "tensor",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": f"{peak_kind}, {peak_src}",
                      "algorithmic": f"2*N*M_per_gpu*d = {flops:.4g} flop per launch / mean K2 event time "
                                     f"{k2_ms:.3f} ms"},
-        "stages_ms": {n: round(stage_sum[i] / args.steps, 4) for i, n in enumerate(
+        "step_ms": step_stats,
+        "value_median": N / (step_stats["median"] / 1e3),
+        "stages_ms": {n: round(stage_sum[i] / len(stages), 4) for i, n in enumerate(
             ["normalise", "similarity_topk", "merge_collective_optimalK", "plan", "redirect", "route_and_batch",
              "total"])},
         "e2e": e2e,
@@ -365,9 +412,7 @@ def main():
         "setup": {"cache_load_s": round(t_load, 2)},
     }
     if rank == 0 and not args.no_cpu_baseline:
-        import numpy as np  # noqa: F401
-        line["cpu_baseline"] = cpu_baseline(cfg, w, N, M, P.cpu().numpy(), args.cpu_sample_prompts,
-                                            args.cpu_sample_rows, torch)
+        line["cpu_baseline"] = cpu_baseline(cfg, w, N, M, P.cpu().numpy())
     if rank == 0:
         print(json.dumps(line), flush=True)
     router.close()
@@ -382,57 +427,32 @@ def max_over_ranks(x, dist, dev, torch):
 
 
 def reference_arm(args, cfg, N, M, rank, world):
-    """The CPU oracle as it stands, timed on this host's cores on bounded samples of the workload."""
+    """The CPU oracle as it stands, timed on this host's cores: each step is one OracleSample (the same
+    bounded sample definition as the cpu_baseline leg), W warm-up steps, then K timed steps."""
     if rank != 0:
         return
-    import numpy as np
     import torch
 
-    from oracle import route as O
-    from synth import BLOCK, Workload
+    from synth import Workload
 
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     w = Workload(cfg, device=dev, M=M)
-    n_rows = min(M, 1 << 19)
-    n_p = 8
-    P = w.prompts(N).cpu().numpy()
-    chunks = []
-    b = 0
-    while b * BLOCK < n_rows:
-        chunks.append((b * BLOCK, w.cache_block(b)[: n_rows - b * BLOCK].cpu().numpy()))
-        b += 1
-    setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=cfg.F, instance_level=cfg.instance_level,
-                    bstar=cfg.bstar, mode=cfg.mode, topk=cfg.topk, seed=cfg.route_seed)
-    rng = np.random.default_rng(1)
-
-    def step(i):
-        idx = (np.arange(n_p) + i * n_p) % N
-        t0 = time.perf_counter()
-        ids, sc, valid = O.topk_streaming(P[idx], iter(chunks), cfg.topk)
-        lev = O.optimal_k_level(sc[:, 0], cfg.thresholds, valid)
-        t_sim = time.perf_counter() - t0
-        levels = rng.integers(0, len(cfg.grid), min(N, 4096))
-        levels[:n_p] = lev
-        t1 = time.perf_counter()
-        O.downstream(levels, setup)
-        t_down = time.perf_counter() - t1
-        return t_sim / n_p * (M / n_rows) + t_down / len(levels)
-
-    for i in range(args.warmup):
-        step(i)
-    per = [step(args.warmup + i) for i in range(args.steps)]
-    per_prompt = sum(per) / len(per)
+    smp = OracleSample(cfg, w, N, M, w.prompts(N).cpu().numpy())
+    for _ in range(args.warmup):
+        smp.step()
+    per = [smp.step() for _ in range(args.steps)]
+    per_prompt = sum(p[0] for p in per) / len(per)
     value = 1.0 / per_prompt
-    threads = torch.get_num_threads()
-    sample = (f"per step: {n_p} prompts x first {n_rows:,} of {M:,} cache rows (fp64 similarity, full-sort "
-              f"top-{cfg.topk}, optimal-K) scaled x{M / n_rows:.1f} to the full cache, + O4..O10 on 4,096 prompts")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_prompt * N * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth-v1)",
             "config": {"workload": f"{args.config}: {N:,} prompts vs {M:,}-entry cache ({cfg.note})", "N": N,
                        "M": M},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": _threads(), "kind": "oracle",
+                             "sample": smp.describe(per[-1][1], per[-1][2]) + f"; mean of {args.steps} steps",
+                             "seconds": {"similarity": round(sum(p[1] for p in per) / len(per), 3),
+                                         "downstream": round(sum(p[2] for p in per) / len(per), 3)},
                              "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

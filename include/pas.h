@@ -45,7 +45,7 @@ typedef enum {
   PAS_ERR_FRACTIONS = -3,    /* F(K) invalid (F >= 0, sum F = 1 +- 1e-9) */
   PAS_ERR_NO_INSTANCE = -4,  /* F_j > 0 but no serving instance at level j */
   PAS_ERR_BANDS = -5,        /* K grid / thresholds invalid */
-  PAS_ERR_DEGRADATION = -6,  /* c(dK) not c[0]=0, non-decreasing, convex (R6) */
+  PAS_ERR_DEGRADATION = -6,  /* c(dK) not c[0]=0, finite, non-decreasing; non-convex c > 1 (R6, R37) */
   PAS_ERR_CAPACITY = -7,     /* store or batch capacity exceeded */
   PAS_ERR_CUDA = -8,
   PAS_ERR_NCCL = -9,
@@ -68,7 +68,7 @@ typedef enum { PAS_GREEDY = 0, PAS_UNIFORM = 1 } pas_mode;  /* P:104 high / low 
 /* Flags per prompt (pas_route_out.flags), informational; the oracle grades with its own. */
 #define PAS_FLAG_INVALID 1        /* non-finite or zero-norm embedding -> treated as cold (R16) */
 #define PAS_FLAG_COLD 2           /* empty cache -> K = 0 */
-#define PAS_FLAG_NEAR_TOP1 4      /* GPU s1 - s2 < 2e-2 (north_star near-tie margin) */
+#define PAS_FLAG_NEAR_TOP1 4      /* GPU s1 - s2 < 2e-2 (north_star near-tie margin); needs topk >= 2 */
 #define PAS_FLAG_NEAR_THRESHOLD 8 /* GPU |s1 - t_m| < 2e-2 for some threshold t_m */
 
 typedef struct {
@@ -109,7 +109,10 @@ typedef struct {
   int64_t f[PAS_MAX_LEVELS];                    /* integer targets from F (R3) */
   int64_t x[PAS_MAX_LEVELS][PAS_MAX_LEVELS];    /* route plan: x[i][j] prompts with optimal level i served at j */
   double D_Q;                                   /* Eq. 1 on the integer plan, sum_{K_j>K_i} x_ij D_ij / N */
-  double D_Q_LP;                                /* Eq. 1 optimum on unrounded (h/N, F), context only */
+  double D_Q_LP;                                /* Eq. 1 optimum on unrounded (h/N, F), context only (NaN:
+                                                   non-convex c) */
+  int plan_solver_iters;                        /* non-convex c: solver augmentations (-1: iteration cap hit,
+                                                   the plan is feasible but not canonical); 0 otherwise */
   int64_t n_redirected, n_upgraded, n_downgraded;   /* K'!=K, K'<K (slower/better), K'>K */
   int64_t n_invalid, n_near_top1, n_near_threshold;
   int64_t bucket_count[PAS_MAX_INSTANCES];      /* prompts per instance */
@@ -209,8 +212,16 @@ pas_status pas_cache_size(const pas_ctx* ctx, int64_t* global_rows, int64_t* loc
  * Invalidates previously set fractions.  Errors: PAS_ERR_BANDS. */
 pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const float* thresholds);
 
-/* Degradation c(dK) for dK = 0..len-1 (Eq. 1's D(K',K) = c(K'-K) for K' > K, 0 otherwise; R5, R6).
- * len must be PAS_T_TOTAL.  c[0] == 0, non-decreasing, convex (second differences >= -1e-12).
+/* Degradation c(dK) for dK = 0..len-1 (Eq. 1's D(K',K) = c(K'-K) for K' > K, 0 otherwise; P:89 leaves
+ * D's form open; R5, R6).  len must be PAS_T_TOTAL; c[0] == 0, finite, non-decreasing.
+ *   - convex c (second differences >= -1e-12 (1 + |c|)): the route plan (a6) is the NW-corner
+ *     coupling, the exact optimum under R7 (ties within 1e-9 relative -> min sum x dK^2);
+ *   - any other c (NEXT f4, R37) must stay in [0, 1] (a quality loss): it is held as integers
+ *     cI = round-half-even(c * 2^24) and the plan is the exact optimum of the integer transportation
+ *     problem under (sum x cI, sum x dK^2) lexicographically, and among those the lexicographically
+ *     greatest x in row-major order (one CTA, min-cost flow; pas_stats.plan_solver_iters).  D_Q is
+ *     still Eq. 1 in fp64 on the real c; D_Q_LP is NaN (not computed).  Not with the forecast mode
+ *     (its coupling plan is the optimum only for convex c).
  * Errors: PAS_ERR_DEGRADATION. */
 pas_status pas_set_degradation(pas_ctx* ctx, const double* c_of_dK, int len);
 
@@ -295,6 +306,18 @@ typedef struct {
 pas_status pas_solve_assignment(pas_ctx* ctx, int W, double lambda_rps, const double* H, const int64_t* service_us,
                                 int bstar, pas_assignment* out);
 
+/* How pas_route_batch combines the ranks when world > 1:
+ *   PAS_COLL_FOLDED (default): N1 ncclAllGather of every rank's [N x k] candidates, then every rank
+ *     merges all N prompts and builds the full H_K itself -- the north_star's all-reduce of H_K is
+ *     folded into the redundant merge (one collective per batch);
+ *   PAS_COLL_EXPLICIT: N1, then each rank merges only its slice of ceil(N / G) prompts, N2
+ *     ncclAllReduce of the slice H_K (+ flag counters), N3 ncclAllGather of the slice results (top-k,
+ *     K, level, flags) in one NCCL group, then the same redundant K5..K7.
+ * Outputs are byte-identical either way (R18, R19).  Errors: PAS_ERR_ARG. */
+#define PAS_COLL_FOLDED 0
+#define PAS_COLL_EXPLICIT 1
+pas_status pas_set_collectives(pas_ctx* ctx, int mode);
+
 /* Reset the Philox key and the batch sequence number (R18). */
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
 
@@ -330,6 +353,16 @@ pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, 
 /* Plan and counters of the last routed batch (host struct).  Synchronises the context's last stream. */
 pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out);
 
+/* Stage-timing ring (bench.py): with slots > 0 every routed batch also records its 7 stage boundaries
+ * into slot (batch index % slots), so per-batch device times of many back-to-back batches can be read
+ * after the fact without a host sync per batch.  slots == 0 turns it off.  Synchronises the device.
+ * pas_stage_ring_read: the last min(n, batches recorded, slots) batches, oldest first, as rows of 7
+ * floats (ms): stages [0..5] as pas_stats.stage_ms, [6] total; *n_out receives the row count.
+ * Synchronises on those batches.  Errors: PAS_ERR_ARG. */
+#define PAS_MAX_RING 4096
+pas_status pas_stage_ring(pas_ctx* ctx, int slots);
+pas_status pas_stage_ring_read(pas_ctx* ctx, int n, float* ms, int* n_out);
+
 /* Last error message of this context ("" if none).  ctx may be NULL (global errors, e.g. create). */
 const char* pas_last_error(const pas_ctx* ctx);
 
@@ -343,6 +376,14 @@ int pas_last_launch_count(const pas_ctx* ctx);
  * element-wise parity test on small inputs only. */
 pas_status pas_debug_scores(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N, float* scores_dev,
                             pas_stream stream);
+
+/* The bf16 rows K1 produced (a1 / a2, R11), for bit-exact checks against the oracle's quantisation:
+ * pas_debug_qhat copies the first N rows of the prompt-side Q_hat written by the last pas_route_batch /
+ * pas_route_local (device [N x d] bf16, out_dev caller-owned); pas_debug_store_rows copies this rank's
+ * store rows [first_local_row, first_local_row + n) (local row r holds gid r * world + rank).
+ * Stream-ordered copies.  Errors: PAS_ERR_ARG (range), PAS_ERR_STATE (no prompt normalised yet). */
+pas_status pas_debug_qhat(pas_ctx* ctx, void* out_dev, int64_t N, pas_stream stream);
+pas_status pas_debug_store_rows(pas_ctx* ctx, int64_t first_local_row, int64_t n, void* out_dev, pas_stream stream);
 
 /* The K2 work schedule a batch of N prompts against M_local rows of width d would get in a context of
  * max_batch prompts (host logic only, no device; DESIGN.md 8 "K2 schedule").  out[8] receives:

@@ -334,6 +334,113 @@ def plan_lp(h, f, grid, c):
     return x
 
 
+# ----------------------------------------------------------------------------------------------
+# O6' Eq. 1 for an arbitrary (non-convex) degradation table (R37; NEXT f4)
+# ----------------------------------------------------------------------------------------------
+DEG_SHIFT = 24   # R37: non-convex c is held as integers cI = round-half-even(c * 2^24)
+
+
+def is_convex(c) -> bool:
+    """R6: second differences >= -1e-12 (1 + |c_t|) -- the tables the NW-corner plan is exact for."""
+    c = [float(v) for v in c]
+    return all(c[t + 1] - 2 * c[t] + c[t - 1] >= -1e-12 * (1.0 + abs(c[t])) for t in range(1, len(c) - 1))
+
+
+def degradation_int(c) -> np.ndarray:
+    """cI = round-half-even(c * 2^24) (exact: scaling a double by 2^24 is exact, np.rint ties to even)."""
+    return np.rint(np.ldexp(np.asarray(c, dtype=np.float64), DEG_SHIFT)).astype(np.int64)
+
+
+def _cost_pairs(grid, cI):
+    nK = len(grid)
+    D = [[int(cI[grid[j] - grid[i]]) if grid[j] > grid[i] else 0 for j in range(nK)] for i in range(nK)]
+    Q = [[(grid[j] - grid[i]) ** 2 for j in range(nK)] for i in range(nK)]
+    return D, Q
+
+
+def plan_int_bruteforce(h, f, grid, cI):
+    """R37 by exhaustive search (tiny N, nK <= 4): min over all integer plans of the exact integer pair
+    (sum x cI, sum x dK^2), then the lexicographically greatest x in row-major order.
+    Returns (x, number of plans sharing the optimal pair)."""
+    nK = len(grid)
+    D, Q = _cost_pairs(grid, cI)
+    best, best_key, ties = None, None, 0
+    for x in _plans([int(v) for v in h], [int(v) for v in f]):
+        d = sum(x[i][j] * D[i][j] for i in range(nK) for j in range(nK))
+        q = sum(x[i][j] * Q[i][j] for i in range(nK) for j in range(nK))
+        flat = [v for row in x for v in row]
+        key = (d, q)
+        if best is None or key < best_key:
+            best, best_key, ties = flat, key, 1
+        elif key == best_key:
+            ties += 1
+            if flat > best:
+                best = flat
+    return np.array(best, dtype=np.int64).reshape(nK, nK), ties
+
+
+def plan_int_lp(h, f, grid, cI):
+    """R37 by phased HiGHS LPs on the transportation polytope (integral vertices: total unimodularity).
+    Phase 1 min sum x cI; phase 2 min sum x dK^2 over the phase-1 optimal face; phase 3 raises
+    x_00, x_01, ... in row-major order, each to its maximum on the face with the earlier cells fixed.
+    The optimal face of a phase is {x feasible : x_ij = 0 where the phase's reduced cost is > 0}
+    (complementary slackness with an optimal dual; with integer data the reduced costs are integers,
+    so > 0.5 decides).  Every objective coefficient is a small integer: no big-M, no D <= D* row."""
+    from scipy.optimize import linprog
+
+    nK = len(grid)
+    h = [int(v) for v in h]
+    f = [int(v) for v in f]
+    A_eq = np.zeros((2 * nK, nK * nK))
+    for i in range(nK):
+        A_eq[i, i * nK:(i + 1) * nK] = 1
+    for j in range(nK):
+        A_eq[nK + j, j::nK] = 1
+    b_eq = np.array(h + f, dtype=np.float64)
+    D, Q = _cost_pairs(grid, cI)
+    ub = [None] * (nK * nK)
+
+    def solve(cost):
+        r = linprog(np.asarray(cost, dtype=np.float64), A_eq=A_eq, b_eq=b_eq,
+                    bounds=[(0, u) for u in ub], method="highs")
+        if r.status != 0:
+            raise RuntimeError(f"LP failed: {r.message}")
+        return r
+
+    for cost in ([v for row in D for v in row], [v for row in Q for v in row]):
+        r = solve(cost)
+        rc = r.lower.marginals           # reduced costs of x >= 0
+        for e in range(nK * nK):
+            if rc[e] > 0.5:
+                ub[e] = 0.0
+    lo = [0.0] * (nK * nK)
+    for e in range(nK * nK):
+        if ub[e] == 0.0:
+            continue
+        obj = np.zeros(nK * nK)
+        obj[e] = -1.0
+        r = linprog(obj, A_eq=A_eq, b_eq=b_eq, bounds=list(zip(lo, ub)), method="highs")
+        if r.status != 0:
+            raise RuntimeError(f"phase-3 LP failed: {r.message}")
+        v = float(np.rint(-r.fun))
+        if abs(-r.fun - v) > 1e-6:
+            raise RuntimeError("phase-3 optimum not integral")
+        lo[e] = v
+        ub[e] = v
+    x = np.array([int(v) for v in lo], dtype=np.int64).reshape(nK, nK)
+    if not (np.array_equal(x.sum(axis=1), h) and np.array_equal(x.sum(axis=0), f)):
+        raise RuntimeError("plan violates the marginals")
+    return x
+
+
+def plan_for(h, f, grid, c, solver: str = "lp"):
+    """The plan the hot path must produce for table c: R7 (convex c) or R37 (any other table)."""
+    if is_convex(c):
+        return plan_bruteforce(h, f, grid, c)[0] if solver == "brute" else plan_lp(h, f, grid, c)
+    cI = degradation_int(c)
+    return plan_int_bruteforce(h, f, grid, cI)[0] if solver == "brute" else plan_int_lp(h, f, grid, cI)
+
+
 def dq_linear_closed_form(h, f, grid, alpha: float, N: int) -> float:
     """For D = alpha * dK (linear), D*/N = alpha * sum_t (K_{t+1}-K_t) max(0, CDF_h(t) - CDF_f(t)) / N:
     every prompt whose level is <= t but is served above t crosses the gap (K_t, K_{t+1})."""
@@ -504,10 +611,8 @@ def downstream(level: np.ndarray, s: Setup, solver: str = "lp"):
     f = apportion(s.F, N)
     if N == 0:
         x = np.zeros((nK, nK), dtype=np.int64)
-    elif solver == "brute":
-        x, _ = plan_bruteforce(h, f, s.grid, s.c)
     else:
-        x = plan_lp(h, f, s.grid, s.c)
+        x = plan_for(h, f, s.grid, s.c, solver)
     DQ = d_q(x, s.grid, s.c, N)
     kp, rank = redirect(level, x, s.seed, s.batch_seq) if N else (np.zeros(0, np.int64),) * 2
     inst, slot = route_and_batch(kp, s.instance_level, s.bstar, s.mode, s.seed, s.batch_seq)

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restr
       if (lane == 0)
         for (int i = 0; i < k; ++i) res[w][i] = Cand{-INFINITY, -1};
     } else {
-      merge_prompt(in, S, P.N, k, p, res[w], lane);
+      merge_prompt(in, S, P.cand_stride ? P.cand_stride : P.N, k, p, res[w], lane);
     }
     __syncwarp();
     for (int i = lane; i < k; i += 32) {
@@ -209,13 +209,14 @@ __global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __r
   ty.zero();
   const int k = P.topk;
   const bool cold = (P.M_total == 0);
+  const int64_t stride = P.cand_stride ? P.cand_stride : P.N;
   const int64_t ntiles = (P.N + TP_THREADS - 1) / TP_THREADS;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {   // persistent over tiles
     const int64_t p0 = tile * TP_THREADS;
     const int np = (int)min((int64_t)TP_THREADS, P.N - p0);
     __syncthreads();   // previous tile's output copy finished reading the staging buffer
     for (int s = 0; s < S; ++s) {   // coalesced global reads into rows padded to k+1 pairs
-      const Cand* src = in + ((int64_t)s * P.N + p0) * k;
+      const Cand* src = in + ((int64_t)s * stride + p0) * k;
       Cand* dst = sm + s * TP_THREADS * kp;
       for (int i = threadIdx.x; i < np * k; i += TP_THREADS) dst[(i / k) * kp + i % k] = src[i];
     }
@@ -328,6 +329,33 @@ __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict
   flush_tally(P, o, ty);
 }
 
+// Explicit-N2 unpack: thread per (prompt, candidate pair); the prompt's first thread copies K / level /
+// flags and stamps its top-1.
+__global__ void __launch_bounds__(256) k_unpack_slices(const Cand* __restrict__ all_cand,
+                                                       const int32_t* __restrict__ all_K,
+                                                       const uint8_t* __restrict__ all_level,
+                                                       const uint8_t* __restrict__ all_flags, const RouteParams P,
+                                                       SelectOut o) {
+  pdl_entry();
+  const int k = P.topk;
+  const int64_t total = P.N * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const Cand c = all_cand[e];
+    if (o.topk_id) o.topk_id[e] = c.g;
+    if (o.topk_score) o.topk_score[e] = c.s;
+    const int64_t p = e / k;
+    if (e == p * k) {
+      const uint8_t fl = all_flags[p];
+      o.K[p] = all_K[p];
+      o.level[p] = all_level[p];
+      if (o.flags) o.flags[p] = fl;
+      if (P.lru_stamp && !(fl & (PAS_FLAG_INVALID | PAS_FLAG_COLD)) && c.g >= 0 && c.g < P.M_total)
+        P.lru_stamp[c.g] = P.lru_tick;
+    }
+  }
+}
+
 __global__ void k_fill_sentinel(Cand* out, int64_t n) {
   pdl_entry();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -378,6 +406,16 @@ cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, co
     const int64_t blocks = (p.N + WARPS - 1) / WARPS;
     launch_pdl(k_merge_select, (unsigned)blocks, WARPS * 32, 0, st, in, S, pflags, p, o);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_slices(const Cand* all_cand, const int32_t* all_K, const uint8_t* all_level,
+                                 const uint8_t* all_flags, const RouteParams& p, const SelectOut& o,
+                                 cudaStream_t st) {
+  if (p.N <= 0) return cudaSuccess;
+  int64_t blocks = (p.N * p.topk + 255) / 256;
+  if (blocks > (int64_t)kNumSMs * 8) blocks = (int64_t)kNumSMs * 8;
+  launch_pdl(k_unpack_slices, (unsigned)blocks, 256, 0, st, all_cand, all_K, all_level, all_flags, p, o);
   return cudaGetLastError();
 }
 

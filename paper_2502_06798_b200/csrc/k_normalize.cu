@@ -35,12 +35,15 @@ __device__ __forceinline__ void load4(const __nv_bfloat16* p, float (&v)[4]) {
 // fp32_RN(v / norm) without a per-element fp64 division: q = v * RN(1 / norm) is within 2 ulp (fp64)
 // of v / norm, so fp32_RN(q) == fp32_RN(v / norm) unless v / norm lies within a few fp64 ulp of an
 // fp32 rounding midpoint -- recognisable from the 29 bits of q below the fp32 mantissa being
-// ~0x10000000 -- in which case (probability ~2^-25) the exact fp64 division decides.  One DMUL per
-// element instead of a division sequence keeps K1 off the fp64 pipe's limit and on the HBM roofline.
+// ~0x10000000 -- in which case (probability ~2^-25) the exact fp64 division decides.  Below 2^-126 the
+// fp32 result is subnormal and rounds at a higher bit than those 29, so there the division always
+// decides (a component < 2^-126 of its row's norm: never in real embeddings; the adversarial rows of
+// tests/test_gpu_k1_exact.py put quotients exactly on subnormal midpoints).  One DMUL per element
+// instead of a division sequence keeps K1 off the fp64 pipe's limit and on the HBM roofline.
 __device__ __forceinline__ float div_rn(float v, double norm, double inv) {
   const double q = (double)v * inv;
   const long long low = __double_as_longlong(q) & 0x1FFFFFFFLL;
-  if (llabs(low - 0x10000000LL) <= 16) return __double2float_rn((double)v / norm);
+  if (llabs(low - 0x10000000LL) <= 16 || fabs(q) < 0x1p-126) return __double2float_rn((double)v / norm);
   return __double2float_rn(q);
 }
 

@@ -10,6 +10,7 @@
 #include <climits>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "pas_internal.cuh"
 
@@ -25,6 +26,9 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -38,10 +42,14 @@ bool nccl_load() {
   g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(h, "ncclCommAbort");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.CommDestroy &&
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllGather && g_nccl.AllReduce &&
+              g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.CommDestroy &&
               g_nccl.CommAbort && g_nccl.GetErrorString;
   return g_nccl.ok;
 }
@@ -87,6 +95,8 @@ struct pas_ctx {
   float thr[kMaxLevels]{};
   double F[kMaxLevels]{};
   double c[kTTotal]{};
+  bool c_convex = true;        // R6: NW-corner plan; false: the exact integer solver (R37)
+  int64_t cI[kTTotal]{};       // R37: round-half-even(c * 2^24)
   int inst_level[kMaxInst]{};
   uint64_t seed = 0, batch_seq = 0;
   int64_t M_total = 0, M_local = 0, cap_rows = 0, q_rows = 0, cand_cap = 0;
@@ -149,9 +159,17 @@ struct pas_ctx {
   CUtensorMap tm_q{}, tm_c{}, tm_c2{};
   // comm
   ncclComm_t comm = nullptr;
+  int coll_mode = PAS_COLL_FOLDED;   // explicit: slice merge + N2 all-reduce of H_K + N3 all-gather
+  Cand* x_cand = nullptr;            // explicit mode: [G * Ns][k] gathered slice results (prompt order)
+  int32_t* x_K = nullptr;
+  uint8_t *x_level = nullptr, *x_flags = nullptr;
   // timing
   cudaEvent_t ev[8]{};
   cudaEvent_t ev_aux = nullptr;   // end event of pas_solve_assignment's timing
+  // stage-timing ring (pas_stage_ring): the 7 stage boundaries of each of the last ring_n batches
+  std::vector<cudaEvent_t> ring;
+  int ring_n = 0;
+  int64_t ring_pos = 0, ring_count = 0;
   bool ev_valid = false;
   cudaStream_t last_stream = nullptr;
 };
@@ -200,6 +218,13 @@ int64_t local_rows_below(int64_t total, int G, int rank) {
   return total > rank ? (total - rank + G - 1) / G : 0;
 }
 
+// Record stage boundary i (0..6) of the current batch: ev[i], and its slot of the timing ring.
+cudaError_t rec_stage(pas_ctx* ctx, int i, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(ctx->ev[i], st);
+  if (e == cudaSuccess && ctx->ring_n > 0) e = cudaEventRecord(ctx->ring[(ctx->ring_pos % ctx->ring_n) * 7 + i], st);
+  return e;
+}
+
 pas_status check_live(pas_ctx* ctx) {
   if (!ctx) return fail(nullptr, PAS_ERR_ARG, "null context");
   if (ctx->poisoned) return fail(ctx, PAS_ERR_STATE, "context poisoned by an earlier CUDA/NCCL error: %s",
@@ -231,6 +256,8 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
     p.F[i] = ctx->F[i];
   }
   for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
+  p.convex = ctx->c_convex ? 1 : 0;
+  for (int t = 0; t < kTTotal; ++t) p.cI[t] = ctx->cI[t];
   for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
   p.lru_stamp = ctx->stamps;
   p.lru_tick = ctx->lru_tick;
@@ -336,7 +363,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   if (pas_status s = ensure_prompt_ws(ctx)) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   ctx->launches++;
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 1, st));
   int R = 1;
   if (ctx->M_local > 0) {
     DynSched dyn;
@@ -361,7 +388,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
     CUDA_TRY(ctx, launch_fill_sentinel(ctx->cand_local, N * k, st));
   }
   ctx->launches++;
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 2, st));
   *cand = ctx->cand_local;
   *S = R;
   if (merged) {
@@ -373,6 +400,8 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
   ctx->last_local_N = N;
   return PAS_OK;
 }
+
+pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_route_out* out, cudaStream_t st);
 
 // a4 (final merge) .. a8 for all N prompts from S candidate blocks [S][N][k].
 pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
@@ -389,7 +418,68 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   ctx->last_local_N = -1;
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[3], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 3, st));
+  return run_downstream(ctx, p, N, out, st);
+}
+
+// The explicit form of SURVEY 8(e) (pas_set_collectives(PAS_COLL_EXPLICIT)): from the all-gathered
+// [G][N][k] candidates each rank merges only its prompt slice [r Ns, r Ns + n_r) (Ns = ceil(N / G)),
+// N2 all-reduces the slice H_K (and the flag counters) -- "an all-reduce of H_K precedes the route
+// plan" (north_star) -- and N3 all-gathers the slice results (top-k, K, level, flags; one NCCL group),
+// which every rank unpacks (stamping the top-1s, R26) before the redundant, deterministic K5..K7.
+pas_status run_global_explicit(pas_ctx* ctx, const Cand* cand_all, int64_t N, const pas_route_out* out,
+                               cudaStream_t st) {
+  const int G = ctx->cfg.world, r = ctx->cfg.rank, k = ctx->cfg.topk;
+  const int64_t Ns = (N + G - 1) / G, lo = (int64_t)r * Ns;
+  const int64_t n_r = N - lo < 0 ? 0 : (N - lo < Ns ? N - lo : Ns);
+  if (!ctx->x_cand) {
+    const int64_t cap = ((ctx->cfg.max_batch + G - 1) / G) * G;
+    cudaError_t e = dmalloc(&ctx->x_cand, (size_t)(cap * k));
+    if (e == cudaSuccess) e = dmalloc(&ctx->x_K, (size_t)cap);
+    if (e == cudaSuccess) e = dmalloc(&ctx->x_level, (size_t)cap);
+    if (e == cudaSuccess) e = dmalloc(&ctx->x_flags, (size_t)cap);
+    if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "explicit-collective workspace: %s", cudaGetErrorString(e));
+  }
+  ctx->lru_tick++;   // f2 clock (R26)
+  RouteParams p = make_params(ctx, N);
+  CUDA_TRY(ctx, launch_zero(ctx->hist, kMaxLevels, reinterpret_cast<int32_t*>(ctx->plan), sizeof(DevPlan) / 4,
+                            nullptr, 0, st));
+  ctx->launches++;
+  const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;
+  ctx->last_local_N = -1;
+  if (n_r > 0) {   // slice merge + select straight into this rank's segment of the gather buffers
+    RouteParams ps = p;
+    ps.N = n_r;
+    ps.cand_stride = N;
+    ps.lru_stamp = nullptr;   // stamped for all N after the gather
+    SelectOut so{ctx->x_K + lo, nullptr, nullptr, ctx->x_flags + lo, ctx->x_level + lo, ctx->x_cand + lo * k,
+                 ctx->hist, ctx->plan};
+    CUDA_TRY(ctx, launch_merge_select(cand_all + lo * k, G, pflags ? pflags + lo : nullptr, ps, so, st));
+    ctx->launches++;
+  }
+  ncclResult_t nr = g_nccl.GroupStart();
+  if (nr == ncclSuccess)   // N2: H_K and the three flag counters (contiguous in DevPlan)
+    nr = g_nccl.AllReduce(ctx->hist, ctx->hist, (size_t)ctx->nK, ncclInt32, ncclSum, ctx->comm, st);
+  if (nr == ncclSuccess)
+    nr = g_nccl.AllReduce(&ctx->plan->n_invalid, &ctx->plan->n_invalid, 3, ncclInt32, ncclSum, ctx->comm, st);
+  // N3 (in place: rank r's segment already sits at r * Ns)
+  if (nr == ncclSuccess)
+    nr = g_nccl.AllGather(ctx->x_cand + lo * k, ctx->x_cand, (size_t)Ns * k * 2, ncclInt32, ctx->comm, st);
+  if (nr == ncclSuccess) nr = g_nccl.AllGather(ctx->x_K + lo, ctx->x_K, (size_t)Ns, ncclInt32, ctx->comm, st);
+  if (nr == ncclSuccess) nr = g_nccl.AllGather(ctx->x_level + lo, ctx->x_level, (size_t)Ns, ncclUint8, ctx->comm, st);
+  if (nr == ncclSuccess) nr = g_nccl.AllGather(ctx->x_flags + lo, ctx->x_flags, (size_t)Ns, ncclUint8, ctx->comm, st);
+  const ncclResult_t ne = g_nccl.GroupEnd();
+  if (nr != ncclSuccess || ne != ncclSuccess)
+    return fail(ctx, PAS_ERR_NCCL, "explicit collectives: %s", g_nccl.GetErrorString(nr != ncclSuccess ? nr : ne));
+  SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
+  CUDA_TRY(ctx, launch_unpack_slices(ctx->x_cand, ctx->x_K, ctx->x_level, ctx->x_flags, p, so, st));
+  ctx->launches++;
+  CUDA_TRY(ctx, rec_stage(ctx, 3, st));
+  return run_downstream(ctx, p, N, out, st);
+}
+
+// a6 .. a8 (plan, redirection, route-and-batch) after the merge stage has written level / hist / plan.
+pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_route_out* out, cudaStream_t st) {
   if (ctx->fc_window > 0) {
     // f1: plan from the forecast (held between rebuilds, R24), i.i.d. K' (R23), window update (R21)
     bool replan = !ctx->fc_planned || ctx->fc_tick % ctx->fc_replan_every == 0;
@@ -400,7 +490,7 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
     }
     ctx->fc_tick++;
     CUDA_TRY(ctx, launch_fc_plan(ctx->hist, p, ctx->plan, ctx->fc_state, replan, st));
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(ctx, rec_stage(ctx, 4, st));
     CUDA_TRY(ctx, launch_fc_sample(ctx->level, p, ctx->plan, ctx->fc_state, out->K_prime, ctx->rw.cls7, st));
     CUDA_TRY(ctx, launch_fc_window(ctx->level, p, ctx->plan, ctx->fc_state, ctx->fc_ring, ctx->fc_window, st));
     ctx->launches += 3;
@@ -408,18 +498,22 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   } else {
     CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
     ctx->launches++;
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(ctx, rec_stage(ctx, 4, st));
     CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, st, &ctx->launches));
     ctx->fc_stats_valid = false;
   }
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[5], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 5, st));
   CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, ctx->bw, out->instance, out->slot,
                                        out->bucket_offsets, out->bucket_prompts, st, &ctx->launches));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[6], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 6, st));
   ctx->ev_valid = true;
   ctx->last_stream = st;
   ctx->last_N = N;
   ctx->batch_seq++;
+  if (ctx->ring_n > 0) {
+    ctx->ring_pos++;
+    ctx->ring_count = ctx->ring_count < ctx->ring_n ? ctx->ring_count + 1 : ctx->ring_n;
+  }
   ctx->disp_stats_valid = ctx->disp_on;
   if (ctx->disp_on) {   // R28: the events until the next batch follow this batch's policy
     ctx->disp_bstar_prev = ctx->bstar;
@@ -471,12 +565,13 @@ pas_status pas_destroy(pas_ctx* ctx) {
                   ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp,
                   ctx->stage_emb, ctx->s_K, ctx->s_Kp,
                   ctx->s_inst,  ctx->s_slot,    ctx->s_tid,      ctx->s_boff,       ctx->s_bpr,     ctx->s_tsc,
-                  ctx->s_flags};
+                  ctx->s_flags, ctx->x_cand, ctx->x_K, ctx->x_level, ctx->x_flags};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_aux) cudaEventDestroy(ctx->ev_aux);
+  for (auto e : ctx->ring) cudaEventDestroy(e);
   delete ctx;
   return PAS_OK;
 }
@@ -773,6 +868,8 @@ pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every) {
     return fail(ctx, PAS_ERR_ARG, "window must be in [0, %d]", PAS_MAX_FORECAST_WINDOW);
   if (replan_every < 1) return fail(ctx, PAS_ERR_ARG, "replan_every must be >= 1");
   if (window > 0 && !ctx->bands_set) return fail(ctx, PAS_ERR_STATE, "pas_set_bands must precede pas_set_forecast");
+  if (window > 0 && !ctx->c_convex)
+    return fail(ctx, PAS_ERR_DEGRADATION, "the forecast-driven mode's coupling plan needs a convex c (R22)");
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   CUDA_TRY(ctx, cudaDeviceSynchronize());   // no batch in flight may still read the old window
   if (window > 0) {
@@ -805,11 +902,22 @@ pas_status pas_set_degradation(pas_ctx* ctx, const double* c, int len) {
     if (!std::isfinite(c[t])) return fail(ctx, PAS_ERR_DEGRADATION, "c must be finite");
   for (int t = 1; t < len; ++t)
     if (c[t] < c[t - 1]) return fail(ctx, PAS_ERR_DEGRADATION, "c must be non-decreasing");
+  bool convex = true;
   for (int t = 1; t + 1 < len; ++t) {
     const double sec = c[t + 1] - 2 * c[t] + c[t - 1];
-    if (sec < -1e-12 * (1.0 + std::fabs(c[t]))) return fail(ctx, PAS_ERR_DEGRADATION, "c must be convex (R6)");
+    if (sec < -1e-12 * (1.0 + std::fabs(c[t]))) convex = false;
   }
-  for (int t = 0; t < kTTotal; ++t) ctx->c[t] = c[t];
+  if (!convex) {   // R37: exact integer costs for the min-cost solver; D_int = sum x cI < 2^50 needs c <= 1
+    if (c[len - 1] > 1.0)
+      return fail(ctx, PAS_ERR_DEGRADATION, "a non-convex c must stay in [0, 1] (quality loss, S:74)");
+    if (ctx->fc_window > 0)
+      return fail(ctx, PAS_ERR_DEGRADATION, "the forecast-driven mode's coupling plan needs a convex c (R22)");
+  }
+  for (int t = 0; t < kTTotal; ++t) {
+    ctx->c[t] = c[t];
+    ctx->cI[t] = convex ? 0 : (int64_t)std::nearbyint(std::ldexp(c[t], kDegShift));   // exact scaling, RNE
+  }
+  ctx->c_convex = convex;
   return PAS_OK;
 }
 
@@ -848,6 +956,46 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
   ctx->mode = mode;
   ctx->load_mode = mode;
   ctx->fractions_set = true;
+  return PAS_OK;
+}
+
+pas_status pas_stage_ring(pas_ctx* ctx, int slots) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (slots < 0 || slots > PAS_MAX_RING) return fail(ctx, PAS_ERR_ARG, "slots outside [0, %d]", PAS_MAX_RING);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  for (auto e : ctx->ring) cudaEventDestroy(e);
+  ctx->ring.assign((size_t)slots * 7, nullptr);
+  for (auto& e : ctx->ring) CUDA_TRY(ctx, cudaEventCreate(&e));
+  ctx->ring_n = slots;
+  ctx->ring_pos = ctx->ring_count = 0;
+  return PAS_OK;
+}
+
+pas_status pas_stage_ring_read(pas_ctx* ctx, int n, float* ms, int* n_out) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ms || !n_out || n < 0) return fail(ctx, PAS_ERR_ARG, "bad arguments");
+  *n_out = 0;
+  const int64_t have = ctx->ring_count < n ? ctx->ring_count : n;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  for (int64_t b = 0; b < have; ++b) {   // oldest first
+    const int64_t slot = (ctx->ring_pos - have + b) % ctx->ring_n;
+    cudaEvent_t* e = &ctx->ring[slot * 7];
+    CUDA_TRY(ctx, cudaEventSynchronize(e[6]));
+    for (int i = 0; i < 6; ++i) CUDA_TRY(ctx, cudaEventElapsedTime(&ms[b * 7 + i], e[i], e[i + 1]));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms[b * 7 + 6], e[0], e[6]));
+  }
+  *n_out = (int)have;
+  return PAS_OK;
+}
+
+pas_status pas_set_collectives(pas_ctx* ctx, int mode) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (mode != PAS_COLL_FOLDED && mode != PAS_COLL_EXPLICIT) return fail(ctx, PAS_ERR_ARG, "unknown collective mode");
+  ctx->coll_mode = mode;
   return PAS_OK;
 }
 
@@ -1031,7 +1179,7 @@ pas_status pas_route_local(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   if ((s = ensure_prompt_ws(ctx))) return s;
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 0, st));
   const Cand* cand;
   int S;
   return run_local(ctx, emb, dtype, N, st, &cand, &S, static_cast<Cand*>(cand_dev));
@@ -1048,9 +1196,9 @@ pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, 
   if (!cand_dev) return fail(ctx, PAS_ERR_ARG, "null candidates");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[1], st));
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[2], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 0, st));
+  CUDA_TRY(ctx, rec_stage(ctx, 1, st));
+  CUDA_TRY(ctx, rec_stage(ctx, 2, st));
   return run_global(ctx, static_cast<const Cand*>(cand_dev), S, N, out, st);
 }
 
@@ -1070,7 +1218,7 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   if ((s = ensure_prompt_ws(ctx))) return s;   // first call only: outside the timed stages
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+  CUDA_TRY(ctx, rec_stage(ctx, 0, st));
   const Cand* cand;
   int S;
   if (!ctx->comm) {
@@ -1083,6 +1231,7 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
     // ncclAllGather places rank r's N*k pairs at offset r*N*k: the layout is [G][N][k]
     cand = ctx->cand_all;
     S = G;
+    if (ctx->coll_mode == PAS_COLL_EXPLICIT) return run_global_explicit(ctx, cand, N, out, st);
   }
   return run_global(ctx, cand, S, N, out, st);
 }
@@ -1160,6 +1309,7 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
   }
   out->D_Q = p.D_Q;
   out->D_Q_LP = p.D_Q_LP;
+  out->plan_solver_iters = p.solver_iters;
   out->n_redirected = p.n_redirected;
   out->n_upgraded = p.n_upgraded;
   out->n_downgraded = p.n_downgraded;
@@ -1199,6 +1349,32 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
   float tot = 0.f;
   if (cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]) == cudaSuccess) out->stage_ms[6] = tot;
   cudaGetLastError();
+  return PAS_OK;
+}
+
+// Test hooks: the bf16 rows K1 wrote -- the prompt-side Q_hat of the last a1 (R11) and this rank's store.
+pas_status pas_debug_qhat(pas_ctx* ctx, void* out_dev, int64_t N, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!out_dev || N < 0 || N > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_ARG, "bad out / N");
+  if (N == 0) return PAS_OK;
+  if (!ctx->qhat) return fail(ctx, PAS_ERR_STATE, "no prompt has been normalised yet");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out_dev, ctx->qhat, (size_t)N * ctx->cfg.d * 2, cudaMemcpyDeviceToDevice,
+                                (cudaStream_t)stream));
+  return PAS_OK;
+}
+
+pas_status pas_debug_store_rows(pas_ctx* ctx, int64_t first_local_row, int64_t n, void* out_dev, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!out_dev || first_local_row < 0 || n < 0 || first_local_row + n > ctx->M_local)
+    return fail(ctx, PAS_ERR_ARG, "rows [%lld, %lld) outside this rank's %lld", (long long)first_local_row,
+                (long long)(first_local_row + n), (long long)ctx->M_local);
+  if (n == 0) return PAS_OK;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaMemcpyAsync(out_dev, ctx->store + first_local_row * ctx->cfg.d, (size_t)n * ctx->cfg.d * 2,
+                                cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return PAS_OK;
 }
 

@@ -91,6 +91,7 @@ struct DispPlan {
 struct RouteParams {
   int nK, W, bstar, mode, topk, G, rank, d;
   int64_t N, M_total;
+  int64_t cand_stride;           // candidate rows between the S source blocks [S][stride][k] (0: N)
   uint64_t seed, batch_seq;
   int kb;                        // K6 bucket bits of kappa
   int bstar_shift;               // log2(bstar) if bstar is a power of two, else -1
@@ -98,6 +99,8 @@ struct RouteParams {
   float thr[kMaxLevels];         // nK-1 thresholds
   double F[kMaxLevels];          // load fractions
   double c[kTTotal];             // degradation c(dK)
+  int convex;                    // c convex: K5 takes the NW-corner closed form (R6, R7)
+  int64_t cI[kTTotal];           // non-convex c: round-half-even(c * 2^24), K5's exact integer costs (R37)
   int inst_level[kMaxInst];      // level index of each serving instance
   uint32_t* lru_stamp;           // f2: [global slots] last-use ticks (K4 stamps each usable top-1)
   uint32_t lru_tick;             // this batch's tick
@@ -123,7 +126,9 @@ struct DevPlan {
   int n_redirected, n_upgraded, n_downgraded;
   int n_invalid, n_near_top1, n_near_threshold;
   int inst_count[kMaxInst];
+  int solver_iters;                  // non-convex K5: min-cost-flow augmentations (+ lex-max cycles); -1: cap hit
 };
+constexpr int kDegShift = 24;        // R37: non-convex c held as integers on a 2^-24 grid
 
 // ------------------------------------------------------------------------------------------------
 // launchers (each returns cudaGetLastError() of its launch)
@@ -206,6 +211,12 @@ struct SelectOut {
 };
 cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p,
                                 const SelectOut& o, cudaStream_t st);
+// Explicit-N2 mode (pas_set_collectives): the per-prompt results of every rank's prompt slice, gathered
+// in prompt order (all_cand [N][k], all_K / all_level / all_flags [N]), copied into the outputs, with
+// the LRU stamps of every usable top-1 (R26; the slice merges do not stamp).
+cudaError_t launch_unpack_slices(const Cand* all_cand, const int32_t* all_K, const uint8_t* all_level,
+                                 const uint8_t* all_flags, const RouteParams& p, const SelectOut& o,
+                                 cudaStream_t st);
 
 // K5 plan
 cudaError_t launch_plan(const int* hist, const RouteParams& p, DevPlan* plan, cudaStream_t st);

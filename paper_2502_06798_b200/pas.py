@@ -43,7 +43,7 @@ class PasStats(C.Structure):
     _fields_ = [("nK", C.c_int), ("W", C.c_int), ("N", C.c_int64),
                 ("h", C.c_int64 * PAS_MAX_LEVELS), ("f", C.c_int64 * PAS_MAX_LEVELS),
                 ("x", (C.c_int64 * PAS_MAX_LEVELS) * PAS_MAX_LEVELS),
-                ("D_Q", C.c_double), ("D_Q_LP", C.c_double),
+                ("D_Q", C.c_double), ("D_Q_LP", C.c_double), ("plan_solver_iters", C.c_int),
                 ("n_redirected", C.c_int64), ("n_upgraded", C.c_int64), ("n_downgraded", C.c_int64),
                 ("n_invalid", C.c_int64), ("n_near_top1", C.c_int64), ("n_near_threshold", C.c_int64),
                 ("bucket_count", C.c_int64 * PAS_MAX_INSTANCES), ("stage_ms", C.c_float * 8),
@@ -93,6 +93,9 @@ _SIG = {
     "pas_set_degradation": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
     "pas_set_fractions": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int]),
     "pas_set_seed": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
+    "pas_set_collectives": (C.c_int, [_P, C.c_int]),
+    "pas_stage_ring": (C.c_int, [_P, C.c_int]),
+    "pas_stage_ring_read": (C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "pas_set_forecast": (C.c_int, [_P, C.c_int, C.c_int]),
     "pas_set_dispatcher": (C.c_int, [_P, C.POINTER(C.c_int64), C.c_int, C.c_int64]),
     "pas_set_clock": (C.c_int, [_P, C.c_int64]),
@@ -110,6 +113,8 @@ _SIG = {
     "pas_last_launch_count": (C.c_int, [_P]),
     "pas_debug_scores": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
     "pas_debug_k2_schedule": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int64, _P]),
+    "pas_debug_qhat": (C.c_int, [_P, _P, C.c_int64, _P]),
+    "pas_debug_store_rows": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(lib, _name)
@@ -226,6 +231,25 @@ def pas_set_fractions(ctx, F, instance_level, bstar=4, mode=PAS_GREEDY):
     _check(ctx, lib.pas_set_fractions(ctx, Fa, il, len(instance_level), bstar, mode))
 
 
+PAS_COLL_FOLDED, PAS_COLL_EXPLICIT = 0, 1
+
+
+def pas_set_collectives(ctx, mode):
+    _check(ctx, lib.pas_set_collectives(ctx, mode))
+
+
+def pas_stage_ring(ctx, slots):
+    _check(ctx, lib.pas_stage_ring(ctx, slots))
+
+
+def pas_stage_ring_read(ctx, n) -> list:
+    """Per-batch stage times (ms) of the last <= n batches, oldest first: lists of 7 floats."""
+    buf = (C.c_float * (7 * max(1, n)))()
+    got = C.c_int(0)
+    _check(ctx, lib.pas_stage_ring_read(ctx, n, buf, C.byref(got)))
+    return [list(buf[7 * b:7 * b + 7]) for b in range(got.value)]
+
+
 def pas_set_seed(ctx, seed, batch_seq=0):
     _check(ctx, lib.pas_set_seed(ctx, seed, batch_seq))
 
@@ -328,6 +352,7 @@ def pas_plan_stats(ctx) -> dict:
     nK, W = s.nK, s.W
     return dict(nK=nK, W=W, N=s.N, h=list(s.h[:nK]), f=list(s.f[:nK]),
                 x=[list(s.x[i][:nK]) for i in range(nK)], D_Q=s.D_Q, D_Q_LP=s.D_Q_LP,
+                plan_solver_iters=s.plan_solver_iters,
                 n_redirected=s.n_redirected, n_upgraded=s.n_upgraded, n_downgraded=s.n_downgraded,
                 n_invalid=s.n_invalid, n_near_top1=s.n_near_top1, n_near_threshold=s.n_near_threshold,
                 bucket_count=list(s.bucket_count[:W]), stage_ms=list(s.stage_ms),
@@ -352,6 +377,18 @@ def pas_debug_k2_schedule(N, M_local, d=768, max_batch=None) -> dict:
     if st != PAS_OK:
         raise PasError(st, "pas_debug_k2_schedule: bad arguments")
     return dict(zip(("R", "T", "CS", "MTg", "pair", "MT", "NT", "cand_cap"), list(out)))
+
+
+def pas_debug_qhat(ctx, out, stream=None):
+    """out: CUDA bfloat16 / int16 tensor [N, d] receiving the last batch's quantised prompts."""
+    assert out.is_cuda and out.is_contiguous() and out.element_size() == 2
+    _check(ctx, lib.pas_debug_qhat(ctx, _P(out.data_ptr()), out.shape[0], _stream(stream)))
+
+
+def pas_debug_store_rows(ctx, first_local_row, out, stream=None):
+    """out: CUDA bfloat16 / int16 tensor [n, d] receiving this rank's store rows from first_local_row."""
+    assert out.is_cuda and out.is_contiguous() and out.element_size() == 2
+    _check(ctx, lib.pas_debug_store_rows(ctx, first_local_row, out.shape[0], _P(out.data_ptr()), _stream(stream)))
 
 
 def pas_debug_scores(ctx, emb, scores, stream=None):

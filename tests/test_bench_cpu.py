@@ -49,3 +49,21 @@ def test_clock_sampler_counts_only_the_timed_window():
     c.rows += [row(1400, "Active"), row(1420, "Active")]
     clk = c.stop()
     assert clk["samples"] == 2 and clk["sm_mhz"] == 1410.0 and clk["reasons"] == ["sw_power_cap"]
+
+
+def test_both_oracle_legs_share_one_sample_definition():
+    """cpu_baseline and --impl reference time the same OracleSample (same prompts,
+    rows, scaling), so the two legs report the same quantity."""
+    import inspect
+    b = _bench()
+    assert "OracleSample" in inspect.getsource(b.cpu_baseline)
+    assert "OracleSample" in inspect.getsource(b.reference_arm)
+    from synth import CONFIGS, Workload
+    cfg = CONFIGS["C1"]
+    w = Workload(cfg, device="cpu")
+    P = w.prompts(cfg.N).numpy()
+    a = b.cpu_baseline(cfg, w, cfg.N, cfg.M, P, steps=1)
+    smp = b.OracleSample(cfg, w, cfg.N, cfg.M, P)
+    per, t_sim, t_down = smp.step()
+    assert a["kind"] == "oracle" and a["cores"] >= 1 and a["value"] > 0
+    assert a["sample"].startswith(smp.describe(t_sim, t_down).split(";")[0])

@@ -15,8 +15,8 @@ import torch
 from oracle import route as O
 from synth import BLOCK, CONFIGS, Workload
 
-from .parity import (TAU_B, Report, check_downstream, check_levels, check_levels_tier_b, check_topk,
-                     check_topk_tier_b, oracle_topk_ab)
+from .parity import (TAU_B, Report, check_downstream, check_flag_counts, check_flags, check_levels,
+                     check_levels_tier_b, check_topk, check_topk_tier_b, oracle_topk_ab)
 
 # Minimum fraction of finite top-k positions graded under Tier B per config (the check must
 # never become vacuous; measured fractions are printed by every run).
@@ -94,6 +94,11 @@ def run_parity(pas, name, N=None, M=None, sample=None, mode=None, bstar=None, se
     o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid & (M > 0))
     check_levels(glev[idx], o_sc[:, 0], o_lev, valid & (M > 0), cfg.thresholds, rep)
     check_levels_tier_b(glev[idx], ab["sc_B"][:, 0], valid & (M > 0), cfg.thresholds, rep)
+    amb4, amb8, want = check_flags(g["flags"][idx], ab["sc_B"], cfg.thresholds, valid, M == 0, cfg.topk, rep)
+    check_flag_counts(g["flags"], st)
+    if len(idx) == N:   # every prompt checked: the GPU's counts are the oracle's up to the ambiguous ones
+        assert abs(st["n_near_top1"] - int(((want & 4) != 0).sum())) <= amb4
+        assert abs(st["n_near_threshold"] - int(((want & 8) != 0).sum())) <= amb8
     check_downstream(g, glev, _setup(cfg, mode, bstar), st, rep, len(cfg.instance_level))
     print(f"{name} parity (N={N}, M={M}, {len(idx)} prompts vs the whole cache): {rep.summary()}")
     router.close()
@@ -238,6 +243,8 @@ def test_c5_load_sweep_parity_full_size(pas):
         o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid)
         check_levels(glev[idx[b]], o_sc[:, 0], o_lev, valid, cfg.thresholds, rep)
         check_levels_tier_b(glev[idx[b]], ab["sc_B"][sl][:, 0], valid, cfg.thresholds, rep)
+        check_flags(g["flags"][idx[b]], ab["sc_B"][sl], cfg.thresholds, valid, False, k, rep)
+        check_flag_counts(g["flags"], st)
         setup = O.Setup(grid=cfg.grid, thresholds=cfg.thresholds, F=F, instance_level=cfg.instance_level,
                         bstar=cfg.bstar, mode=cfg.mode, topk=k, seed=cfg.route_seed, batch_seq=b)
         check_downstream(g, glev, setup, st, rep, len(cfg.instance_level))
@@ -503,6 +510,8 @@ def _full_parity(pas, cfg, N, M, topk=8, mode=None, bstar=None, d=None, instance
     o_lev = O.optimal_k_level(o_sc[:, 0], cfg.thresholds, valid)
     check_levels(glev, o_sc[:, 0], o_lev, valid, cfg.thresholds, rep)
     check_levels_tier_b(glev, ab["sc_B"][:, 0], valid, cfg.thresholds, rep)
+    check_flags(g["flags"], ab["sc_B"], cfg.thresholds, valid, False, topk, rep)
+    check_flag_counts(g["flags"], st)
     print(f"full parity N={N} M={M} k={topk} d={cfg.d}: {rep.summary()}")
     check_downstream(g, glev, _setup(cfg, mode, bstar), st, rep, len(cfg.instance_level))
     return rep, st

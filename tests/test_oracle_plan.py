@@ -127,3 +127,132 @@ def test_apportion_recovers_h(h):
         return
     F = [v / N for v in h]
     assert O.apportion(F, N).tolist() == h
+
+
+# ------------------------------------------------------------------------------------------------
+# R37 (NEXT f4): the exact plan for an arbitrary, non-convex degradation table
+# ------------------------------------------------------------------------------------------------
+def _concave_c():
+    """c(t) = min(1, 0.09 t): c(10) = 0.9, c(20) = 1.0 -- concave, non-decreasing, in [0, 1]."""
+    return np.minimum(1.0, 0.09 * np.arange(50))
+
+
+def test_r37_hand_example_where_nw_corner_is_suboptimal():
+    """Eq. 1 with a concave D: two prompts at K = {0, 10}, targets at {10, 20}.  The NW-corner
+    (monotone) coupling moves both by 10 steps, D = 0.9 + 0.9 = 1.8; sending the K = 0 prompt to 20 and
+    keeping the other costs D = 1.0 -- the exact optimum (NW is suboptimal on arbitrary
+    tables)."""
+    grid, c = [0, 10, 20], _concave_c()
+    assert not O.is_convex(c)
+    h, f = [1, 1, 0], [0, 1, 1]
+    want = [[0, 0, 1], [0, 1, 0], [0, 0, 0]]
+    cI = O.degradation_int(c)
+    xb, ties = O.plan_int_bruteforce(h, f, grid, cI)
+    assert xb.tolist() == want and ties == 1
+    assert O.plan_int_lp(h, f, grid, cI).tolist() == want
+    assert O.plan_for(h, f, grid, c).tolist() == want
+    assert abs(O.d_q(xb, grid, c, 2) - 0.5) < 1e-15                       # D_Q = 1.0 / N
+    nw = O.plan_lp(h, f, grid, O.default_degradation())                     # the convex-table plan
+    assert nw.tolist() == [[0, 1, 0], [0, 0, 1], [0, 0, 0]] and O.d_q(nw, grid, c, 2) > 0.89
+
+
+def test_r37_degradation_int_is_round_half_even():
+    c = np.zeros(50)
+    c[1] = 0.5 * 2.0 ** -24          # exactly half a unit: ties to even -> 0
+    c[2] = 1.5 * 2.0 ** -24          # -> 2
+    c[3] = 2.5 * 2.0 ** -24          # -> 2
+    c[4] = 0.3
+    c[5:] = 1.0
+    cI = O.degradation_int(c)
+    assert cI[:4].tolist() == [0, 0, 2, 2] and cI[4] == round(0.3 * 2 ** 24) and cI[5] == 2 ** 24
+
+
+def _r37_instances(rng, n, nK_max=4, N_max=8):
+    """Random small instances: random grids and tables, plus arithmetic grids with step tables, where
+    (D, Q) ties occur and the lexicographic rule decides."""
+    for it in range(n):
+        if it % 2:
+            nK = 4
+            grid = [0, 5, 10, 15] if it % 4 == 1 else [0, 10, 20, 30]
+            steps = np.sort(rng.choice([0.0, 0.25, 0.5, 1.0], 3))
+            c = np.zeros(50)
+            c[1:] = steps[np.minimum(np.arange(1, 50) // 11, 2)]
+        else:
+            nK = int(rng.integers(2, nK_max + 1))
+            grid = [0] + sorted(rng.choice(np.arange(1, 50), nK - 1, replace=False).tolist())
+            c = np.concatenate([[0.0], np.sort(rng.uniform(0, 1, 49))])
+        N = int(rng.integers(1, N_max + 1))
+        h = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        f = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        yield grid, c, h, f
+
+
+def r37_tie_instances(n_ties: int, seed: int = 4):
+    """Arithmetic grids with step tables, searched (seeded, bounded) until n_ties instances have
+    several (D, Q)-optimal plans, where only the lexicographic row-major rule decides."""
+    rng = np.random.default_rng(seed)
+    found = []
+    for it in range(50_000):
+        grid = [0, 5, 10, 15] if it % 2 else [0, 10, 20, 30]
+        steps = np.sort(rng.choice([0.0, 0.25, 0.5, 1.0], 3))
+        c = np.zeros(50)
+        c[1:] = steps[np.minimum(np.arange(1, 50) // 11, 2)]
+        N = int(rng.integers(2, 11))
+        h = rng.multinomial(N, rng.dirichlet(np.ones(4)))
+        f = rng.multinomial(N, rng.dirichlet(np.ones(4)))
+        if O.plan_int_bruteforce(h, f, grid, O.degradation_int(c))[1] > 1:
+            found.append((grid, c, h, f))
+            if len(found) == n_ties:
+                return found
+    raise AssertionError("no tie instances found")
+
+
+def test_r37_lp_equals_bruteforce_with_ties():
+    """Exhaustive search (the definition) = the phased LP on 300 random instances and on instances
+    with several (D, Q)-optimal plans, decided by the lexicographic row-major rule on both sides."""
+    rng = np.random.default_rng(37)
+    for grid, c, h, f in list(_r37_instances(rng, 300)) + r37_tie_instances(6):
+        cI = O.degradation_int(c)
+        xb, nt = O.plan_int_bruteforce(h, f, grid, cI)
+        xl = O.plan_int_lp(h, f, grid, cI)
+        assert np.array_equal(xb, xl), (grid, h.tolist(), f.tolist())
+
+
+def test_r37_agrees_with_r7_on_exactly_linear_tables():
+    """Where both rules apply -- a linear table whose integer image is exactly linear (c = t / 64) --
+    R37's plan is R7's unique optimum (the NW-corner plan; LP and brute force)."""
+    rng = np.random.default_rng(7)
+    c = np.arange(50) / 64.0
+    cI = O.degradation_int(c)
+    assert np.all(np.diff(cI, 2) == 0)
+    for _ in range(60):
+        nK = int(rng.integers(2, 7))
+        grid = [0] + sorted(rng.choice(np.arange(1, 50), nK - 1, replace=False).tolist())
+        N = int(rng.integers(1, 40))
+        h = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        f = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        assert np.array_equal(O.plan_int_lp(h, f, grid, cI), O.plan_lp(h, f, grid, c))
+
+
+def test_r37_never_worse_than_nw_and_often_better():
+    """SURVEY V2 in integer form: on arbitrary tables the exact plan's D is <= the NW-corner plan's,
+    strictly lower on a good share of instances (what makes the solver worth having)."""
+    rng = np.random.default_rng(2)
+    better = 0
+    for _ in range(100):
+        nK = int(rng.integers(3, 9))
+        grid = [0] + sorted(rng.choice(np.arange(1, 50), nK - 1, replace=False).tolist())
+        c = np.concatenate([[0.0], np.sort(rng.uniform(0, 1, 49))])
+        cI = O.degradation_int(c)
+        N = int(rng.integers(5, 200))
+        h = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        f = rng.multinomial(N, rng.dirichlet(np.ones(nK)))
+        x = O.plan_int_lp(h, f, grid, cI)
+        hc, fc = np.concatenate([[0], np.cumsum(h)]), np.concatenate([[0], np.cumsum(f)])
+        nw = np.array([[max(0, min(hc[i + 1], fc[j + 1]) - max(hc[i], fc[j])) for j in range(nK)]
+                       for i in range(nK)])
+        D = lambda y: sum(int(y[i, j]) * int(cI[grid[j] - grid[i]]) for i in range(nK) for j in range(nK)
+                          if grid[j] > grid[i])
+        assert D(x) <= D(nw)
+        better += D(x) < D(nw)
+    assert better >= 20

@@ -156,3 +156,34 @@ def test_route_on_synthetic_c1():
     assert np.allclose(r.topk_score[:, 0], S.max(axis=1))
     assert np.array_equal(r.topk_id[:, 0], S.argmax(axis=1))
     assert np.array_equal(np.bincount(r.level_prime, minlength=6), r.f)
+
+
+def test_tier_a_flags_margins_pinned():
+    """Flag bits 4 / 8 (north_star: margins below 2e-2 reported, not failed) on hand-built score rows
+    just inside and just outside the margin, k = 1 (the next score comes from s1_next), sentinels,
+    and the invalid / cold precedence (R16)."""
+    from oracle import route as O
+    thr = [0.65, 0.72, 0.79, 0.86, 0.93]
+    t = np.asarray(thr, np.float32).astype(np.float64)
+    eps = 1e-4
+    sc = np.array([
+        [0.50, 0.50 - 0.02 + eps],      # top-1 margin just below 2e-2        -> 4
+        [0.50, 0.50 - 0.02 - eps],      # just above                          -> 0
+        [t[2] + 0.02 - eps, 0.0],       # s1 just inside the band above t_2   -> 8
+        [t[2] + 0.02 + eps, 0.0],       # just outside                        -> 0
+        [t[4] - 0.02 + eps, 0.0],       # just below the top threshold        -> 8
+        [t[0] - 0.02 - eps, 0.0],       # far below the lowest threshold      -> 0
+        [t[1] + 0.005, t[1] - 0.001],   # both                                -> 12
+        [0.40, -np.inf],                # M = 1: no second score              -> 0
+        [0.40, 0.39],                   # invalid prompt: only 1
+        [0.99, 0.98],
+    ])
+    valid = np.array([True] * 8 + [False, True])
+    f = O.tier_a_flags(sc, np.full(10, -np.inf), thr, valid, cold=False)
+    assert f.tolist() == [4, 0, 8, 0, 8, 0, 12, 0, 1, 4]
+    # k = 1: the margin is taken against s1_next
+    f1 = O.tier_a_flags(sc[:2, :1], np.array([0.50 - 0.02 + eps, 0.50 - 0.02 - eps]), thr, valid[:2], cold=False)
+    assert f1.tolist() == [4, 0]
+    # cold cache: 2 for valid prompts, 1 for invalid ones, never 4 / 8
+    fc = O.tier_a_flags(sc, np.full(10, -np.inf), thr, valid, cold=True)
+    assert fc.tolist() == [2] * 8 + [1, 2]

@@ -135,3 +135,35 @@ def test_merge_of_parts_equals_whole(m, k, cut, seed):
 def test_histogram_counts():
     lv = np.array([0, 2, 2, 5, 0, 2])
     assert O.histogram(lv, 6).tolist() == [2, 0, 3, 0, 0, 1]
+
+
+def test_k1_adversarial_rows_are_what_they_claim():
+    """The adversarial K1 inputs (tests/k1_adversarial.py) pinned by exact rational arithmetic: integer
+    sums of squares (order-free norms), the straddle flag really separates the fp64 product from the
+    quotient under fp32 rounding, and the subnormal quotients sit EXACTLY on fp32 midpoints whose two
+    neighbours round to different bf16 values."""
+    import math
+    from fractions import Fraction
+
+    from oracle import route as O
+    from tests.k1_adversarial import near_midpoint_rows, subnormal_rows
+
+    mid, straddle = near_midpoint_rows(16)
+    for r, st in zip(mid, straddle):
+        ss = sum(int(v) ** 2 for v in r)
+        assert ss == int(np.sum(r * r)) and ss < 2 ** 53
+        norm = math.sqrt(ss)
+        assert (np.float32(r[0] / norm) != np.float32(r[0] * (1.0 / norm))) == st
+    sub = subnormal_rows(2, per_row=8)
+    for r in sub:
+        norm = Fraction(3) * 2 ** 40
+        assert sum(Fraction(float(v)) ** 2 for v in r[:3]) == norm ** 2
+        for v in r[3:11]:
+            q = abs(Fraction(float(v))) / norm
+            units = q / Fraction(1, 2 ** 149)                    # fp32 subnormal spacing
+            assert units.denominator == 2 and (units.numerator // 2) & 0xFFFF == 0x7FFF
+        q, _ = O.quantize(r[None, :].astype(np.float32))
+        # fp32 ties to even (c + 1 = h 2^16 + 0x8000), then that bf16 tie rounds to even: h + 1 units
+        b = (q[0, 3:11].astype(np.float32).view(np.uint32) >> 16) & 0x7FFF
+        h = (np.abs(r[3:11]) / 3 * 2.0 ** 110 - 1) / 2 / 2 ** 16
+        assert np.array_equal(b, np.floor(h).astype(np.uint32) + 1)

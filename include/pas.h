@@ -326,10 +326,21 @@ pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq);
  * out: device arrays, written in full on every rank.  N == 0 is a no-op; N > max_batch ->
  * PAS_ERR_CAPACITY.  Requires bands and fractions (PAS_ERR_STATE).  Enqueue-only (no host sync);
  * batch_seq increments on success.  world > 1 needs the NCCL communicator.  One batch in flight per
- * context (its workspace is reused), and not capturable into a CUDA graph for replay: each call passes
- * per-call host state to its kernels (batch_seq for the Philox counters, the K2 schedule's epoch tag). */
+ * context (its workspace is reused).  The batch-varying state lives in device memory, so the whole
+ * call can be replayed as a CUDA graph (pas_set_graph). */
 pas_status pas_route_batch(pas_ctx* ctx, const void* emb_dev, pas_dtype dtype, int64_t N,
                            const pas_route_out* out, pas_stream stream);
+
+/* CUDA-graph replay of pas_route_batch.  on != 0: the next pas_route_batch captures the
+ * whole batch (K1 .. K7, and the NCCL collectives for world > 1) into a graph owned by the context and
+ * every later call with the same (emb_dev, dtype, N, out pointers) replays it with one cudaGraphLaunch
+ * -- one host call per batch instead of ~14 launches.  The batch-varying state (Philox batch_seq, the
+ * LRU tick, the K2 epoch) lives in device memory and is advanced by the batch's own kernels, so a
+ * replay is exactly the batch an eager call would run.  Any setter, cache load / insert / clear, or a
+ * different pointer / N re-captures (the next call).  The forecast (f1) and dispatcher (f3) modes keep
+ * per-batch host state and always run eagerly.  In graph mode pas_stats.stage_ms holds only the total
+ * [6].  on == 0: eager launches (default).  Errors: PAS_ERR_STATE (poisoned). */
+pas_status pas_set_graph(pas_ctx* ctx, int on);
 
 /* Same, from HOST buffers: copies emb_host (should be pinned) to the device, routes, copies every
  * non-NULL array of out_host (host pointers, same shapes as pas_route_out) back, and synchronises.

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
                                                       int32_t* __restrict__ slot, int32_t* __restrict__ prompts,
                                                       int32_t* __restrict__ user_off) {
   pdl_entry();
+  advance_batch_counters(P);   // the batch's last kernel: every reader of the counters has finished
   __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
   __shared__ int32_t tile_off[NCLS];
   __shared__ int32_t icount[kMaxInst], ioff[kMaxInst + 1];   // per-instance counts, batch-list offsets

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k_fc_sample(const uint8_t* __restrict__ l
   int my_unf = 0;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.N; p += stride) {
     const int i = level[p];
-    const uint32_t u = philox_stream(P.seed, P.batch_seq, (uint32_t)p, kStreamForecast).x;
+    const uint32_t u = philox_stream(P.seed, batch_seq_of(P), (uint32_t)p, kStreamForecast).x;
     const uint64_t w = Hc[i + 1] - Hc[i];
     my_unf += w == 0;
     uint64_t pos = Hc[i] + (((uint64_t)u * w) >> 32);
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) k_fc_sample(const uint8_t* __restrict__ l
     while (j < nK - 1 && Fc[j + 1] <= pos) ++j;
     K_prime[p] = P.grid[j];
     if (P.mode == PAS_UNIFORM) {
-      const uint4 r = philox_stream(P.seed, P.batch_seq, (uint32_t)p, kStreamUniform);
+      const uint4 r = philox_stream(P.seed, batch_seq_of(P), (uint32_t)p, kStreamUniform);
       cls7[p] = plan->inst_list[j][(uint32_t)(((uint64_t)r.x * (uint32_t)plan->n_inst[j]) >> 32)];
     } else {
       cls7[p] = j;

@@ -109,7 +109,7 @@ __device__ __forceinline__ void select_one(float s1, float s2, int32_t g1, int64
   }
   // f2: the top-1 entry is the one whose state is reused (R26); gids outside the store (e.g. from a
   // caller's candidate lists) are ignored
-  if (P.lru_stamp && !invalid && !cold && g1 >= 0 && g1 < P.M_total) P.lru_stamp[g1] = P.lru_tick;
+  if (P.lru_stamp && !invalid && !cold && g1 >= 0 && g1 < P.M_total) P.lru_stamp[g1] = lru_tick_of(P);
   o.level[p] = (uint8_t)lvl;
   o.K[p] = P.grid[lvl];
   if (o.flags) o.flags[p] = fl;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256) k_unpack_slices(const Cand* __restrict__ 
       o.level[p] = all_level[p];
       if (o.flags) o.flags[p] = fl;
       if (P.lru_stamp && !(fl & (PAS_FLAG_INVALID | PAS_FLAG_COLD)) && c.g >= 0 && c.g < P.M_total)
-        P.lru_stamp[c.g] = P.lru_tick;
+        P.lru_stamp[c.g] = lru_tick_of(P);
     }
   }
 }

@@ -83,8 +83,13 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
-                                                   int64_t first_gid, int G, int rank, int* invalid_count) {
+                                                   int64_t first_gid, int G, int rank, int* invalid_count,
+                                                   uint32_t* epoch_bump) {
   pdl_entry();
+  if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) {   // the epoch of the K2 launch that follows
+    const uint32_t e = *epoch_bump + 1;
+    *epoch_bump = e ? e : 1;
+  }
   const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
 
 template <typename T>
 cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8_t* flags, int64_t first_gid, int G,
-                     int rank, int* invalid_count, cudaStream_t st) {
+                     int rank, int* invalid_count, cudaStream_t st, uint32_t* eb) {
   const int threads = 256;
   const int vec = d % 128 == 0 && d <= 1024 ? d / 128 : 0;
   // one warp per row, one CTA per 8 rows (PAS_K1_GRIDCAP 1: capped at the resident CTAs, grid-stride)
@@ -184,15 +189,15 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
   if (PAS_K1_GRIDCAP && blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
   switch (vec) {
-    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count); break;
-    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count);
+    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
+    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb);
   }
   return cudaGetLastError();
 }
@@ -201,11 +206,13 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
 
 cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t* epoch_bump) {
   if (rows <= 0) return cudaSuccess;
   if (dtype == PAS_F32)
-    return launch_t(static_cast<const float*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st);
-  return launch_t(static_cast<const __nv_bfloat16*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st);
+    return launch_t(static_cast<const float*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st,
+                    epoch_bump);
+  return launch_t(static_cast<const __nv_bfloat16*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st,
+                  epoch_bump);
 }
 
 }  // namespace pas

@@ -47,7 +47,7 @@ __device__ __forceinline__ void emit(const RouteParams& P, const int* grid, cons
                                      int64_t p, int j, int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7) {
   K_prime[p] = grid[j];
   if (P.mode == PAS_UNIFORM) {
-    const uint4 w = philox_stream(P.seed, P.batch_seq, (uint32_t)p, kStreamUniform);
+    const uint4 w = philox_stream(P.seed, batch_seq_of(P), (uint32_t)p, kStreamUniform);
     const uint32_t nj = (uint32_t)plan->n_inst[j];
     cls7[p] = (uint8_t)plan->inst_list[j][(uint32_t)(((uint64_t)w.x * nj) >> 32)];
   } else {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(RT) k6_hist(const uint8_t* __restrict__ level,
   pdl_entry();
   const int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x;
   if (p >= P.N) return;
-  const uint4 w = philox_stream(P.seed, P.batch_seq, (uint32_t)p, kStreamRedirect);
+  const uint4 w = philox_stream(P.seed, batch_seq_of(P), (uint32_t)p, kStreamRedirect);
   const uint64_t kappa = (((uint64_t)w.y << 32) | w.x) >> 4;
   key[p] = kappa;
   atomicAdd(&hist[((uint32_t)level[p] << P.kb) | top_bits(kappa, P.kb)], 1);

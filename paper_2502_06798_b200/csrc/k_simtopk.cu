@@ -279,8 +279,8 @@ template <int KMAX, bool DUMP, bool PAIR, bool DYN, bool MC = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
-              float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch, uint32_t slack,
-              const DynSched dyn) {
+              float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch_arg,
+              const uint32_t* __restrict__ epoch_dev, uint32_t slack, const DynSched dyn) {
   static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
   // MC: clusters of two single-CTA tiles on the dynamic schedule, streaming the same cache chunk for
   // prompt tiles 2 mp and 2 mp + 1; each CTA TMA-loads half of every B k-block and multicasts it to
@@ -339,6 +339,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
   pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
+  // this launch's epoch: bumped on the device by the K1 that precedes it (graph-replayable), else the
+  // host's argument
+  const uint32_t epoch = epoch_dev ? *reinterpret_cast<const volatile uint32_t*>(epoch_dev) : epoch_arg;
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
@@ -854,7 +857,7 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   // the CTA pair and the B multicast read the cache through the 128-row box map
   return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN, MC>, *a.tmap_q,
                             (PAIR || MC) ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
-                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, slack, a.dyn);
+                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, a.epoch_dev, slack, a.dyn);
 }
 
 }  // namespace

@@ -1,0 +1,181 @@
+// K3..K7 fused for small batches -- the latency path (low loads are served for
+// latency).  For N <= kSmallMax prompts the multi-kernel downstream (merge +
+// optimal-K, plan, 6 redirect kernels, count / scan / rank) is a chain of ~11 launches of a few
+// microseconds each; here ONE CTA of 1024 threads runs all of it from the K2 candidates:
+//   a4/a5  thread per prompt: S-way merge of the sorted candidate lists (score desc, gid asc, ties to
+//          the lower source, R10), optimal-K level #{m : s1 >= t_m}, flags, LRU stamp of the top-1
+//          (R26), H_K and the flag counters in shared memory;
+//   a6     warp 0: the Eq. 1 plan (plan_body: the same code as K5);
+//   a7     kappa_p = Philox(p) (stream 1), the class rank of (kappa, p) by counting (O(N) per prompt over
+//          shared memory), K' from the plan's row prefix (R3) -- the order statistic K6 selects;
+//   a8     greedy: t = #{q < p : K'_q = K'_p}, instance I_j[(t div b*) mod n_j], slot (R13); uniform:
+//          instance by Philox stream 2, slot = FIFO rank (R14); per-instance counts, offsets and the
+//          batch lists.
+// Same definitions, same fp32 / fp64 operations as the multi-kernel path: the outputs are byte-
+// identical to it (tests/test_gpu_graph.py forces both paths on the same batches).  Stateless
+// exact-plan modes only (the forecast f1 and dispatcher f3 modes take the multi-kernel path).
+#include "philox.cuh"
+#include "plan_body.cuh"
+
+namespace pas {
+namespace {
+
+constexpr int SM_THREADS = 1024;
+
+__global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __restrict__ in, int S,
+                                                               const uint8_t* __restrict__ pflags, const RouteParams P,
+                                                               SmallOut o) {
+  pdl_entry();
+  __shared__ uint8_t lvl_s[kSmallMax], cls_s[kSmallMax];
+  __shared__ uint64_t kap_s[kSmallMax];
+  __shared__ int hist_s[kMaxLevels];
+  __shared__ int cnt_s[3];
+  __shared__ int X_s[kMaxLevels][kMaxLevels];
+  __shared__ int icount_s[kMaxInst], ioff_s[kMaxInst + 1];
+  const int tid = threadIdx.x;
+  const int N = (int)P.N, k = P.topk, nK = P.nK;
+  const bool cold = P.M_total == 0;
+  {   // zero the plan (as launch_zero does for the multi-kernel path) and the shared tallies
+    int32_t* w = reinterpret_cast<int32_t*>(o.plan);
+    for (int i = tid; i < (int)(sizeof(DevPlan) / 4); i += SM_THREADS) w[i] = 0;
+    if (tid < kMaxLevels) hist_s[tid] = 0;
+    if (tid < 3) cnt_s[tid] = 0;
+    if (tid < kMaxInst) icount_s[tid] = 0;
+  }
+  __syncthreads();
+  const uint32_t tick = lru_tick_of(P);
+  const int64_t stride = P.cand_stride ? P.cand_stride : P.N;
+  // ---- a4 + a5: merge, optimal-K, flags, stamps, H_K
+  for (int p = tid; p < N; p += SM_THREADS) {
+    const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
+    Cand res[PAS_MAX_TOPK];
+    if (invalid || cold) {
+      for (int i = 0; i < k; ++i) res[i] = Cand{-INFINITY, -1};
+    } else {
+      uint8_t pos[128];
+      for (int s = 0; s < S; ++s) pos[s] = 0;
+      for (int i = 0; i < k; ++i) {
+        Cand best{-INFINITY, -1};
+        int bs = -1;
+        for (int s = 0; s < S; ++s) {
+          if (pos[s] >= k) continue;
+          const Cand c = in[((int64_t)s * stride + p) * k + pos[s]];
+          if (bs < 0 || cand_better(c, best)) {
+            best = c;
+            bs = s;
+          }
+        }
+        if (bs >= 0) pos[bs]++;
+        res[i] = bs >= 0 ? best : Cand{-INFINITY, -1};
+      }
+    }
+    for (int i = 0; i < k; ++i) {
+      if (o.topk_id) o.topk_id[(int64_t)p * k + i] = res[i].g;
+      if (o.topk_score) o.topk_score[(int64_t)p * k + i] = res[i].s;
+    }
+    // select_one of k_merge.cu
+    const float s1 = res[0].s, s2 = k > 1 ? res[1].s : -INFINITY;
+    int lv = 0;
+    uint8_t fl = 0;
+    if (invalid) fl |= PAS_FLAG_INVALID;
+    else if (cold) fl |= PAS_FLAG_COLD;
+    else {
+#pragma unroll
+      for (int step = 8; step >= 1; step >>= 1)
+        if (s1 >= P.thr[lv + step - 1]) lv += step;
+      if (s2 != -INFINITY && s1 - s2 < 2e-2f) fl |= PAS_FLAG_NEAR_TOP1;
+      if ((lv > 0 && s1 - P.thr[lv - 1] < 2e-2f) || (lv < nK - 1 && P.thr[lv] - s1 < 2e-2f))
+        fl |= PAS_FLAG_NEAR_THRESHOLD;
+    }
+    const int32_t g1 = res[0].g;
+    if (P.lru_stamp && !invalid && !cold && g1 >= 0 && g1 < P.M_total) P.lru_stamp[g1] = tick;
+    lvl_s[p] = (uint8_t)lv;
+    o.level[p] = (uint8_t)lv;
+    o.K[p] = P.grid[lv];
+    if (o.flags) o.flags[p] = fl;
+    atomicAdd(&hist_s[lv], 1);
+    if (fl & PAS_FLAG_INVALID) atomicAdd(&cnt_s[0], 1);
+    if (fl & PAS_FLAG_NEAR_TOP1) atomicAdd(&cnt_s[1], 1);
+    if (fl & PAS_FLAG_NEAR_THRESHOLD) atomicAdd(&cnt_s[2], 1);
+  }
+  __syncthreads();
+  // ---- a6: the plan, one warp (the same code as K5)
+  if (tid < 32) plan_body(hist_s, P, o.plan);
+  __syncthreads();
+  if (tid == 0) {
+    o.plan->n_invalid = cnt_s[0];
+    o.plan->n_near_top1 = cnt_s[1];
+    o.plan->n_near_threshold = cnt_s[2];
+  }
+  for (int e = tid; e < nK * kMaxLevels; e += SM_THREADS) X_s[e / kMaxLevels][e % kMaxLevels] = o.plan->X[e / kMaxLevels][e % kMaxLevels];
+  const uint64_t bseq = batch_seq_of(P);
+  for (int p = tid; p < N; p += SM_THREADS) {
+    const uint4 w = philox_stream(P.seed, bseq, (uint32_t)p, kStreamRedirect);
+    kap_s[p] = (((uint64_t)w.y << 32) | w.x) >> 4;
+  }
+  __syncthreads();
+  // ---- a7: class rank of (kappa, p), K' from the row prefix of the plan
+  for (int p = tid; p < N; p += SM_THREADS) {
+    const int i = lvl_s[p];
+    const uint64_t kp = kap_s[p];
+    int r = 0;
+    for (int q = 0; q < N; ++q)
+      r += (lvl_s[q] == i && (kap_s[q] < kp || (kap_s[q] == kp && q < p))) ? 1 : 0;
+    int j = 0;
+    while (j + 1 < nK && X_s[i][j] <= r) ++j;
+    o.K_prime[p] = P.grid[j];
+    int c = j;
+    if (P.mode == PAS_UNIFORM) {
+      const uint4 u = philox_stream(P.seed, bseq, (uint32_t)p, kStreamUniform);
+      c = o.plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)o.plan->n_inst[j]) >> 32)];
+    }
+    cls_s[p] = (uint8_t)c;
+  }
+  __syncthreads();
+  // ---- a8: instance and slot (FIFO rank within the class), then the batch lists
+  for (int p = tid; p < N; p += SM_THREADS) {
+    const int c = cls_s[p];
+    int t = 0;
+    for (int q = 0; q < p; ++q) t += cls_s[q] == c ? 1 : 0;
+    int inst, sl;
+    if (P.mode == PAS_UNIFORM) {
+      inst = c;
+      sl = t;
+    } else {
+      const int b = P.bstar, nj = o.plan->n_inst[c];
+      const int q1 = t / b;
+      inst = o.plan->inst_list[c][q1 % nj];
+      sl = (q1 / nj) * b + t % b;
+    }
+    o.instance[p] = inst;
+    o.slot[p] = sl;
+    atomicAdd(&icount_s[inst], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < P.W; ++w) {
+      ioff_s[w] = acc;
+      acc += icount_s[w];
+      o.plan->inst_count[w] = icount_s[w];
+    }
+    ioff_s[P.W] = acc;
+  }
+  __syncthreads();
+  if (o.bucket_offsets && tid <= P.W) o.bucket_offsets[tid] = ioff_s[tid];
+  if (o.bucket_prompts)
+    for (int p = tid; p < N; p += SM_THREADS) o.bucket_prompts[ioff_s[o.instance[p]] + o.slot[p]] = p;
+  __syncthreads();
+  advance_batch_counters(P);   // after every read of the counters in this batch
+}
+
+}  // namespace
+
+cudaError_t launch_small_route(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p, const SmallOut& o,
+                               cudaStream_t st) {
+  if (p.N <= 0) return cudaSuccess;
+  launch_pdl(k_small_route, 1, SM_THREADS, 0, st, in, S, pflags, p, o);
+  return cudaGetLastError();
+}
+
+}  // namespace pas

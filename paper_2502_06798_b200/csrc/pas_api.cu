@@ -118,6 +118,7 @@ struct pas_ctx {
   int64_t k2_state_tiles = 0;
   int k2_last_R = 0, k2_last_T = 0, k2_last_CS = 0;   // schedule of the last K2 launch (pas_plan_stats)
   K2Tuning k2_tune;                                    // experiment knobs, read at pas_create
+  int small_max = kSmallMax;   // the one-CTA latency path serves N <= small_max (PAS_SMALL_MAX; 0: off)
   // f1 forecast-driven mode (0 = exact per-batch plan)
   int fc_window = 0, fc_replan_every = 1;
   int64_t fc_tick = 0;
@@ -144,6 +145,7 @@ struct pas_ctx {
   int32_t *lru_counts = nullptr, *lru_scanned = nullptr, *lru_scan_tmp = nullptr, *lru_victims = nullptr;
   int32_t *ins_idx = nullptr, *ins_count = nullptr;
   uint8_t* level = nullptr;
+  BatchCounters* bc = nullptr;       // device: Philox batch_seq, next LRU tick, K2 epoch (graph-replayable)
   int* hist = nullptr;
   int* invalid_count = nullptr;
   DevPlan* plan = nullptr;
@@ -170,6 +172,15 @@ struct pas_ctx {
   std::vector<cudaEvent_t> ring;
   int ring_n = 0;
   int64_t ring_pos = 0, ring_count = 0;
+  // CUDA-graph replay of pas_route_batch (pas_set_graph): the batch is captured once per (emb, dtype,
+  // N, outputs) and replayed; any setter or cache change invalidates it
+  bool graph_on = false, graph_valid = false, capturing = false, stages_valid = false;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  const void* g_emb = nullptr;
+  int g_dtype = -1, g_launches = 0;
+  int64_t g_N = -1;
+  pas_route_out g_out{};
   bool ev_valid = false;
   cudaStream_t last_stream = nullptr;
 };
@@ -220,6 +231,7 @@ int64_t local_rows_below(int64_t total, int G, int rank) {
 
 // Record stage boundary i (0..6) of the current batch: ev[i], and its slot of the timing ring.
 cudaError_t rec_stage(pas_ctx* ctx, int i, cudaStream_t st) {
+  if (ctx->capturing) return cudaSuccess;   // a replayed graph is timed as a whole (pas_route_batch)
   cudaError_t e = cudaEventRecord(ctx->ev[i], st);
   if (e == cudaSuccess && ctx->ring_n > 0) e = cudaEventRecord(ctx->ring[(ctx->ring_pos % ctx->ring_n) * 7 + i], st);
   return e;
@@ -261,6 +273,7 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
   p.lru_stamp = ctx->stamps;
   p.lru_tick = ctx->lru_tick;
+  p.bc = ctx->bc;
   p.disp = ctx->disp_on ? 1 : 0;
   p.bstar_prev = ctx->disp_bstar_prev;
   p.now_us = ctx->disp_now;
@@ -361,7 +374,8 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
                      int* S, Cand* merged) {
   const int k = ctx->cfg.topk;
   if (pas_status s = ensure_prompt_ws(ctx)) return s;
-  CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
+  CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st,
+                                 &ctx->bc->k2_epoch));
   ctx->launches++;
   CUDA_TRY(ctx, rec_stage(ctx, 1, st));
   int R = 1;
@@ -374,10 +388,9 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
       dyn.done = ctx->k2_done;
       dyn.sched = ctx->k2_sched;
     }
-    if (++ctx->k2_epoch == 0) ctx->k2_epoch = 1;
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
                   ctx->qhat, ctx->cand_local, nullptr, ctx->k2_tune.no_leash ? nullptr : ctx->k2_progress,
-                  ctx->k2_epoch, dyn};
+                  0, &ctx->bc->k2_epoch, dyn};
     CUDA_TRY(ctx, launch_simtopk(a, st));
     ctx->k2_last_R = R;
     ctx->k2_last_T = dyn.T;
@@ -402,6 +415,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
 }
 
 pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_route_out* out, cudaStream_t st);
+pas_status finish_batch(pas_ctx* ctx, int64_t N, cudaStream_t st);
 
 // a4 (final merge) .. a8 for all N prompts from S candidate blocks [S][N][k].
 pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
@@ -416,6 +430,18 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
   // here, so a later pas_route_from_candidates with the same N never reuses them (else: all valid)
   const uint8_t* pflags = ctx->last_local_N == N ? ctx->pflags : nullptr;
   ctx->last_local_N = -1;
+  if (N <= ctx->small_max && S <= 128 && ctx->fc_window == 0 && !ctx->disp_on) {
+    // the latency path: merge .. route-and-batch in one CTA (k_small.cu), no DevPlan zeroing launch
+    SmallOut sm{out->K, out->K_prime, out->instance, out->slot, out->topk_id, out->topk_score, out->flags,
+                out->bucket_offsets, out->bucket_prompts, ctx->level, ctx->plan};
+    CUDA_TRY(ctx, launch_small_route(cand, S, pflags, p, sm, st));
+    ctx->launches++;
+    CUDA_TRY(ctx, rec_stage(ctx, 3, st));
+    CUDA_TRY(ctx, rec_stage(ctx, 4, st));
+    CUDA_TRY(ctx, rec_stage(ctx, 5, st));
+    ctx->fc_stats_valid = false;
+    return finish_batch(ctx, N, st);
+  }
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
   CUDA_TRY(ctx, rec_stage(ctx, 3, st));
@@ -505,8 +531,14 @@ pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_rou
   CUDA_TRY(ctx, rec_stage(ctx, 5, st));
   CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, ctx->bw, out->instance, out->slot,
                                        out->bucket_offsets, out->bucket_prompts, st, &ctx->launches));
+  return finish_batch(ctx, N, st);
+}
+
+// The batch's last stage boundary and the host-side bookkeeping of a routed batch.
+pas_status finish_batch(pas_ctx* ctx, int64_t N, cudaStream_t st) {
   CUDA_TRY(ctx, rec_stage(ctx, 6, st));
   ctx->ev_valid = true;
+  ctx->stages_valid = !ctx->capturing;
   ctx->last_stream = st;
   ctx->last_N = N;
   ctx->batch_seq++;
@@ -560,7 +592,7 @@ pas_status pas_destroy(pas_ctx* ctx) {
                   ctx->dstate, ctx->dplan, ctx->asg_keys, ctx->asg_out,
                   ctx->stamps, ctx->lru_sel, ctx->lru_counts, ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims,
                   ctx->ins_idx, ctx->ins_count,
-                  ctx->level,   ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.hist,
+                  ctx->level,   ctx->bc, ctx->hist,      ctx->invalid_count, ctx->plan,      ctx->rw.key,    ctx->rw.hist,
                   ctx->rw.used, ctx->rw.csum, ctx->rw.bnd, ctx->rw.lists,  ctx->rw.cand,    ctx->rw.cls7,
                   ctx->bw.blk_counts, ctx->bw.blk_off, ctx->bw.offsets, ctx->bw.scan_tmp,
                   ctx->stage_emb, ctx->s_K, ctx->s_Kp,
@@ -572,6 +604,8 @@ pas_status pas_destroy(pas_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->ev_aux) cudaEventDestroy(ctx->ev_aux);
   for (auto e : ctx->ring) cudaEventDestroy(e);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   delete ctx;
   return PAS_OK;
 }
@@ -612,6 +646,10 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
   ctx->cand_cap = k2_cand_cap(mb);
   ctx->k2_tune = K2Tuning::from_env();
+  if (const char* v = getenv("PAS_SMALL_MAX")) {   // A/B and tests: force the multi-kernel chain
+    const int m = atoi(v);
+    ctx->small_max = m < 0 ? 0 : (m > kSmallMax ? kSmallMax : m);
+  }
   const int64_t nb = (int64_t)kMaxLevels << redirect_kb(mb);
   const int64_t ncls = 64 * (int64_t)batch_tiles(mb);
   cudaError_t e = cudaSuccess;
@@ -622,6 +660,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   if (e == cudaSuccess)
     e = cudaMemset(ctx->stamps, 0, sizeof(uint32_t) * (size_t)cfg->world * (ctx->cap_rows > 0 ? ctx->cap_rows : 1));
   ALLOC(ctx->level, mb);
+  ALLOC(ctx->bc, 1);
   ALLOC(ctx->hist, kMaxLevels);
   ALLOC(ctx->invalid_count, 1);
   ALLOC(ctx->plan, 1);
@@ -650,6 +689,13 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   if (cudaEventCreate(&ctx->ev_aux) != cudaSuccess) {
     pas_destroy(ctx);
     return fail(nullptr, PAS_ERR_CUDA, "cudaEventCreate failed");
+  }
+  {
+    const BatchCounters b0{0, 1, 0};   // batch 0, next LRU tick 1 (host tick 0), K2 epoch 0 = none yet
+    if (cudaMemcpy(ctx->bc, &b0, sizeof b0, cudaMemcpyHostToDevice) != cudaSuccess) {
+      pas_destroy(ctx);
+      return fail(nullptr, PAS_ERR_CUDA, "batch counter initialisation failed");
+    }
   }
   if (!encode_map(&ctx->tm_c, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c((int)d)) ||
       !encode_map(&ctx->tm_c2, ctx->store, ctx->cap_rows > 0 ? ctx->cap_rows : 1, (int)d, simtopk_box_c_pair())) {
@@ -681,6 +727,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
 pas_status pas_cache_clear(pas_ctx* ctx) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   ctx->M_total = 0;
   ctx->M_local = 0;
   return PAS_OK;
@@ -697,6 +744,7 @@ pas_status pas_cache_load(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64
                           pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (M < 0 || (M > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / M");
   if ((s = validate_rows(ctx, rows, dtype))) return s;
   const int G = ctx->cfg.world, rank = ctx->cfg.rank;
@@ -720,6 +768,7 @@ pas_status pas_cache_load(pas_ctx* ctx, const void* rows, pas_dtype dtype, int64
   if (bad) return fail(ctx, PAS_ERR_INVALID_ROWS, "%d of the rows are non-finite or have zero norm", bad);
   ctx->lru_tick++;
   CUDA_TRY(ctx, launch_fill_u32(ctx->stamps + ctx->M_total, M, ctx->lru_tick, st));
+  CUDA_TRY(ctx, launch_fill_u32(&ctx->bc->lru_tick, 1, ctx->lru_tick + 1, st));   // the next batch's tick
   ctx->M_total = new_total;
   ctx->M_local = new_local;
   return PAS_OK;
@@ -759,6 +808,7 @@ pas_status insert_staged(pas_ctx* ctx, const int32_t* src, int64_t n, int32_t* g
                                      ctx->lru_scanned, ctx->lru_scan_tmp, ctx->lru_victims, st));
   CUDA_TRY(ctx, launch_store_rows(ctx->qhat, src, n, n_append, ctx->M_total, ctx->lru_victims, ctx->cfg.d, G, rank,
                                   ctx->store, ctx->stamps, ctx->lru_tick, gids_out, gids_by_prompt, st));
+  CUDA_TRY(ctx, launch_fill_u32(&ctx->bc->lru_tick, 1, ctx->lru_tick + 1, st));   // the next batch's tick
   ctx->M_total += n_append;
   ctx->M_local = local_rows_below(ctx->M_total, G, rank);
   ctx->last_local_N = -1;   // the staging buffers no longer hold the last routed batch
@@ -771,6 +821,7 @@ pas_status pas_cache_insert(pas_ctx* ctx, const void* rows, pas_dtype dtype, int
                             pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (n < 0 || (n > 0 && !rows)) return fail(ctx, PAS_ERR_ARG, "bad rows / n");
   if ((s = validate_rows(ctx, rows, dtype))) return s;
   if (n > ctx->cfg.max_batch) return fail(ctx, PAS_ERR_CAPACITY, "n > max_batch (rows are staged like a batch)");
@@ -795,6 +846,7 @@ pas_status pas_cache_insert_vanilla(pas_ctx* ctx, const void* emb, pas_dtype dty
                                     pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (n_inserted) *n_inserted = 0;
   if (N < 0 || (N > 0 && (!emb || !K_prime))) return fail(ctx, PAS_ERR_ARG, "bad emb / K_prime / N");
   if ((s = validate_rows(ctx, emb, dtype))) return s;
@@ -832,6 +884,7 @@ pas_status pas_cache_stamps(pas_ctx* ctx, uint32_t* stamps_dev, int64_t n, pas_s
 pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const float* thresholds) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (!K_levels || nK < 1 || nK > kMaxLevels || (nK > 1 && !thresholds))
     return fail(ctx, PAS_ERR_BANDS, "need 1 <= nK <= %d levels and nK-1 thresholds", kMaxLevels);
   if (K_levels[0] != 0) return fail(ctx, PAS_ERR_BANDS, "level 0 required (K_levels[0] == 0, S:29)");
@@ -864,6 +917,7 @@ pas_status pas_set_bands(pas_ctx* ctx, const int32_t* K_levels, int nK, const fl
 pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (window < 0 || window > PAS_MAX_FORECAST_WINDOW)
     return fail(ctx, PAS_ERR_ARG, "window must be in [0, %d]", PAS_MAX_FORECAST_WINDOW);
   if (replan_every < 1) return fail(ctx, PAS_ERR_ARG, "replan_every must be >= 1");
@@ -896,6 +950,7 @@ pas_status pas_set_forecast(pas_ctx* ctx, int window, int replan_every) {
 pas_status pas_set_degradation(pas_ctx* ctx, const double* c, int len) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (!c || len != kTTotal) return fail(ctx, PAS_ERR_DEGRADATION, "c must have PAS_T_TOTAL = %d entries", kTTotal);
   if (c[0] != 0.0) return fail(ctx, PAS_ERR_DEGRADATION, "c[0] must be 0");
   for (int t = 0; t < len; ++t)
@@ -925,6 +980,7 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
                              pas_mode mode) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (!ctx->bands_set) return fail(ctx, PAS_ERR_STATE, "pas_set_bands must precede pas_set_fractions");
   if (!F || !instance_level) return fail(ctx, PAS_ERR_ARG, "null argument");
   if (W < 1 || W > kMaxInst) return fail(ctx, PAS_ERR_ARG, "W must be in [1, %d]", kMaxInst);
@@ -962,6 +1018,7 @@ pas_status pas_set_fractions(pas_ctx* ctx, const double* F, const int32_t* insta
 pas_status pas_stage_ring(pas_ctx* ctx, int slots) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (slots < 0 || slots > PAS_MAX_RING) return fail(ctx, PAS_ERR_ARG, "slots outside [0, %d]", PAS_MAX_RING);
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   CUDA_TRY(ctx, cudaDeviceSynchronize());
@@ -994,6 +1051,7 @@ pas_status pas_stage_ring_read(pas_ctx* ctx, int n, float* ms, int* n_out) {
 pas_status pas_set_collectives(pas_ctx* ctx, int mode) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (mode != PAS_COLL_FOLDED && mode != PAS_COLL_EXPLICIT) return fail(ctx, PAS_ERR_ARG, "unknown collective mode");
   ctx->coll_mode = mode;
   return PAS_OK;
@@ -1002,14 +1060,19 @@ pas_status pas_set_collectives(pas_ctx* ctx, int mode) {
 pas_status pas_set_seed(pas_ctx* ctx, uint64_t seed, uint64_t batch_seq) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaDeviceSynchronize());   // batches in flight keep the sequence they were enqueued with
+  CUDA_TRY(ctx, cudaMemcpy(&ctx->bc->batch_seq, &batch_seq, sizeof batch_seq, cudaMemcpyHostToDevice));
   ctx->seed = seed;
   ctx->batch_seq = batch_seq;
+  ctx->graph_valid = false;
   return PAS_OK;
 }
 
 pas_status pas_set_dispatcher(pas_ctx* ctx, const int64_t* service_us, int W, int64_t timeout_us) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (!service_us) {   // back to the stateless packing
     ctx->disp_on = false;
     ctx->disp_stats_valid = false;
@@ -1060,6 +1123,7 @@ pas_status pas_set_clock(pas_ctx* ctx, int64_t now_us) {
 pas_status pas_set_load(pas_ctx* ctx, double lambda_rps, int bstar_high, pas_mode* mode_out) {
   pas_status s = check_live(ctx);
   if (s) return s;
+  ctx->graph_valid = false;   // a captured batch bakes this state in
   if (!ctx->disp_on) return fail(ctx, PAS_ERR_STATE, "pas_set_load needs pas_set_dispatcher (service times)");
   if (!(lambda_rps >= 0.0) || !std::isfinite(lambda_rps)) return fail(ctx, PAS_ERR_ARG, "lambda must be finite, >= 0");
   if (bstar_high < 1 || bstar_high > kArrRing) return fail(ctx, PAS_ERR_ARG, "bstar_high outside [1, %d]", kArrRing);
@@ -1202,22 +1266,12 @@ pas_status pas_route_from_candidates(pas_ctx* ctx, const void* cand_dev, int S, 
   return run_global(ctx, static_cast<const Cand*>(cand_dev), S, N, out, st);
 }
 
-pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, const pas_route_out* out,
-                           pas_stream stream) {
-  pas_status s = check_live(ctx);
-  if (s) return s;
-  if ((s = ready(ctx, N))) return s;
-  if ((s = validate_rows(ctx, emb, dtype))) return s;
-  ctx->launches = 0;
-  if (N == 0) return PAS_OK;
-  if ((s = validate_out(ctx, out))) return s;
-  if (!emb) return fail(ctx, PAS_ERR_ARG, "emb is NULL");
+namespace {
+// The whole batch enqueued on st (eager, or into a graph being captured).
+pas_status route_enqueue(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, const pas_route_out* out,
+                         cudaStream_t st) {
+  pas_status s;
   const int G = ctx->cfg.world;
-  if (G > 1 && !ctx->comm)
-    return fail(ctx, PAS_ERR_STATE, "world > 1 without an NCCL communicator: use the split calls");
-  cudaStream_t st = (cudaStream_t)stream;
-  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
-  if ((s = ensure_prompt_ws(ctx))) return s;   // first call only: outside the timed stages
   CUDA_TRY(ctx, rec_stage(ctx, 0, st));
   const Cand* cand;
   int S;
@@ -1234,6 +1288,93 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
     if (ctx->coll_mode == PAS_COLL_EXPLICIT) return run_global_explicit(ctx, cand, N, out, st);
   }
   return run_global(ctx, cand, S, N, out, st);
+}
+
+bool same_out(const pas_route_out& a, const pas_route_out& b) { return memcmp(&a, &b, sizeof a) == 0; }
+
+// Capture the batch into ctx->gexec (the host-side counters the capture advanced are restored: the
+// graph has not run yet).
+pas_status capture_graph(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, const pas_route_out* out) {
+  if (!ctx->cap_stream) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  const uint64_t bseq = ctx->batch_seq;
+  const uint32_t tick = ctx->lru_tick;
+  CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;
+  ctx->launches = 0;
+  pas_status s = route_enqueue(ctx, emb, dtype, N, out, ctx->cap_stream);
+  ctx->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+  ctx->batch_seq = bseq;
+  ctx->lru_tick = tick;
+  if (s != PAS_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  if (e != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e));
+  const cudaError_t ei = cudaGraphInstantiate(&ctx->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ei != cudaSuccess) return fail(ctx, PAS_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ei));
+  ctx->g_emb = emb;
+  ctx->g_dtype = dtype;
+  ctx->g_N = N;
+  ctx->g_out = *out;
+  ctx->g_launches = ctx->launches;
+  ctx->graph_valid = true;
+  return PAS_OK;
+}
+}  // namespace
+
+pas_status pas_set_graph(pas_ctx* ctx, int on) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  ctx->graph_on = on != 0;
+  ctx->graph_valid = false;
+  return PAS_OK;
+}
+
+pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64_t N, const pas_route_out* out,
+                           pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if ((s = ready(ctx, N))) return s;
+  if ((s = validate_rows(ctx, emb, dtype))) return s;
+  ctx->launches = 0;
+  if (N == 0) return PAS_OK;
+  if ((s = validate_out(ctx, out))) return s;
+  if (!emb) return fail(ctx, PAS_ERR_ARG, "emb is NULL");
+  const int G = ctx->cfg.world;
+  if (G > 1 && !ctx->comm)
+    return fail(ctx, PAS_ERR_STATE, "world > 1 without an NCCL communicator: use the split calls");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_prompt_ws(ctx))) return s;   // first call only: outside the timed stages
+  // graph replay: the stateless exact-plan path (the forecast / dispatcher modes carry host-side state
+  // per batch and run eagerly)
+  if (ctx->graph_on && !ctx->disp_on && ctx->fc_window == 0) {
+    if (!ctx->graph_valid || ctx->g_emb != emb || ctx->g_dtype != (int)dtype || ctx->g_N != N ||
+        !same_out(ctx->g_out, *out))
+      if ((s = capture_graph(ctx, emb, dtype, N, out))) return s;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[0], st));
+    CUDA_TRY(ctx, cudaGraphLaunch(ctx->gexec, st));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev[6], st));
+    ctx->launches = ctx->g_launches;
+    ctx->lru_tick++;   // the host mirrors of what the replayed batch advanced on the device
+    ctx->batch_seq++;
+    ctx->last_local_N = -1;
+    ctx->ev_valid = true;
+    ctx->stages_valid = false;
+    ctx->last_stream = st;
+    ctx->last_N = N;
+    ctx->fc_stats_valid = false;
+    ctx->disp_stats_valid = false;
+    return PAS_OK;
+  }
+  return route_enqueue(ctx, emb, dtype, N, out, st);
 }
 
 pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
@@ -1342,7 +1483,7 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
                                   out->fired_batches)))
       return s;
   }
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 6 && ctx->stages_valid; ++i) {   // a replayed graph: only the total
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) out->stage_ms[i] = ms;
   }
@@ -1405,7 +1546,7 @@ pas_status pas_debug_scores(pas_ctx* ctx, const void* emb, pas_dtype dtype, int6
   if ((s = ensure_prompt_ws(ctx))) return s;
   CUDA_TRY(ctx, launch_normalize(emb, dtype, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st));
   SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, 1, ctx->cfg.world, ctx->cfg.rank, 1,
-                ctx->qhat, ctx->cand_local, scores_dev, nullptr, 0};
+                ctx->qhat, ctx->cand_local, scores_dev, nullptr, 0, nullptr};
   CUDA_TRY(ctx, launch_simtopk(a, st));
   return PAS_OK;
 }

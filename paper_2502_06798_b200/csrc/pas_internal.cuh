@@ -88,6 +88,16 @@ struct DispPlan {
 };
 
 // Per-batch parameters, passed BY VALUE to the kernels that need them (no upload, no host sync).
+// Per-batch counters kept on the device so a batch's kernels need no per-call host state (CUDA-graph
+// replay, pas_set_graph): the Philox batch sequence (R18), the f2 LRU tick of the next batch (R26), and
+// the K2 launch epoch.  The last kernel of each batch advances batch_seq and lru_tick; K1 on the prompt
+// path advances k2_epoch before the K2 that follows it.
+struct BatchCounters {
+  uint64_t batch_seq;
+  uint32_t lru_tick;
+  uint32_t k2_epoch;
+};
+
 struct RouteParams {
   int nK, W, bstar, mode, topk, G, rank, d;
   int64_t N, M_total;
@@ -103,7 +113,8 @@ struct RouteParams {
   int64_t cI[kTTotal];           // non-convex c: round-half-even(c * 2^24), K5's exact integer costs (R37)
   int inst_level[kMaxInst];      // level index of each serving instance
   uint32_t* lru_stamp;           // f2: [global slots] last-use ticks (K4 stamps each usable top-1)
-  uint32_t lru_tick;             // this batch's tick
+  uint32_t lru_tick;             // this batch's tick (when bc == nullptr)
+  BatchCounters* bc;             // device counters (batch_seq, lru_tick override the fields above)
   // f3 stateful dispatcher (disp == 0: the stateless packing of R13 / R14)
   int disp;
   int bstar_prev;                // b* in force since the last batch (events in between, R28)
@@ -136,7 +147,21 @@ constexpr int kDegShift = 24;        // R37: non-convex c held as integers on a 
 // K1: normalise + quantise rows; shard filter (first_gid + i) % G == rank -> local row (first_gid+i)/G
 cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
-                             cudaStream_t st);
+                             cudaStream_t st, uint32_t* epoch_bump = nullptr);
+
+__device__ __forceinline__ uint64_t batch_seq_of(const RouteParams& P) {
+  return P.bc ? *reinterpret_cast<const volatile uint64_t*>(&P.bc->batch_seq) : P.batch_seq;
+}
+__device__ __forceinline__ uint32_t lru_tick_of(const RouteParams& P) {
+  return P.bc ? *reinterpret_cast<const volatile uint32_t*>(&P.bc->lru_tick) : P.lru_tick;
+}
+// The last kernel of a batch, one thread: the next batch's Philox sequence and LRU tick.
+__device__ __forceinline__ void advance_batch_counters(const RouteParams& P) {
+  if (P.bc && blockIdx.x == 0 && threadIdx.x == 0) {
+    P.bc->batch_seq += 1;
+    P.bc->lru_tick += 1;
+  }
+}
 
 // K2 dynamic schedule (DESIGN.md 8 "K2 schedule"): units (chunk step, range, prompt tile) handed out
 // in that order by a global counter; each (range, prompt tile) parks its two half top-k lists between
@@ -181,6 +206,7 @@ struct SimTopkArgs {
   float* dump;                    // test hook: [N x M_local] raw scores instead of top-k (or null)
   uint64_t* progress;             // [kNumSMs] leash words (epoch << 32 | tiles issued), or null: no leash
   uint32_t epoch;                 // this launch's epoch (never 0: zeroed words read as "not started")
+  const uint32_t* epoch_dev;      // or, if set, read from here after the PDL wait (bumped by K1)
   DynSched dyn;                   // T > 0: the dynamic schedule (simtopk_plan_dynamic)
 };
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
@@ -211,6 +237,21 @@ struct SelectOut {
 };
 cudaError_t launch_merge_select(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p,
                                 const SelectOut& o, cudaStream_t st);
+// The latency path (k_small.cu): a4 .. a8 of a batch of N <= kSmallMax prompts in one CTA (stateless
+// exact-plan modes), byte-identical to the multi-kernel chain it replaces.
+constexpr int kSmallMax = 1024;
+struct SmallOut {
+  int32_t *K, *K_prime, *instance, *slot;
+  int32_t* topk_id;          // optional
+  float* topk_score;         // optional
+  uint8_t* flags;            // optional
+  int32_t *bucket_offsets, *bucket_prompts;   // optional
+  uint8_t* level;            // workspace [N]
+  DevPlan* plan;
+};
+cudaError_t launch_small_route(const Cand* in, int S, const uint8_t* pflags, const RouteParams& p, const SmallOut& o,
+                               cudaStream_t st);
+
 // Explicit-N2 mode (pas_set_collectives): the per-prompt results of every rank's prompt slice, gathered
 // in prompt order (all_cand [N][k], all_K / all_level / all_flags [N]), copied into the outputs, with
 // the LRU stamps of every usable top-1 (R26; the slice merges do not stamp).

@@ -1,0 +1,284 @@
+// plan_body.cuh -- K5's Eq. 1 route plan for one batch, executed by one warp: largest-remainder
+// targets f, the plan x (NW-corner closed form for convex c; the exact min-cost solver of R37
+// otherwise), D_Q, D_Q_LP, counters, prefix tables and instance lists into a DevPlan.  Shared by the
+// K5 kernel (k_plan.cu) and the fused small-batch kernel (k_small.cu).  Readings and the algorithm's
+// description: the head of k_plan.cu.
+#pragma once
+#include "pas_internal.cuh"
+
+namespace pas {
+namespace {
+
+// (D, Q) cost pair, compared lexicographically
+struct Cost2 {
+  long long d, q;
+};
+__device__ __forceinline__ bool lt(const Cost2& a, const Cost2& b) { return a.d < b.d || (a.d == b.d && a.q < b.q); }
+__device__ __forceinline__ Cost2 add(const Cost2& a, const Cost2& b) { return {a.d + b.d, a.q + b.q}; }
+__device__ __forceinline__ Cost2 sub(const Cost2& a, const Cost2& b) { return {a.d - b.d, a.q - b.q}; }
+__device__ __forceinline__ bool is_zero(const Cost2& a) { return a.d == 0 && a.q == 0; }
+
+constexpr long long kInfD = (long long)1 << 62;
+
+// Exact lexicographic min-cost transportation plan (R37) for rows h, columns f (sum h == sum f),
+// unit cost of cell (i, j) = (cI[K_j - K_i] if K_j > K_i else 0, (K_j - K_i)^2); then the
+// lexicographically greatest optimal x in row-major order.  One thread; x in shared memory.  Returns
+// the number of augmentations, or -1 if the iteration cap was hit (x is then feasible, not canonical).
+__device__ int mcf_plan(const int* h, const int* f, const RouteParams& P, int (*x)[kMaxLevels]) {
+  const int nK = P.nK;
+  const int V = 2 * nK + 2, S = 0, T = 2 * nK + 1;   // S, rows 1..nK, cols nK+1..2nK, T
+  // working arrays in shared memory (one thread runs the solver; no per-thread stack frame)
+  __shared__ Cost2 C[kMaxLevels][kMaxLevels];
+  for (int i = 0; i < nK; ++i)
+    for (int j = 0; j < nK; ++j) {
+      const int dk = P.grid[j] - P.grid[i];
+      C[i][j] = {dk > 0 ? P.cI[dk] : 0, (long long)dk * dk};
+      x[i][j] = 0;
+    }
+  __shared__ int rs[kMaxLevels], rd[kMaxLevels];
+  for (int i = 0; i < nK; ++i) {
+    rs[i] = h[i];
+    rd[i] = f[i];
+  }
+  __shared__ Cost2 pot[2 * kMaxLevels + 2], dist[2 * kMaxLevels + 2];
+  __shared__ int prev[2 * kMaxLevels + 2];
+  __shared__ bool done[2 * kMaxLevels + 2];
+  for (int v = 0; v < V; ++v) pot[v] = {0, 0};
+  int iters = 0;
+  const int cap = 64 * nK * nK + 64;
+  int left = 0;
+  for (int i = 0; i < nK; ++i) left += rs[i];
+  // residual capacity of edge u -> v (0 = absent); cost of u -> v
+  auto rcap = [&](int u, int v) -> long long {
+    if (u == S && v >= 1 && v <= nK) return rs[v - 1];
+    if (v == S && u >= 1 && u <= nK) return h[u - 1] - rs[u - 1];
+    if (u >= 1 && u <= nK && v > nK && v < T) return kInfD;
+    if (u > nK && u < T && v >= 1 && v <= nK) return x[v - 1][u - nK - 1];
+    if (u > nK && u < T && v == T) return rd[u - nK - 1];
+    if (u == T && v > nK && v < T) return f[v - nK - 1] - rd[v - nK - 1];
+    return 0;
+  };
+  auto cost = [&](int u, int v) -> Cost2 {
+    if (u >= 1 && u <= nK && v > nK && v < T) return C[u - 1][v - nK - 1];
+    if (u > nK && u < T && v >= 1 && v <= nK) return Cost2{-C[v - 1][u - nK - 1].d, -C[v - 1][u - nK - 1].q};
+    return Cost2{0, 0};
+  };
+  while (left > 0) {
+    if (++iters > cap) return -1;
+    for (int v = 0; v < V; ++v) {
+      dist[v] = {kInfD, 0};
+      done[v] = false;
+      prev[v] = -1;
+    }
+    dist[S] = {0, 0};
+    for (int it = 0; it < V; ++it) {   // dense Dijkstra on reduced costs (all >= 0)
+      int u = -1;
+      for (int v = 0; v < V; ++v)
+        if (!done[v] && dist[v].d < kInfD && (u < 0 || lt(dist[v], dist[u]))) u = v;
+      if (u < 0) break;
+      done[u] = true;
+      for (int v = 0; v < V; ++v) {
+        if (done[v] || rcap(u, v) <= 0) continue;
+        const Cost2 nd = add(dist[u], sub(add(cost(u, v), pot[u]), pot[v]));
+        if (dist[v].d >= kInfD || lt(nd, dist[v])) {
+          dist[v] = nd;
+          prev[v] = u;
+        }
+      }
+    }
+    if (dist[T].d >= kInfD) return -1;   // cannot happen: every cell is open
+    for (int v = 0; v < V; ++v) pot[v] = add(pot[v], (dist[v].d < kInfD && lt(dist[v], dist[T])) ? dist[v] : dist[T]);
+    long long b = kInfD;
+    for (int v = T; v != S; v = prev[v]) {
+      const long long c = rcap(prev[v], v);
+      b = c < b ? c : b;
+    }
+    for (int v = T; v != S; v = prev[v]) {
+      const int u = prev[v];
+      if (u == S) rs[v - 1] -= (int)b;
+      else if (v == T) rd[u - nK - 1] -= (int)b;
+      else if (u <= nK) x[u - 1][v - nK - 1] += (int)b;   // row -> col: more on the cell
+      else x[v - 1][u - nK - 1] -= (int)b;                // col -> row: less on the cell
+    }
+    left -= (int)b;
+  }
+  // optimal face: cells with zero reduced cost under the final potentials (optimal duals)
+  __shared__ bool tight[kMaxLevels][kMaxLevels];
+  for (int i = 0; i < nK; ++i)
+    for (int j = 0; j < nK; ++j) tight[i][j] = is_zero(sub(add(C[i][j], pot[1 + i]), pot[1 + nK + j]));
+  // lexicographically greatest x in row-major order on the face: raise x_ij along cycles
+  // row i -> col j -> row r (lower a later cell (r, j)) -> col c (raise a later tight (r, c)) -> ... -> row i
+  __shared__ int q[2 * kMaxLevels], from[2 * kMaxLevels];
+  for (int e = 0; e < nK * nK; ++e) {
+    const int i = e / nK, j = e % nK;
+    if (!tight[i][j]) continue;
+    for (;;) {
+      if (++iters > cap) return -1;
+      // BFS over nodes: rows 0..nK-1, cols nK..2nK-1; start at col j, target row i
+      for (int v = 0; v < 2 * nK; ++v) from[v] = -2;
+      int qh = 0, qt = 0;
+      q[qt++] = nK + j;
+      from[nK + j] = -1;
+      bool found = false;
+      while (qh < qt && !found) {
+        const int u = q[qh++];
+        if (u >= nK) {   // col c: lower a later cell (r, c) with x > 0
+          const int c = u - nK;
+          for (int r = 0; r < nK; ++r)
+            if (from[r] == -2 && r * nK + c > e && x[r][c] > 0) {
+              from[r] = u;
+              q[qt++] = r;
+              if (r == i) {
+                found = true;
+                break;
+              }
+            }
+        } else {         // row r: raise a later tight cell (r, c)
+          const int r = u;
+          for (int c = 0; c < nK; ++c)
+            if (from[nK + c] == -2 && r * nK + c > e && tight[r][c]) {
+              from[nK + c] = u;
+              q[qt++] = nK + c;
+            }
+        }
+      }
+      if (!found) break;
+      long long b = kInfD;
+      for (int v = i; from[v] != -1; v = from[v]) {
+        const int u = from[v];
+        if (u >= nK) {   // col u -> row v: lowered cell (v, u - nK)
+          const long long c = x[v][u - nK];
+          b = c < b ? c : b;
+        }
+      }
+      for (int v = i; from[v] != -1; v = from[v]) {
+        const int u = from[v];
+        if (u >= nK) x[v][u - nK] -= (int)b;   // lowered
+        else x[u][v - nK] += (int)b;           // raised (row u -> col v)
+      }
+      x[i][j] += (int)b;
+    }
+  }
+  return iters;
+}
+
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+
+// One warp (lanes threadIdx.x & 31 of the calling warp); hist may point to shared or global memory.
+__device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan) {
+  __shared__ int h_s[kMaxLevels], f_s[kMaxLevels], hc[kMaxLevels + 1], fc[kMaxLevels + 1];
+  __shared__ double frac_s[kMaxLevels];
+  __shared__ int x_s[kMaxLevels][kMaxLevels];
+  __shared__ int iters_s;
+  const int lane = threadIdx.x & 31;
+  const int nK = P.nK;
+  const int N = (int)P.N;
+  // ---- O5 largest remainder apportionment of N*F
+  int fl = 0;
+  double frac = -1.0;
+  if (lane < nK) {
+    h_s[lane] = hist[lane];
+    const double q = __dmul_rn((double)N, P.F[lane]);
+    const double f0 = floor(q);
+    fl = (int)f0;
+    frac = __dsub_rn(q, f0);
+    frac_s[lane] = frac;
+  }
+  const int R = N - warp_sum(lane < nK ? fl : 0);
+  __syncwarp();
+  if (lane < nK) {
+    int rank = 0;
+    for (int j = 0; j < nK; ++j) rank += (frac_s[j] > frac || (frac_s[j] == frac && j < lane)) ? 1 : 0;
+    f_s[lane] = fl + (rank < R ? 1 : 0);
+  }
+  __syncwarp();
+  if (lane == 0) {   // cumulative sums (<= 16 terms)
+    hc[0] = 0;
+    fc[0] = 0;
+    for (int i = 0; i < nK; ++i) {
+      hc[i + 1] = hc[i] + h_s[i];
+      fc[i + 1] = fc[i] + f_s[i];
+    }
+  }
+  __syncwarp();
+  // ---- O6 plan: NW-corner coupling in closed form (convex c), else the exact min-cost solver (R37)
+  if (P.convex) {
+    for (int e = lane; e < nK * nK; e += 32) {
+      const int i = e / nK, j = e % nK;
+      const int lo = max(hc[i], fc[j]), hi = min(hc[i + 1], fc[j + 1]);
+      x_s[i][j] = hi > lo ? hi - lo : 0;
+    }
+    if (lane == 0) iters_s = 0;
+  } else if (lane == 0) {
+    iters_s = mcf_plan(h_s, f_s, P, x_s);
+  }
+  __syncwarp();
+  // ---- O7 D_Q and counters
+  double dq = 0.0, lp = 0.0;
+  int n_red = 0, n_up = 0, n_down = 0;
+  const double invN = N > 0 ? __ddiv_rn(1.0, (double)N) : 0.0;
+  for (int e = lane; e < nK * nK; e += 32) {
+    const int i = e / nK, j = e % nK;
+    const int x = x_s[i][j];
+    plan->x[i][j] = x;
+    if (j != i) n_red += x;
+    if (j < i) n_up += x;
+    if (j > i) {
+      n_down += x;
+      dq = __dadd_rn(dq, __dmul_rn((double)x, P.c[P.grid[j] - P.grid[i]]));
+    }
+    // D_Q_LP: the same monotone coupling on the unrounded masses (h/N, F), context only
+    double hlo = __dmul_rn((double)hc[i], invN), hhi = __dmul_rn((double)hc[i + 1], invN);
+    double flo = 0.0, fhi = 0.0;
+    for (int jj = 0; jj < j; ++jj) flo = __dadd_rn(flo, P.F[jj]);
+    fhi = __dadd_rn(flo, P.F[j]);
+    const double ov = fmin(hhi, fhi) - fmax(hlo, flo);
+    if (j > i && ov > 0) lp = __dadd_rn(lp, __dmul_rn(ov, P.c[P.grid[j] - P.grid[i]]));
+  }
+  dq = warp_sum_fixed(dq);
+  lp = warp_sum_fixed(lp);
+  n_red = warp_sum(n_red);
+  n_up = warp_sum(n_up);
+  n_down = warp_sum(n_down);
+  __syncwarp();
+  if (lane < nK) {   // row prefix tables and class starts
+    const int i = lane;
+    plan->h[i] = h_s[i];
+    plan->f[i] = f_s[i];
+    plan->class_start[i] = hc[i];
+    int acc = 0;
+    for (int j = 0; j < nK; ++j) {
+      acc += x_s[i][j];
+      plan->X[i][j] = acc;
+    }
+    // I_j: ascending instance ids at level j, and the multiply-high constant for div n_j
+    int n = 0;
+    for (int w = 0; w < P.W; ++w)
+      if (P.inst_level[w] == i) plan->inst_list[i][n++] = w;
+    plan->n_inst[i] = n;
+    const uint64_t d = n > 0 ? (uint64_t)n : 1;
+    plan->n_inst_magic[i] = ((1ull << 32) + d - 1) / d;
+  }
+  if (lane == 0) {
+    plan->class_start[nK] = hc[nK];
+    plan->D_Q = N > 0 ? __ddiv_rn(dq, (double)N) : 0.0;
+    plan->D_Q_LP = P.convex ? lp : __longlong_as_double(0x7FF8000000000000LL);
+    plan->solver_iters = iters_s;
+    plan->n_redirected = n_red;
+    plan->n_upgraded = n_up;
+    plan->n_downgraded = n_down;
+  }
+}
+
+}  // namespace
+}  // namespace pas

@@ -94,6 +94,7 @@ _SIG = {
     "pas_set_fractions": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int]),
     "pas_set_seed": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
     "pas_set_collectives": (C.c_int, [_P, C.c_int]),
+    "pas_set_graph": (C.c_int, [_P, C.c_int]),
     "pas_stage_ring": (C.c_int, [_P, C.c_int]),
     "pas_stage_ring_read": (C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "pas_set_forecast": (C.c_int, [_P, C.c_int, C.c_int]),
@@ -236,6 +237,10 @@ PAS_COLL_FOLDED, PAS_COLL_EXPLICIT = 0, 1
 
 def pas_set_collectives(ctx, mode):
     _check(ctx, lib.pas_set_collectives(ctx, mode))
+
+
+def pas_set_graph(ctx, on=True):
+    _check(ctx, lib.pas_set_graph(ctx, 1 if on else 0))
 
 
 def pas_stage_ring(ctx, slots):

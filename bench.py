@@ -46,6 +46,8 @@ def parse():
                          "rebuilt every batch, i.i.d. Philox K' (0: the exact per-batch plan)")
     ap.add_argument("--force-collective", action="store_true",
                     help="use the NCCL all-gather path even with one rank (transport self-test)")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay each batch as a captured CUDA graph (pas_set_graph; stage times then total only)")
     ap.add_argument("--collectives", default="folded", choices=["folded", "explicit"],
                     help="G > 1: folded (N1 all-gather, every rank merges all N) or explicit (N1 + slice merge + "
                          "N2 all-reduce of H_K + N3 all-gather), pas_set_collectives")
@@ -278,6 +280,8 @@ def main():
         pas.pas_set_collectives(router.ctx, pas.PAS_COLL_EXPLICIT if args.collectives == "explicit"
                                 else pas.PAS_COLL_FOLDED)
     gap_us = 0
+    if args.graph:
+        pas.pas_set_graph(router.ctx, True)
     if args.forecast:
         router.set_forecast(args.forecast, 1)
     if args.dispatcher:
@@ -346,9 +350,10 @@ def main():
     stages = pas.pas_stage_ring_read(router.ctx, args.steps)
     pas.pas_stage_ring(router.ctx, 0)
     stage_sum = [sum(r[i] for r in stages) for i in range(7)]
+    n_st = max(1, len(stages))        # 0 in graph mode: a replayed batch is timed as a whole
     total_ms = sum(step_ms) if flush is not None else ev0.elapsed_time(ev1)
     total_ms = max_over_ranks(total_ms, dist, dev, torch)
-    k2_ms = max_over_ranks(stage_sum[1] / len(stages), dist, dev, torch)
+    k2_ms = max_over_ranks(stage_sum[1] / n_st, dist, dev, torch) if stages else None
     value = N * args.steps / (total_ms / 1e3)
     q = statistics.quantiles(step_ms, n=10) if len(step_ms) >= 2 else [step_ms[0]] * 9
     step_stats = {"median": statistics.median(step_ms), "p10": q[0], "p90": q[-1], "min": min(step_ms),
@@ -379,7 +384,7 @@ def main():
 
     peaks, peak_src = measured_peaks()
     flops = 2.0 * N * M_local * cfg.d
-    achieved = flops / (k2_ms / 1e3) / 1e12
+    achieved = flops / (k2_ms / 1e3) / 1e12 if k2_ms else None
     peak, peak_kind = select_peak(peaks, clk)
     traffic = profiled_traffic(args.config, G)
     line = {
@@ -392,18 +397,20 @@ def main():
                    "instances": len(cfg.instance_level), "mode": "uniform" if cfg.mode else "greedy",
                    "bstar": cfg.bstar, "dispatcher": "stateful (f3)" if args.dispatcher else "stateless (R13)",
                    "plan": f"forecast (f1, window {args.forecast})" if args.forecast else "exact per batch",
+                   "launch": "CUDA graph replay" if args.graph else "eager",
                    "parallelism": f"cache row-sharded x{G}" + ((" + NCCL all-gather" if args.collectives == "folded" else
                                                                    " + NCCL all-gather / all-reduce H_K / all-gather (explicit N2)")
                                                                   if G > 1 else ""),
                    "l2": l2_note},
         "roofline": {"kernel": "k_simtopk (K2: tcgen05 similarity GEMM + fused top-k)", "bound": "tensor",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "peak_source": f"{peak_kind}, {peak_src}",
                      "algorithmic": f"2*N*M_per_gpu*d = {flops:.4g} flop per launch / mean K2 event time "
-                                    f"{k2_ms:.3f} ms"},
+                                    + (f"{k2_ms:.3f} ms" if k2_ms else "n/a (graph replay: no per-stage events)")},
         "step_ms": step_stats,
         "value_median": N / (step_stats["median"] / 1e3),
-        "stages_ms": {n: round(stage_sum[i] / len(stages), 4) for i, n in enumerate(
+        "stages_ms": {n: round(stage_sum[i] / n_st, 4) for i, n in enumerate(
             ["normalise", "similarity_topk", "merge_collective_optimalK", "plan", "redirect", "route_and_batch",
              "total"])},
         "e2e": e2e,

@@ -142,6 +142,9 @@ typedef struct {
    * and for the dynamic schedule the cache tiles per chunk and the chunk steps per range (0, 0: the
    * static schedule, one unit per (prompt tile, range)) */
   int k2_ranges, k2_chunk_tiles, k2_chunk_steps;
+  /* K6 (a7): 1 if the windowed split search fell back to the exact histogram path for this batch (a split
+   * rank outside its kappa window -- probability ~1e-15 --, a list overflow, > 32 splits, or forced) */
+  int k6_fallback;
 } pas_stats;
 
 /* Library and build identification ("sm_100a", version). Never fails. */

@@ -80,27 +80,30 @@ __device__ __forceinline__ void column_counts(int32_t* cnt, int nC, const int (&
 }
 
 __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict__ cls, int64_t N, int ntiles,
-                                                       int nC, int32_t* __restrict__ counts /*[nC][ntiles]*/) {
+                                                       int nC, int32_t* __restrict__ counts /*[nC][ntiles]*/,
+                                                       const int* __restrict__ gate) {
   pdl_entry();
+  // gate: K6's windowed pass already wrote the counts unless it fell back to the exact path
+  if (gate && *reinterpret_cast<const volatile int*>(gate) == 0) return;
   extern __shared__ int32_t cnt[];      // [nC][THREADS]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int v[PER], r[PER];
-  load_cls(cls, (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * PER, N, v);
-  column_counts(cnt, nC, v, r);
-  __syncthreads();
-  for (int c = w; c < nC; c += WARPS) {   // one warp per class: sum its row
-    int sum = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {   // gated launches use a capped grid
+    int v[PER], r[PER];
+    load_cls(cls, (int64_t)tile * TILE + (int64_t)threadIdx.x * PER, N, v);
+    __syncthreads();   // the previous tile's row sums have read the columns
+    column_counts(cnt, nC, v, r);
+    __syncthreads();
+    for (int c = w; c < nC; c += WARPS) {   // one warp per class: sum its row
+      int sum = 0;
 #pragma unroll
-    for (int i = 0; i < THREADS / 32; ++i) sum += cnt[c * THREADS + lane + 32 * i];
+      for (int i = 0; i < THREADS / 32; ++i) sum += cnt[c * THREADS + lane + 32 * i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) counts[(int64_t)c * ntiles + blockIdx.x] = sum;
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) counts[(int64_t)c * ntiles + tile] = sum;
+    }
   }
 }
 
-#ifndef PAS_K7_BALLOT
-#define PAS_K7_BALLOT 0   // 1: in-row ranking by class-bit ballots (<= 32 classes; measured slower: 297 vs 261 us)
-#endif
 #ifndef PAS_K7_MINB
 #define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers, no spills
 #endif
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
 // path; compile-time so the per-row loop carries no mode branches or parameter reloads): 0 greedy with
 // b* a power of two, 1 greedy with any b*, 2 uniform.  The DISP instantiation reads P.mode.
 template <bool DISP, int MODE>
-__global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(const uint8_t* __restrict__ cls, const RouteParams P,
+__global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(const uint8_t* __restrict__ cls, const __grid_constant__ RouteParams P,
                                                       int ntiles, int nC, const int32_t* __restrict__ scanned,
                                                       DevPlan* __restrict__ plan, int32_t* __restrict__ instance,
                                                       int32_t* __restrict__ slot, int32_t* __restrict__ prompts,
@@ -194,41 +197,15 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   // the rank is packed above the class byte (c[j] = rank << 8 | class, class 0xFF past the end): one
   // register per row instead of two
   const unsigned lt = (1u << lane) - 1;
-  if (PAS_K7_BALLOT && nC <= 32) {
-    // multisplit by class bits: nb ballots per row give every lane the mask of its own class's lanes
-    // and the mask of the lanes of class `lane`; lane L keeps the warp's running count of class L in a
-    // register (no shared memory, no per-row warp syncs)
-    int nb = 0;
-    while ((1 << nb) < nC) ++nb;
-    int run = 0;
 #pragma unroll
-    for (int j = 0; j < ROWS; ++j) {
-      const int cj = c[j];
-      unsigned own = __ballot_sync(0xffffffffu, cj >= 0), mine = own;
-#pragma unroll
-      for (int b = 0; b < 5; ++b) {
-        if (b >= nb) break;
-        const unsigned bb = __ballot_sync(0xffffffffu, (cj >> b) & 1);
-        own &= ((cj >> b) & 1) ? bb : ~bb;
-        mine &= ((lane >> b) & 1) ? bb : ~bb;
-      }
-      const int before = __shfl_sync(0xffffffffu, run, cj & 31);
-      run += __popc(mine);
-      const int r = cj >= 0 ? before + __popc(own & lt) : 0;
-      c[j] = (r << 8) | (cj & 0xFF);
-    }
-    if (lane < nC) wcnt[w][lane] = run;
-  } else {
-#pragma unroll
-    for (int j = 0; j < ROWS; ++j) {
-      const unsigned m = __match_any_sync(0xffffffffu, c[j]);
-      const bool lead = lane == __ffs(m) - 1;
-      const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
-      __syncwarp();
-      if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
-      __syncwarp();
-      c[j] = (r << 8) | (c[j] & 0xFF);
-    }
+  for (int j = 0; j < ROWS; ++j) {
+    const unsigned m = __match_any_sync(0xffffffffu, c[j]);
+    const bool lead = lane == __ffs(m) - 1;
+    const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
+    __syncwarp();
+    if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
+    __syncwarp();
+    c[j] = (r << 8) | (c[j] & 0xFF);
   }
   __syncthreads();
   if (threadIdx.x < nC) {   // per class: the tile's offset plus the exclusive prefix over warps
@@ -274,6 +251,7 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
       sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
     }
     if (!DISP) pos = sl;
+    PAS_CHECK(inst >= 0 && inst < P.W && pos >= 0 && ioff[inst] + pos < ioff[inst + 1], "K7 batch-list position");
     inst_w[32 * j] = inst;
     slot_w[32 * j] = sl;
     if (prompts) prompts[ioff[inst] + pos] = p_w + 32 * j;   // the batch lists (counting-sort scatter)
@@ -292,14 +270,16 @@ cudaError_t batch_init() {
   return e;
 }
 
-cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan, const BatchWs& w,
+cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan, const int* count_gate,
+                                   const BatchWs& w,
                                    int32_t* instance, int32_t* slot, int32_t* bucket_offsets,
                                    int32_t* bucket_prompts, cudaStream_t st, int* launches) {
   if (p.N <= 0) return cudaSuccess;
   const int ntiles = batch_tiles(p.N);
   const int nclasses = p.mode == PAS_UNIFORM ? p.W : p.nK;
   const size_t smem = (size_t)nclasses * THREADS * sizeof(int32_t);
-  launch_pdl(k_cls_count, ntiles, THREADS, smem, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts);
+  const int cgrid = count_gate && ntiles > kNumSMs * 4 ? kNumSMs * 4 : ntiles;   // gated: capped, grid-stride
+  launch_pdl(k_cls_count, cgrid, THREADS, smem, st, r.cls7, p.N, ntiles, nclasses, w.blk_counts, count_gate);
   cudaError_t e = launch_exclusive_scan(w.blk_counts, w.blk_off, nclasses * ntiles, w.scan_tmp, st, launches);
   if (e != cudaSuccess) return e;
   if (p.disp) {   // f3: queue events since the last batch, pick tables, counts, state after

@@ -49,7 +49,7 @@ __device__ int64_t disp_advance(int64_t& Q, int64_t base, int64_t& fp, int64_t& 
   return B;
 }
 
-__global__ void __launch_bounds__(kMaxInst) k_disp_prep(const RouteParams P, int ntiles, int nC,
+__global__ void __launch_bounds__(kMaxInst) k_disp_prep(const __grid_constant__ RouteParams P, int ntiles, int nC,
                                                         const int32_t* __restrict__ scanned) {
   pdl_entry();
   DispState* S = P.dstate;

@@ -34,7 +34,7 @@ __device__ void fill_instance_lists(const RouteParams& P, DevPlan* plan, int lan
   }
 }
 
-__global__ void __launch_bounds__(32) k_fc_plan(const int* __restrict__ hist, const RouteParams P,
+__global__ void __launch_bounds__(32) k_fc_plan(const int* __restrict__ hist, const __grid_constant__ RouteParams P,
                                                 DevPlan* __restrict__ plan, FcState* __restrict__ fcs, int replan) {
   pdl_entry();
   const int lane = threadIdx.x;
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(32) k_fc_plan(const int* __restrict__ hist, co
   fcs->n_unforecast = 0;
 }
 
-__global__ void __launch_bounds__(256) k_fc_sample(const uint8_t* __restrict__ level, const RouteParams P,
+__global__ void __launch_bounds__(256) k_fc_sample(const uint8_t* __restrict__ level, const __grid_constant__ RouteParams P,
                                                    DevPlan* __restrict__ plan, FcState* __restrict__ fcs,
                                                    int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7) {
   pdl_entry();
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_fc_sample(const uint8_t* __restrict__ l
   if (threadIdx.x == 0 && unf) atomicAdd(&fcs->n_unforecast, unf);
 }
 
-__global__ void __launch_bounds__(1024) k_fc_window(const uint8_t* __restrict__ level, const RouteParams P,
+__global__ void __launch_bounds__(1024) k_fc_window(const uint8_t* __restrict__ level, const __grid_constant__ RouteParams P,
                                                     DevPlan* __restrict__ plan, FcState* __restrict__ fcs,
                                                     uint8_t* __restrict__ ring, int window) {
   pdl_entry();

@@ -159,7 +159,7 @@ __device__ __forceinline__ void flush_tally(const RouteParams& P, const SelectOu
 // Warp per prompt (any S <= 128).
 __global__ void __launch_bounds__(WARPS * 32) k_merge_select(const Cand* __restrict__ in, int S,
                                                              const uint8_t* __restrict__ pflags,
-                                                             const RouteParams P, SelectOut o) {
+                                                             const __grid_constant__ RouteParams P, SelectOut o) {
   pdl_entry();
   __shared__ Cand res[WARPS][PAS_MAX_TOPK];
   Tally ty;
@@ -197,7 +197,7 @@ constexpr int TP_MAXSK = 32;
 
 __global__ void __launch_bounds__(TP_THREADS) k_merge_select_thr(const Cand* __restrict__ in, int S,
                                                                  const uint8_t* __restrict__ pflags,
-                                                                 const RouteParams P, SelectOut o) {
+                                                                 const __grid_constant__ RouteParams P, SelectOut o) {
   pdl_entry();
   extern __shared__ __align__(16) Cand sm[];   // S * 128 * (k + 1) pairs (dynamic, padded rows)
   // after the merge the staging buffer is reused for the outgoing ids and scores (rows padded to k+1
@@ -286,7 +286,7 @@ constexpr int S1_THREADS = 256;
 constexpr int S1_UNROLL = PAS_S1_UNROLL;
 template <int HALF>
 __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict__ in,
-                                                          const uint8_t* __restrict__ pflags, const RouteParams P,
+                                                          const uint8_t* __restrict__ pflags, const __grid_constant__ RouteParams P,
                                                           SelectOut o) {
   pdl_entry();
   Tally ty;
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(S1_THREADS) k_select_s1(const int4* __restrict
 __global__ void __launch_bounds__(256) k_unpack_slices(const Cand* __restrict__ all_cand,
                                                        const int32_t* __restrict__ all_K,
                                                        const uint8_t* __restrict__ all_level,
-                                                       const uint8_t* __restrict__ all_flags, const RouteParams P,
+                                                       const uint8_t* __restrict__ all_flags, const __grid_constant__ RouteParams P,
                                                        SelectOut o) {
   pdl_entry();
   const int k = P.topk;
@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(256) k_unpack_slices(const Cand* __restrict__ 
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const Cand c = all_cand[e];
+    PAS_CHECK(c.g < P.M_total, "explicit-N2 gathered candidate");
     if (o.topk_id) o.topk_id[e] = c.g;
     if (o.topk_score) o.topk_score[e] = c.s;
     const int64_t p = e / k;

@@ -21,6 +21,22 @@
 // Per prompt: level 1 B read twice, kappa 8 B written + read, K' 4 B + K7 class 1 B written; plus one
 // L2 atomic.  The previous full counting-sort ranking (scatter + in-bucket rank of all N entries)
 // moved 53 B per prompt through scattered accesses (8.8 ms at 64M prompts).
+//
+// Windowed split search (the default since round 2; the histogram path above is its exact fallback):
+// kappa is uniform, so the kappa of the prompt at class rank X lies, with probability 1 - 1e-15, in a
+// window of +- 8 sd around the X-th order statistic of h uniforms (K5 computes the windows, merged into
+// zones: pas_internal.cuh DevPlan).  A prompt whose kappa falls OUTSIDE every zone of its class has its
+// K' fixed by the zones below it alone -- every split in them has a smaller kappa -- so
+//   k6_fused   one streaming pass, 4,096 prompts per CTA (K7's tiles): Philox, zone test, K' and the K7
+//              class for the outside prompts, (kappa, p) appended to the zone's list for the inside ones
+//              (~8 sqrt(h) per split: 0.1 % at 64M prompts), per-(class, gap) counts, and K7's per-tile
+//              class counts (so k_cls_count only runs on the fallback);
+//   k6_zone    one CTA per zone: the zone's class prompts below it (gap counts + lower zones), each
+//              split's rank inside the zone located through a 2,048-bucket histogram and an exact
+//              (kappa, p) selection in its bucket, then every entry's K', class and tile count.
+// If a split rank falls outside its zone (or a list overflows, or there are > 32 splits) the
+// flag DevPlan::k6_fallback is set and the histogram path below (gated kernels, no-ops otherwise)
+// recomputes every K' exactly.  Per prompt: level 1 B read, K' 4 B + class 1 B written: 6 B.
 #include "pas_internal.cuh"
 #include "philox.cuh"
 
@@ -32,6 +48,9 @@ constexpr int RT = 256;
 #define PAS_K6_GRIDCAP 1   // k6_assign: grid capped at 8 CTAs per SM (grid-stride); 0: uncapped
 #endif
 constexpr int kSmemList = 2048;   // k6_resolve: entries staged in shared memory (else read from L2)
+// The windowed split search serves N >= kWindowMinN; below, its fixed launch cost (fused pass, zone
+// kernels, gated fallback launches) exceeds what it saves, and the exact histogram path runs alone.
+constexpr int64_t kWindowMinN = 1 << 18;
 
 __device__ __forceinline__ bool entry_less(uint64_t ka, int32_t pa, uint64_t kb, int32_t pb) {
   return ka < kb || (ka == kb && pa < pb);
@@ -55,22 +74,39 @@ __device__ __forceinline__ void emit(const RouteParams& P, const int* grid, cons
   }
 }
 
-__global__ void __launch_bounds__(RT) k6_hist(const uint8_t* __restrict__ level, const RouteParams P,
-                                              uint64_t* __restrict__ key, int32_t* __restrict__ hist) {
+// Fallback gate: the histogram kernels run only when the windowed pass could not decide every prompt.
+__device__ __forceinline__ bool gated_off(const int* gate) {
+  return gate && *reinterpret_cast<const volatile int*>(gate) == 0;
+}
+
+__global__ void __launch_bounds__(RT) k6_zero(const int* __restrict__ gate, int32_t* __restrict__ a, int64_t n,
+                                              int32_t* __restrict__ b, int nb) {
   pdl_entry();
-  const int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x;
-  if (p >= P.N) return;
-  const uint4 w = philox_stream(P.seed, batch_seq_of(P), (uint32_t)p, kStreamRedirect);
-  const uint64_t kappa = (((uint64_t)w.y << 32) | w.x) >> 4;
-  key[p] = kappa;
-  atomicAdd(&hist[((uint32_t)level[p] << P.kb) | top_bits(kappa, P.kb)], 1);
+  if (gated_off(gate)) return;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) a[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < nb) b[threadIdx.x] = 0;
+}
+
+__global__ void __launch_bounds__(RT) k6_hist(const uint8_t* __restrict__ level, const __grid_constant__ RouteParams P,
+                                              const int* __restrict__ gate, uint64_t* __restrict__ key,
+                                              int32_t* __restrict__ hist) {
+  pdl_entry();
+  if (gated_off(gate)) return;   // a capped grid (grid-stride): a gated-off launch costs ~a microsecond
+  const uint64_t bseq = batch_seq_of(P);
+  for (int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x; p < P.N; p += (int64_t)gridDim.x * RT) {
+    const uint4 w = philox_stream(P.seed, bseq, (uint32_t)p, kStreamRedirect);
+    const uint64_t kappa = (((uint64_t)w.y << 32) | w.x) >> 4;
+    key[p] = kappa;
+    atomicAdd(&hist[((uint32_t)level[p] << P.kb) | top_bits(kappa, P.kb)], 1);
+  }
 }
 
 // Per (class, chunk of kChunks) sums of the bucket counts, coalesced, many CTAs.
 constexpr int kChunks = 256;
-__global__ void __launch_bounds__(RT) k6_chunks(const RouteParams P, const int32_t* __restrict__ hist,
-                                                int32_t* __restrict__ csum) {
+__global__ void __launch_bounds__(RT) k6_chunks(const __grid_constant__ RouteParams P, const int* __restrict__ gate,
+                                                const int32_t* __restrict__ hist, int32_t* __restrict__ csum) {
   pdl_entry();
+  if (gated_off(gate)) return;
   __shared__ int32_t ws[RT / 32];
   const int i = blockIdx.x / kChunks, c = blockIdx.x % kChunks;
   const int nb = 1 << P.kb, len = (nb + kChunks - 1) / kChunks;
@@ -90,11 +126,12 @@ __global__ void __launch_bounds__(RT) k6_chunks(const RouteParams P, const int32
 
 // One CTA per class: the chunk holding each split rank (scan of the chunk sums), then one warp per
 // split walks that chunk 32 buckets at a time (warp scan) to the bucket and the split's rank in it.
-__global__ void __launch_bounds__(RT) k6_bounds(const RouteParams P, const DevPlan* __restrict__ plan,
+__global__ void __launch_bounds__(RT) k6_bounds(const __grid_constant__ RouteParams P, const DevPlan* __restrict__ plan,
                                                 const int32_t* __restrict__ hist, const int32_t* __restrict__ csum,
                                                 K6Bounds* __restrict__ bnd, K6List* __restrict__ lists,
-                                                int32_t* __restrict__ used) {
+                                                int32_t* __restrict__ used, const int* __restrict__ gate) {
   pdl_entry();
+  if (gated_off(gate)) return;
   __shared__ int32_t cex[kChunks + 1];
   __shared__ int32_t sb[kMaxLevels], so[kMaxLevels];
   const int i = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -178,11 +215,12 @@ __global__ void __launch_bounds__(RT) k6_bounds(const RouteParams P, const DevPl
 }
 
 __global__ void __launch_bounds__(RT) k6_assign(const uint8_t* __restrict__ level, const uint64_t* __restrict__ key,
-                                                const RouteParams P, const DevPlan* __restrict__ plan,
+                                                const __grid_constant__ RouteParams P, const DevPlan* __restrict__ plan,
                                                 const K6Bounds* __restrict__ bnd, K6List* __restrict__ lists,
                                                 KeyEntry* __restrict__ cand, int32_t* __restrict__ K_prime,
-                                                uint8_t* __restrict__ cls7) {
+                                                uint8_t* __restrict__ cls7, const int* __restrict__ gate) {
   pdl_entry();
+  if (gated_off(gate)) return;
   __shared__ int32_t sb[kMaxLevels][kMaxLevels], sl[kMaxLevels][kMaxLevels];
   __shared__ int grid_s[kMaxLevels];
   if (threadIdx.x < kMaxLevels) grid_s[threadIdx.x] = P.grid[threadIdx.x];
@@ -211,11 +249,13 @@ __global__ void __launch_bounds__(RT) k6_assign(const uint8_t* __restrict__ leve
   }
 }
 
-__global__ void __launch_bounds__(RT) k6_resolve(const RouteParams P, const DevPlan* __restrict__ plan,
+__global__ void __launch_bounds__(RT) k6_resolve(const __grid_constant__ RouteParams P, const DevPlan* __restrict__ plan,
                                                  const K6Bounds* __restrict__ bnd, const K6List* __restrict__ lists,
                                                  const int32_t* __restrict__ used, const KeyEntry* __restrict__ cand,
-                                                 int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7) {
+                                                 int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7,
+                                                 const int* __restrict__ gate) {
   pdl_entry();
+  if (gated_off(gate)) return;
   __shared__ uint64_t sk[kSmemList];
   __shared__ int32_t sp[kSmemList];
   __shared__ int grid_s[kMaxLevels];
@@ -243,6 +283,241 @@ __global__ void __launch_bounds__(RT) k6_resolve(const RouteParams P, const DevP
   }
 }
 
+// ---- windowed split search -----------------------------------------------------------------------
+constexpr int FT = 256;                 // k6_fused threads; 16 consecutive prompts each = one K7 tile
+constexpr int FPER = 16;
+constexpr int kSlots = kMaxLevels + kMaxZones;   // (class, gap) slots
+
+// Private byte counter columns in shared memory (the column is the thread: no atomics, no conflicts).
+template <int NCLS>
+__global__ void __launch_bounds__(FT) k6_fused(const uint8_t* __restrict__ level, const __grid_constant__ RouteParams P,
+                                               DevPlan* __restrict__ plan, KeyEntry* __restrict__ cand,
+                                               int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7,
+                                               int32_t* __restrict__ blk_counts, int ntiles) {
+  pdl_entry();
+  __shared__ uint64_t zlo[kMaxZones], zhi[kMaxZones];
+  __shared__ int zjb[kMaxZones], zcap[kMaxZones], zbase[kMaxZones];
+  __shared__ int cz0[kMaxLevels], cnz[kMaxLevels], cjt[kMaxLevels], cs0[kMaxLevels];
+  __shared__ int grid_s[kMaxLevels];
+  __shared__ uint8_t gcol[kSlots][FT];      // (class, gap) counts per thread (<= 16 each)
+  __shared__ uint8_t ccol[NCLS][FT];        // K7 class counts per thread
+  const int t = threadIdx.x;
+  if (t < kMaxZones) {
+    zlo[t] = plan->z_lo[t];
+    zhi[t] = plan->z_hi[t];
+    zjb[t] = plan->z_jbelow[t];
+    zcap[t] = plan->z_cap[t];
+    zbase[t] = plan->z_base[t];
+  }
+  if (t < kMaxLevels) {
+    cz0[t] = plan->cls_zone0[t];
+    cnz[t] = t < P.nK ? plan->cls_nzone[t] : 0;
+    cjt[t] = plan->cls_jtot[t];
+    cs0[t] = plan->cls_slot0[t];
+    grid_s[t] = P.grid[t];
+  }
+  for (int q = 0; q < kSlots; ++q) gcol[q][t] = 0;
+  for (int q = 0; q < NCLS; ++q) ccol[q][t] = 0;
+  __syncthreads();
+  const uint64_t bseq = batch_seq_of(P);
+  // the tile's prompts in warp-coalesced order: p = tile base + e * 256 + t (level loads, K' and class
+  // stores 32 consecutive per warp instruction); the counters are per thread, so the order is free
+  const int64_t p0 = (int64_t)blockIdx.x * (FT * FPER) + t;
+  bool overflow = false;
+#pragma unroll 4
+  for (int e = 0; e < FPER; ++e) {
+    const int64_t p = p0 + (int64_t)e * FT;
+    if (p >= P.N) break;
+    const int i = __ldg(level + p);
+    const uint4 w = philox_stream(P.seed, bseq, (uint32_t)p, kStreamRedirect);
+    const uint64_t kappa = (((uint64_t)w.y << 32) | w.x) >> 4;
+    const int z0 = cz0[i], nz = cnz[i];
+    int g = 0;
+    bool inside = false;
+    for (; g < nz; ++g) {
+      if (kappa < zlo[z0 + g]) break;
+      if (kappa < zhi[z0 + g]) {
+        inside = true;
+        break;
+      }
+    }
+    if (inside) {
+      const int z = z0 + g;
+      const int slot = atomicAdd(&plan->z_fill[z], 1);
+      PAS_CHECK(zbase[z] + zcap[z] <= P.N, "K6 zone list beyond N");
+      if (slot < zcap[z]) cand[zbase[z] + slot] = KeyEntry{kappa, (int32_t)p, 0};
+      else overflow = true;
+      continue;
+    }
+    PAS_CHECK(i < P.nK && cs0[i] + g < kSlots, "K6 gap slot");
+    ++gcol[cs0[i] + g][t];
+    const int j = g < nz ? zjb[z0 + g] : cjt[i];
+    PAS_CHECK(j < P.nK, "K6 K' level");
+    K_prime[p] = grid_s[j];
+    int c = j;
+    if (NCLS > kMaxLevels) {   // uniform: the instance I_j[(u n_j) >> 32]
+      const uint4 u = philox_stream(P.seed, bseq, (uint32_t)p, kStreamUniform);
+      c = plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)plan->n_inst[j]) >> 32)];
+    }
+    cls7[p] = (uint8_t)c;
+    ++ccol[c][t];
+  }
+  if (overflow) plan->k6_fallback = 1;
+  __syncthreads();
+  // column sums: one warp per counter row
+  const int lane = t & 31, wp = t >> 5;
+  const int nslots = cs0[P.nK - 1] + cnz[P.nK - 1] + 1;
+  const int nC = NCLS > kMaxLevels ? P.W : P.nK;
+  for (int q = wp; q < nslots + nC; q += FT / 32) {
+    const uint8_t* row = q < nslots ? gcol[q] : ccol[q - nslots];
+    int sum = 0;
+#pragma unroll
+    for (int r = 0; r < FT / 32; ++r) sum += row[lane + 32 * r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      if (q < nslots) {
+        if (sum) atomicAdd(&plan->gapcnt[q], sum);
+      } else {
+        blk_counts[(int64_t)(q - nslots) * ntiles + blockIdx.x] = sum;   // the zone entries are added later
+      }
+    }
+  }
+}
+
+constexpr int ZT = 1024;          // k6_zone threads
+constexpr int ZB = 2048;          // buckets over a zone
+constexpr int kZoneSel = 2048;    // bucket entries staged for the exact selection (mean ~32 at 64M prompts)
+
+// One CTA per zone: locate each split's threshold entry (the prompt at its class rank X) -- the zone's
+// class prompts below it (gap counts + lower zones), a 2,048-bucket histogram of the zone's entries, the
+// bucket holding rank X, an exact (kappa, p) selection inside that bucket -- into the DevPlan.
+__global__ void __launch_bounds__(ZT, 1) k6_zone_select(DevPlan* __restrict__ plan, const KeyEntry* __restrict__ cand) {
+  pdl_entry();
+  __shared__ int hist[ZB + 1];
+  __shared__ int wsum[ZT / 32];
+  __shared__ uint64_t sel_k[kZoneSel];
+  __shared__ int sel_p[kZoneSel];
+  __shared__ int nsel;
+  const int z = blockIdx.x, t = threadIdx.x;
+  if (z >= plan->k6_nz || *reinterpret_cast<const volatile int*>(&plan->k6_fallback)) return;
+  const int i = plan->z_cls[z];
+  const int n = plan->z_fill[z];
+  if (n > plan->z_cap[z]) return;   // overflow: k6_fused has set the fallback
+  const KeyEntry* E = cand + plan->z_base[z];
+  const uint64_t lo = plan->z_lo[z], width = plan->z_hi[z] - lo;
+  int shift = 0;                     // bucket = (kappa - lo) >> shift, < ZB
+  while ((width - 1) >> shift >= (uint64_t)ZB) ++shift;
+  // class prompts below the zone: gaps 0..g and the lower zones of the class
+  const int zi = z - plan->cls_zone0[i];
+  int below = 0;
+  for (int g = 0; g <= zi; ++g) below += plan->gapcnt[plan->cls_slot0[i] + g];
+  for (int y = plan->cls_zone0[i]; y < z; ++y) below += plan->z_fill[y];
+  for (int b = t; b <= ZB; b += ZT) hist[b] = 0;
+  __syncthreads();
+  for (int e = t; e < n; e += ZT) atomicAdd(&hist[(int)((E[e].key - lo) >> shift)], 1);
+  __syncthreads();
+  {   // exclusive scan of hist[0..ZB) in place (2 buckets per thread), hist[ZB] = n
+    const int a0 = hist[2 * t], a1 = hist[2 * t + 1];
+    int v = a0 + a1, incl = v;
+    const int lane = t & 31, wp = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[wp] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int q = 0; q < wp; ++q) before += wsum[q];
+    const int ex = before + incl - v;
+    __syncthreads();
+    hist[2 * t] = ex;
+    hist[2 * t + 1] = ex + a0;
+    if (t == ZT - 1) hist[ZB] = ex + v;
+  }
+  __syncthreads();
+  const int s0 = plan->z_first[z], ns = plan->z_nsplit[z];
+  for (int s = 0; s < ns; ++s) {
+    const int r = plan->s_X[s0 + s] - below;
+    if (r < 0 || r >= n) {   // the split's kappa lies outside its window: exact fallback
+      if (t == 0) plan->k6_fallback = 1;
+      return;                 // uniform across the CTA (r, n are block-uniform)
+    }
+    int b = 0;                // the last bucket with hist[b] <= r
+    for (int step = ZB / 2; step > 0; step >>= 1)
+      if (hist[b + step] <= r) b += step;
+    if (t == 0) nsel = 0;
+    __syncthreads();
+    for (int e = t; e < n; e += ZT)
+      if ((int)((E[e].key - lo) >> shift) == b) {
+        const int q = atomicAdd(&nsel, 1);
+        if (q < kZoneSel) {
+          sel_k[q] = E[e].key;
+          sel_p[q] = E[e].p;
+        }
+      }
+    __syncthreads();
+    const int m = nsel, want = r - hist[b];
+    if (m > kZoneSel) {
+      if (t == 0) plan->k6_fallback = 1;
+      return;
+    }
+    for (int e = t; e < m; e += ZT) {   // the entry of rank `want` in the bucket by (kappa, p)
+      int rk = 0;
+      for (int f = 0; f < m; ++f) rk += entry_less(sel_k[f], sel_p[f], sel_k[e], sel_p[e]);
+      if (rk == want) {
+        plan->s_thr_k[s0 + s] = sel_k[e];
+        plan->s_thr_p[s0 + s] = sel_p[e];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Every zone entry, spread over many CTAs (blockIdx.y = zone): K' level = the level below the zone +
+// the splits of the zone at or below it; K7 class and tile count.
+template <int NCLS>
+__global__ void __launch_bounds__(RT) k6_zone_apply(const __grid_constant__ RouteParams P, const DevPlan* __restrict__ plan,
+                                                    const KeyEntry* __restrict__ cand, int32_t* __restrict__ K_prime,
+                                                    uint8_t* __restrict__ cls7, int32_t* __restrict__ blk_counts,
+                                                    int ntiles) {
+  pdl_entry();
+  const int z = blockIdx.y;
+  if (z >= plan->k6_nz || *reinterpret_cast<const volatile int*>(&plan->k6_fallback)) return;
+  const int n = plan->z_fill[z];
+  if (n > plan->z_cap[z]) return;
+  __shared__ uint64_t tk[kMaxZones];
+  __shared__ int tp[kMaxZones], tm[kMaxZones];
+  const int s0 = plan->z_first[z], ns = plan->z_nsplit[z];
+  if (threadIdx.x < ns) {
+    tk[threadIdx.x] = plan->s_thr_k[s0 + threadIdx.x];
+    tp[threadIdx.x] = plan->s_thr_p[s0 + threadIdx.x];
+    tm[threadIdx.x] = plan->s_mult[s0 + threadIdx.x];
+  }
+  __syncthreads();
+  const KeyEntry* E = cand + plan->z_base[z];
+  const int jb = plan->z_jbelow[z];
+  const uint64_t bseq = batch_seq_of(P);
+  for (int e = blockIdx.x * RT + threadIdx.x; e < n; e += gridDim.x * RT) {
+    const uint64_t k = E[e].key;
+    const int p = E[e].p;
+    int j = jb;
+    for (int s = 0; s < ns; ++s)
+      if (!entry_less(k, p, tk[s], tp[s])) j += tm[s];
+    PAS_CHECK(p >= 0 && p < P.N && j < P.nK, "K6 zone entry");
+    K_prime[p] = P.grid[j];
+    int c = j;
+    if (NCLS > kMaxLevels) {
+      const uint4 u = philox_stream(P.seed, bseq, (uint32_t)p, kStreamUniform);
+      c = plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)plan->n_inst[j]) >> 32)];
+    }
+    PAS_CHECK(c < NCLS, "K6 K7 class");
+    cls7[p] = (uint8_t)c;
+    atomicAdd(&blk_counts[(int64_t)c * ntiles + p / (FT * FPER)], 1);
+  }
+}
+
 }  // namespace
 
 int redirect_kb(int64_t N) {
@@ -252,20 +527,63 @@ int redirect_kb(int64_t N) {
   return b < 0 ? 0 : (b > kMaxK6Bits ? kMaxK6Bits : b);
 }
 
-cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan, const RedirectWs& w,
-                            int32_t* K_prime, cudaStream_t st, int* launches) {
+cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, DevPlan* plan, const RedirectWs& w,
+                            int32_t* K_prime, int32_t* blk_counts, int ntiles, int nC, cudaStream_t st,
+                            int* launches, bool* counts_ready) {
+  *counts_ready = false;
   if (p.N <= 0) return cudaSuccess;
-  cudaError_t e;
-  if ((e = launch_zero(w.hist, (int64_t)p.nK << p.kb, w.used, 2, nullptr, 0, st))) return e;
+  if (p.N < kWindowMinN) {   // small batches: the exact histogram path alone (fewer launches)
+    cudaError_t e;
+    if ((e = launch_zero(w.hist, (int64_t)p.nK << p.kb, w.used, 2, nullptr, 0, st))) return e;
+    const unsigned blocks = (unsigned)((p.N + RT - 1) / RT);
+    const unsigned hblocks = blocks < (unsigned)kNumSMs * 8 ? blocks : (unsigned)kNumSMs * 8;
+    const int* ug = nullptr;   // ungated
+    launch_pdl(k6_hist, hblocks, RT, 0, st, level, p, ug, w.key, w.hist);
+    launch_pdl(k6_chunks, p.nK * kChunks, RT, 0, st, p, ug, w.hist, w.csum);
+    launch_pdl(k6_bounds, p.nK, RT, 0, st, p, (const DevPlan*)plan, w.hist, w.csum, w.bnd, w.lists, w.used, ug);
+    const unsigned ablocks = (!PAS_K6_GRIDCAP || blocks < (unsigned)kNumSMs * 8) ? blocks : (unsigned)kNumSMs * 8;
+    launch_pdl(k6_assign, ablocks, RT, 0, st, level, w.key, p, (const DevPlan*)plan, w.bnd, w.lists, w.cand, K_prime,
+               w.cls7, ug);
+    launch_pdl(k6_resolve, p.nK * (p.nK - 1) > 0 ? p.nK * (p.nK - 1) : 1, RT, 0, st, p, (const DevPlan*)plan, w.bnd,
+               w.lists, w.used, w.cand, K_prime, w.cls7, ug);
+    *launches += 6;
+    return cudaGetLastError();
+  }
+  *counts_ready = true;
+  static_assert(FT * FPER == 4096, "k6_fused tiles are K7's tiles (batch_tiles)");
+  const bool uniform = p.mode == PAS_UNIFORM;
+  // the windowed pass and the zone resolves (K7's tile counts included)
+  // zone entries per batch ~ 8 sqrt(h) per split: 64 CTAs per zone spread the apply over the SMs
+  const dim3 agrid(64, kMaxZones);
+  if (uniform) {
+    launch_pdl(k6_fused<kMaxInst>, (unsigned)ntiles, FT, 0, st, level, p, plan, w.cand, K_prime, w.cls7, blk_counts, ntiles);
+    launch_pdl(k6_zone_select, (unsigned)kMaxZones, ZT, 0, st, plan, (const KeyEntry*)w.cand);
+    launch_pdl(k6_zone_apply<kMaxInst>, agrid, RT, 0, st, p, (const DevPlan*)plan, (const KeyEntry*)w.cand, K_prime,
+               w.cls7, blk_counts, ntiles);
+  } else {
+    launch_pdl(k6_fused<kMaxLevels>, (unsigned)ntiles, FT, 0, st, level, p, plan, w.cand, K_prime, w.cls7, blk_counts, ntiles);
+    launch_pdl(k6_zone_select, (unsigned)kMaxZones, ZT, 0, st, plan, (const KeyEntry*)w.cand);
+    launch_pdl(k6_zone_apply<kMaxLevels>, agrid, RT, 0, st, p, (const DevPlan*)plan, (const KeyEntry*)w.cand, K_prime,
+               w.cls7, blk_counts, ntiles);
+  }
+  (void)nC;
+  // the exact histogram path, each kernel a no-op unless k6_fallback was set
+  const int* gate = &plan->k6_fallback;
+  const int64_t nzero = (int64_t)p.nK << p.kb;
+  int64_t zb = (nzero + RT - 1) / RT;
+  if (zb > kNumSMs * 8) zb = kNumSMs * 8;
+  launch_pdl(k6_zero, (unsigned)zb, RT, 0, st, gate, w.hist, nzero, w.used, 2);
   const unsigned blocks = (unsigned)((p.N + RT - 1) / RT);
-  launch_pdl(k6_hist, blocks, RT, 0, st, level, p, w.key, w.hist);
-  launch_pdl(k6_chunks, p.nK * kChunks, RT, 0, st, p, w.hist, w.csum);
-  launch_pdl(k6_bounds, p.nK, RT, 0, st, p, plan, w.hist, w.csum, w.bnd, w.lists, w.used);
+  const unsigned hblocks = blocks < (unsigned)kNumSMs * 8 ? blocks : (unsigned)kNumSMs * 8;
+  launch_pdl(k6_hist, hblocks, RT, 0, st, level, p, gate, w.key, w.hist);
+  launch_pdl(k6_chunks, p.nK * kChunks, RT, 0, st, p, gate, w.hist, w.csum);
+  launch_pdl(k6_bounds, p.nK, RT, 0, st, p, (const DevPlan*)plan, w.hist, w.csum, w.bnd, w.lists, w.used, gate);
   const unsigned ablocks = (!PAS_K6_GRIDCAP || blocks < (unsigned)kNumSMs * 8) ? blocks : (unsigned)kNumSMs * 8;
-  launch_pdl(k6_assign, ablocks, RT, 0, st, level, w.key, p, plan, w.bnd, w.lists, w.cand, K_prime, w.cls7);
-  launch_pdl(k6_resolve, p.nK * (p.nK - 1) > 0 ? p.nK * (p.nK - 1) : 1, RT, 0, st, p, plan, w.bnd, w.lists, w.used,
-             w.cand, K_prime, w.cls7);
-  *launches += 6;
+  launch_pdl(k6_assign, ablocks, RT, 0, st, level, w.key, p, (const DevPlan*)plan, w.bnd, w.lists, w.cand, K_prime,
+             w.cls7, gate);
+  launch_pdl(k6_resolve, p.nK * (p.nK - 1) > 0 ? p.nK * (p.nK - 1) : 1, RT, 0, st, p, (const DevPlan*)plan, w.bnd,
+             w.lists, w.used, w.cand, K_prime, w.cls7, gate);
+  *launches += 9;
   return cudaGetLastError();
 }
 

@@ -52,12 +52,6 @@
 #define PAS_K2_PAIR_MAX_TILES 4
 #endif
 
-#ifndef PAS_K2_EPI_ARGMAX
-#define PAS_K2_EPI_ARGMAX 1   // top-k insert path: repeated chunk max + knock-out (0: column-order scan)
-#endif
-#ifndef PAS_K2_EPI_VOTE
-#define PAS_K2_EPI_VOTE 0     // with ARGMAX=0: a warp vote per column before its insert (measured slower)
-#endif
 
 namespace pas {
 namespace {
@@ -127,13 +121,12 @@ __device__ __forceinline__ void bubble_insert(float x, int32_t g, float (&s)[KMA
 
 // Epilogue over one accumulator: 32-column chunks (tcgen05.ld), chain max (FMNMX3), the column id
 // materialised only inside the insert path, the tail mask only on the last partial tile.
-// Insert path (PAS_K2_EPI_ARGMAX, default): while the chunk max beats the k-th best, insert it and knock
-// it out (lowest column among equal values), so a lane pays per candidate, not per column; a warp pays
-// the most candidates of any lane.  Inserting in value order (ties: column ascending) with a strict >
-// keeps the list the top-k under (score desc, column asc), exactly as the column-order scan does.
-// Measured alternatives: the column-order scan of all 32 columns (PAS_K2_EPI_ARGMAX=0;
-// a warp pays 32 bubble inserts whenever any lane has a candidate), a warp-vote per column on top of it
-// (PAS_K2_EPI_VOTE=1, slower still), a double-buffered tcgen05.ld + tree max (7 % slower).
+// Insert path: while the chunk max beats the k-th best, insert it and knock it out (lowest column among
+// equal values), so a lane pays per candidate, not per column; a warp pays the most candidates of any
+// lane.  Inserting in value order (ties: column ascending) with a strict > keeps the list the top-k
+// under (score desc, column asc), exactly as a column-order scan would.  Measured and removed
+// (DESIGN.md 8): the column-order scan of all 32 columns (a warp pays 32 bubble inserts whenever any
+// lane has a candidate), a warp vote per column on top of it, a double-buffered tcgen05.ld + tree max.
 template <int KMAX, bool PARTIAL, int NCH = BN / 64>
 __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_local, float (&s)[KMAX],
                                             int32_t (&gl)[KMAX]) {
@@ -149,7 +142,6 @@ __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_loc
         if (base + j >= M_local) v[j] = __float_as_uint(-INFINITY);
     }
     float mx = max32(v);
-#if PAS_K2_EPI_ARGMAX
     while (mx > s[KMAX - 1]) {
       int col = 0;
       bool hit = false;
@@ -163,24 +155,6 @@ __device__ __forceinline__ void epi_tile(uint32_t taddr, int col_base, int M_loc
       bubble_insert<KMAX>(mx, base + col, s, gl);
       mx = max32(v);
     }
-#elif PAS_K2_EPI_VOTE
-    if (__any_sync(0xffffffffu, mx > s[KMAX - 1])) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float x = __uint_as_float(v[j]);
-        if (!__any_sync(0xffffffffu, x > s[KMAX - 1])) continue;
-        if (x > s[KMAX - 1]) bubble_insert<KMAX>(x, base + j, s, gl);
-      }
-    }
-#else
-    if (mx > s[KMAX - 1]) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float x = __uint_as_float(v[j]);
-        if (x > s[KMAX - 1]) bubble_insert<KMAX>(x, base + j, s, gl);
-      }
-    }
-#endif
   }
 }
 
@@ -275,18 +249,13 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
 
-template <int KMAX, bool DUMP, bool PAIR, bool DYN, bool MC = false>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch_arg,
               const uint32_t* __restrict__ epoch_dev, uint32_t slack, const DynSched dyn) {
   static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
-  // MC: clusters of two single-CTA tiles on the dynamic schedule, streaming the same cache chunk for
-  // prompt tiles 2 mp and 2 mp + 1; each CTA TMA-loads half of every B k-block and multicasts it to
-  // both, so a cache tile crosses L2 -> SMEM once per pair instead of once per CTA.  Units hold
-  // prompt-tile PAIRS (MTp of them); the leader takes them from the counter and hands them to the peer.
-  static_assert(!MC || DYN, "B multicast is built on the dynamic schedule");
   using TL = Tile<PAIR>;
   constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
                 B_BYTES = TL::B_BYTES, STAGE_BYTES = TL::STAGE_BYTES, UNIT_ROWS = TL::UNIT_ROWS;
@@ -300,11 +269,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  const uint32_t crank = (PAIR || MC) ? ptx::cluster_ctarank() : 0;
+  const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0;
   const bool leader = crank == 0;
-  const int worker = (PAIR || MC) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int nworkers = (PAIR || MC) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int MTu = MC ? (MT + 1) / 2 : MT;   // schedule rows: prompt tiles (or pairs of them under MC)
+  const int worker = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nworkers = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int MTu = MT;   // schedule rows: prompt tiles
   const int units = DYN ? dyn.CS * MTu * R : MT * R;
 
   if (warp == 0 && lane == 0) {
@@ -312,12 +281,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&bars->full[s], 1);
-      ptx::mbar_init(&bars->empty[s], MC ? 2 : 1);   // MC: both CTAs' MMAs read the stage's B halves
+      ptx::mbar_init(&bars->empty[s], 1);
     }
     for (int s = 0; s < UNIT_RING; ++s) {
       ptx::mbar_init(&bars->ufull[s], 1);
-      // MC: the leader's slot is released by both CTAs' MMA issuer + epilogue warps and the peer's producer
-      ptx::mbar_init(&bars->uempty[s], MC ? 2 * (1 + EPI_WARPS) + 1 : 1 + EPI_WARPS);
+      ptx::mbar_init(&bars->uempty[s], 1 + EPI_WARPS);   // released by the MMA issuer + every epilogue warp
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&bars->tfull[a], 1);
@@ -335,7 +303,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   ptx::tc_fence_before();
-  if (PAIR || MC) ptx::cluster_sync(); else __syncthreads();
+  if (PAIR) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = bars->tmem_base;
   pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
@@ -354,45 +322,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int stage = 0, us = 0;
         uint32_t phase = 0, uph = 0;
         for (;;) {
-          int u;
-          if (!MC || leader) {
-            u = (int)atomicAdd(dyn.sched, 1u);
-            if (u >= units) u = -1;
-            ptx::mbar_wait(&bars->uempty[us], uph ^ 1);
-            bars->unit[us] = u;
-            if (MC) {   // the peer's ring slot (released with ours: its consumers arrive on our uempty)
-              ptx::st_cluster_u32(&bars->unit[us], 1, (uint32_t)u);
-              ptx::mbar_arrive_cluster(&bars->ufull[us], 1);
-            }
-            ptx::mbar_arrive(&bars->ufull[us]);
-          } else {
-            ptx::mbar_wait_cluster(&bars->ufull[us], uph);
-            u = bars->unit[us];
-            ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
-          }
+          int u = (int)atomicAdd(dyn.sched, 1u);
+          if (u >= units) u = -1;
+          ptx::mbar_wait(&bars->uempty[us], uph ^ 1);
+          bars->unit[us] = u;
+          ptx::mbar_arrive(&bars->ufull[us]);
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
           if (u < 0) break;
           int c, j, ta, tb;
           dyn_decode(u, MTu, R, NT, dyn, c, j, ta, tb);
-          const int qrow = (MC ? 2 * (j % MTu) + (int)crank : j % MT) * BM;
+          const int qrow = (j % MT) * BM;
           for (int t = ta; t < tb; ++t) {
             for (int kb = 0; kb < kblocks; ++kb) {
               ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
               ptx::mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
               ptx::tma_load_2d(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
-              if (MC)   // this CTA's half of the cache tile, into both CTAs (tmC: 128-row boxes)
-                ptx::tma_load_2d_mcast(&tmC, sB + stage * B_BYTES + crank * (B_BYTES / 2), &bars->full[stage],
-                                       kb * BK, t * BN + (int)crank * (BN / 2), 0x3, ptx::kEvictNormal);
-              else
-                ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN,
-                                 ptx::kEvictNormal);
+              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN,
+                               ptx::kEvictNormal);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
           }
         }
         // every worker has taken its last unit once all have arrived here: the last one out re-arms
         // the counter for the next launch (kernel boundaries order this against the next K2)
-        if ((!MC || leader) && atomicAdd(dyn.sched + 1, 1u) == (uint32_t)nworkers - 1) {
+        if (atomicAdd(dyn.sched + 1, 1u) == (uint32_t)nworkers - 1) {
           dyn.sched[0] = 0;
           dyn.sched[1] = 0;
         }
@@ -435,7 +388,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer ---------------------------------
-    // (CTA pair: the leader issues for both CTAs; every other tile, incl. each CTA of an MC pair, its own)
+    // (CTA pair: the leader issues for both CTAs; the single-CTA tile its own)
     if ((!PAIR || leader) && ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(UNIT_ROWS, BN);
       int stage = 0;
@@ -447,11 +400,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = worker; DYN || u < units; u += nworkers) {
         int t0, t1;
         if (DYN) {
-          if (MC) ptx::mbar_wait_cluster(&bars->ufull[us], uph);
-          else ptx::mbar_wait(&bars->ufull[us], uph);
+          ptx::mbar_wait(&bars->ufull[us], uph);
           u = bars->unit[us];
-          if (MC) ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
-          else ptx::mbar_arrive(&bars->uempty[us]);
+          ptx::mbar_arrive(&bars->uempty[us]);
           if (++us == UNIT_RING) { us = 0; uph ^= 1; }
           if (u < 0) break;
           int c, j;
@@ -478,7 +429,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               else ptx::umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
             }
             if (PAIR) ptx::umma_commit_pair(&bars->empty[stage], 0x3);
-            else if (MC) ptx::umma_commit_mcast(&bars->empty[stage], 0x3);   // frees the stage in both CTAs
             else ptx::umma_commit(&bars->empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -503,25 +453,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int u = worker; DYN || u < units; u += nworkers) {
       int m, r, t0, t1, c = 0, j = 0;
       if (DYN) {
-        if (MC) ptx::mbar_wait_cluster(&bars->ufull[us], uph);
-        else ptx::mbar_wait(&bars->ufull[us], uph);
+        ptx::mbar_wait(&bars->ufull[us], uph);
         u = bars->unit[us];
         __syncwarp();
-        if (lane == 0) {
-          if (MC) ptx::mbar_arrive_cluster(&bars->uempty[us], 0);
-          else ptx::mbar_arrive(&bars->uempty[us]);
-        }
+        if (lane == 0) ptx::mbar_arrive(&bars->uempty[us]);
         if (++us == UNIT_RING) { us = 0; uph ^= 1; }
         if (u < 0) break;
         dyn_decode(u, MTu, R, NT, dyn, c, j, t0, t1);
-        if (MC) {   // j = r MTp + mp -> this CTA's prompt tile 2 mp + crank, its parked-list slot 2 j + crank
-          m = 2 * (j % MTu) + (int)crank;
-          r = j / MTu;
-          j = 2 * j + (int)crank;
-        } else {
-          m = j % MT;
-          r = j / MT;
-        }
+        PAS_CHECK(u < units && c < dyn.CS && t0 <= t1 && t1 <= NT, "K2 unit decode");
+        m = j % MT;
+        r = j / MT;
       } else {
         m = u % MT;
         r = u / MT;
@@ -535,6 +476,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; gl[i] = -1; }
       // dynamic schedule: resume the lists this (range, prompt tile) had after chunk c - 1
       const int64_t st_off = ((int64_t)(j * 2 + half) * KMAX) * BM + row;
+      PAS_CHECK(!DYN || j < dyn.slots, "K2 parked-list slot");
+      PAS_CHECK(r < R && m < MT, "K2 range / prompt tile");
       if (DYN && c > 0) {
         if (warp == 2 && lane == 0) dyn_wait_state(dyn.done + j, ((uint64_t)epoch << 32) | (uint32_t)c);
         epi_barrier();
@@ -603,8 +546,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (prompt < N) {
             Cand* dst = out + ((int64_t)r * N + prompt) * k;
 #pragma unroll
-            for (int i = 0; i < KMAX; ++i)
+            for (int i = 0; i < KMAX; ++i) {
+              PAS_CHECK(gl[i] < (int64_t)M_local, "K2 top-k row beyond the shard");
               if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
+            }
           }
         }
         epi_barrier();
@@ -613,233 +558,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  if (PAIR || MC) ptx::cluster_sync(); else __syncthreads();   // MC: no CTA leaves while the peer may
-  if (warp == 1) {                                               // still multicast into it or arrive on it
+  if (PAIR) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 1) {
     ptx::tc_fence_after();
     if (PAIR) ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
     else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
-// ------------------------------------------------------------------------------------------------
-// A-in-TMEM variant (d <= 768): the CTA's 128 prompt rows (Q_hat, bf16) are written into tensor
-// memory once per work unit (tcgen05.st by the epilogue warps, K/2 columns of packed bf16 pairs per
-// lane) and every tcgen05.mma takes A from TMEM ("[a]" operand) and only B from shared memory.
-// Per cache tile only the B k-blocks cross L2 -> SMEM (8 KB stages, 64 cache rows), cutting the L2
-// and SMEM traffic per flop by a third against the SS tile.  TMEM: A in columns [0, d/2), two
-// 64-column fp32 accumulators at 384 and 448.  MMA M = 128, N = 64, K = 16 (32 cycles each).
-// ------------------------------------------------------------------------------------------------
-constexpr int TA_BN = 64;
-constexpr int TA_STAGES = 12;
-constexpr int TA_B_BYTES = TA_BN * BK * 2;
-constexpr int TA_ACC_COL = 384;
-constexpr int TA_SMEM_BYTES = TA_STAGES * TA_B_BYTES + 1024 /*align*/ + 512 /*barriers*/ + LIST_BYTES;
-
-struct __align__(8) TaBars {
-  uint64_t full[TA_STAGES];
-  uint64_t empty[TA_STAGES];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
-  uint64_t a_ready;
-  uint32_t tmem_base;
-};
-
-template <int KMAX, bool DUMP>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_simtopk_ta(const __grid_constant__ CUtensorMap tmC, const __nv_bfloat16* __restrict__ qhat, int64_t N,
-                 int64_t M_local, int d, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
-                 float* __restrict__ dump) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;
-  TaBars* bars = reinterpret_cast<TaBars*>(smem + TA_STAGES * TA_B_BYTES);
-  float* list_s = reinterpret_cast<float*>(smem + TA_STAGES * TA_B_BYTES + 512);
-  int32_t* list_g = reinterpret_cast<int32_t*>(list_s + BM * KMAX);
-
-  const uint32_t warp = ptx::warp_id();
-  const uint32_t lane = ptx::lane_id();
-  const int units = MT * R;
-  const int kblocks = d / BK;
-
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmC);
-    for (int s = 0; s < TA_STAGES; ++s) {
-      ptx::mbar_init(&bars->full[s], 1);
-      ptx::mbar_init(&bars->empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      ptx::mbar_init(&bars->tfull[a], 1);
-      ptx::mbar_init(&bars->tempty[a], EPI_WARPS);
-    }
-    ptx::mbar_init(&bars->a_ready, EPI_WARPS);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
-    ptx::tmem_relinquish();
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = bars->tmem_base;
-  pdl_entry();   // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous kernel
-
-  if (warp == 0) {
-    // ------------------------------- TMA producer (B only) ---------------------------
-    if (ptx::elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int r = u / MT;
-        const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-        for (int t = t0; t < t1; ++t) {
-          for (int kb = 0; kb < kblocks; ++kb) {
-            ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&bars->full[stage], TA_B_BYTES);
-            ptx::tma_load_2d(&tmC, sB + stage * TA_B_BYTES, &bars->full[stage], kb * BK, t * TA_BN,
-                             ptx::kEvictNormal);
-            if (++stage == TA_STAGES) { stage = 0; phase ^= 1; }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------- MMA issuer --------------------------------------
-    if (ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, TA_BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      uint32_t a_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int r = u / MT;
-        const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-        ptx::mbar_wait(&bars->a_ready, a_phase);   // this unit's prompt rows are in TMEM
-        a_phase ^= 1;
-        ptx::tc_fence_after();
-        for (int t = t0; t < t1; ++t) {
-          ptx::mbar_wait(&bars->tempty[acc], acc_phase ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + TA_ACC_COL + acc * TA_BN;
-          for (int kb = 0; kb < kblocks; ++kb) {
-            ptx::mbar_wait(&bars->full[stage], phase);
-            ptx::tc_fence_after();
-            const uint32_t b0 = ptx::smem_u32(sB + stage * TA_B_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              ptx::umma_f16_ts(d_tmem, tmem_base + kb * (BK / 2) + kk * 8, ptx::sdesc_kmajor_sw128(b0 + kk * 32),
-                               idesc, (kb | kk) != 0);
-            ptx::umma_commit(&bars->empty[stage]);
-            if (++stage == TA_STAGES) { stage = 0; phase ^= 1; }
-          }
-          ptx::umma_commit(&bars->tfull[acc]);
-          acc ^= 1;
-          if (acc == 0) acc_phase ^= 1;
-        }
-      }
-    }
-  } else {
-    // ------------------------------- epilogue ----------------------------------------
-    const uint32_t q = warp & 3;
-    const int half = (int)(warp - 2) >> 2;      // chunk of the 64-column tile: columns half*32..+32
-    const int row = (int)(q * 32 + lane);
-    const uint32_t lane_off = (q * 32u) << 16;
-    const int Ml = (int)M_local;
-    const int acols = d / 4;                    // 32-bit A columns written by each half
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int m = u % MT, r = u / MT;
-      const int t0 = (int)((int64_t)r * NT / R), t1 = (int)((int64_t)(r + 1) * NT / R);
-      const int64_t prompt = (int64_t)m * BM + row;
-      // A rows -> TMEM (the previous unit's MMAs are complete: this warp consumed its last tile)
-      {
-        const uint4* src = reinterpret_cast<const uint4*>(qhat + prompt * d + half * (d / 2));
-#pragma unroll 1
-        for (int g = 0; g < acols / 16; ++g) {
-          uint32_t v[16];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 x = __ldg(src + g * 4 + j);
-            v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
-          }
-          ptx::tmem_st_32x32b_x16(tmem_base + lane_off + half * acols + g * 16, v);
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars->a_ready);
-      }
-      float s[KMAX];
-      int32_t gl[KMAX];
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i) { s[i] = -INFINITY; gl[i] = -1; }
-      for (int t = t0; t < t1; ++t) {
-        ptx::mbar_wait(&bars->tfull[acc], acc_phase);
-        ptx::tc_fence_after();
-        const int col_base = t * TA_BN + half * 32;
-        const uint32_t taddr = tmem_base + lane_off + TA_ACC_COL + acc * TA_BN + half * 32;
-        if (DUMP) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(taddr, v);
-          ptx::tmem_wait_ld();
-          if (prompt < N)
-            for (int j = 0; j < 32; ++j)
-              if ((int64_t)col_base + j < M_local) dump[prompt * M_local + col_base + j] = __uint_as_float(v[j]);
-        } else if (col_base + 32 > Ml) {
-          epi_tile<KMAX, true, 1>(taddr, col_base, Ml, s, gl);
-        } else {
-          epi_tile<KMAX, false, 1>(taddr, col_base, Ml, s, gl);
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars->tempty[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
-      if (!DUMP) {
-        if (half == 1) {
-#pragma unroll
-          for (int i = 0; i < KMAX; ++i) {
-            list_s[row * KMAX + i] = s[i];
-            list_g[row * KMAX + i] = gl[i];
-          }
-        }
-        epi_barrier();
-        if (half == 0) {
-          merge_lists<KMAX>(s, gl, list_s + row * KMAX, list_g + row * KMAX);
-          if (prompt < N) {
-            Cand* dst = out + ((int64_t)r * N + prompt) * k;
-#pragma unroll
-            for (int i = 0; i < KMAX; ++i)
-              if (i < k) dst[i] = Cand{s[i], gl[i] < 0 ? -1 : gl[i] * G + rank};
-          }
-        }
-        epi_barrier();
-      }
-    }
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
-  }
-}
-
-template <int KMAX, bool DUMP>
-cudaError_t launch_ta(const SimTopkArgs& a, int MT, int NT, int grid, cudaStream_t st) {
-  launch_pdl(k_simtopk_ta<KMAX, DUMP>, grid, NUM_THREADS, TA_SMEM_BYTES, st, *a.tmap_c, a.qhat, a.N, a.M_local, a.d, a.k, a.G,
-                                                                     a.rank, a.R, MT, NT, a.out, a.dump);
-  return cudaGetLastError();
-}
-
-template <int KMAX, bool DUMP, bool PAIR, bool DYN = false, bool MC = false>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN = false>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
   using TL = Tile<PAIR>;
-  constexpr int CTAS = (PAIR || MC) ? 2 : 1;   // cluster size
+  constexpr int CTAS = PAIR ? 2 : 1;   // cluster size
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -853,45 +583,37 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (PAIR || MC) ? 2 : 1;
+  cfg.numAttrs = PAIR ? 2 : 1;
   // the CTA pair and the B multicast read the cache through the 128-row box map
-  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN, MC>, *a.tmap_q,
-                            (PAIR || MC) ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN>, *a.tmap_q,
+                            PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
                             a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, a.epoch_dev, slack, a.dyn);
 }
 
 }  // namespace
 
-#ifndef PAS_K2_ATMEM   // A-in-TMEM variant: correct, but 29 % slower under the power cap
-#define PAS_K2_ATMEM 0
-#endif
-bool simtopk_uses_tmem_a(int d) { return PAS_K2_ATMEM && d <= 2 * TA_ACC_COL; }
 bool simtopk_pair(int64_t N, int d) {
   static const int max_tiles = [] {   // A/B experiments: PAS_K2_PAIR_MAX_TILES in the environment
     const char* v = getenv("PAS_K2_PAIR_MAX_TILES");
     return v ? atoi(v) : PAS_K2_PAIR_MAX_TILES;
   }();
-  return !simtopk_uses_tmem_a(d) && (N + BM - 1) / BM <= max_tiles;
+  (void)d;
+  return (N + BM - 1) / BM <= max_tiles;
 }
 int simtopk_prompt_rows() { return Tile<true>::UNIT_ROWS; }   // prompt buffers are padded to whole pair tiles
 int simtopk_box_q() { return BM; }
-int simtopk_box_c(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : Tile<false>::BN_CTA; }
+int simtopk_box_c(int d) { return (void)d, Tile<false>::BN_CTA; }
 int simtopk_box_c_pair() { return Tile<true>::BN_CTA; }
-static int tile_rows(int d) { return simtopk_uses_tmem_a(d) ? TA_BN : BN; }
+static int tile_rows(int d) { return (void)d, BN; }
 
 // Opt the kernel variants into > 48 KB dynamic shared memory on the current device.
 cudaError_t simtopk_init() {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk_ta<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk_ta<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM_BYTES))) return e;
   const int ss = Tile<false>::SMEM_BYTES, pr = Tile<true>::SMEM_BYTES;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
   if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
   return cudaFuncSetAttribute(k_simtopk<16, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
@@ -916,9 +638,6 @@ cudaError_t simtopk_init() {
 #ifndef PAS_K2_DYN_TMAX
 #define PAS_K2_DYN_TMAX 128       // longest chunk (tiles)
 #endif
-#ifndef PAS_K2_MCAST
-#define PAS_K2_MCAST 0            // clusters of two sharing B by TMA multicast (dynamic schedule)
-#endif
 #ifndef PAS_K2_DYN_MIN_PAIRS
 #define PAS_K2_DYN_MIN_PAIRS 2
 #endif
@@ -940,28 +659,25 @@ K2Tuning K2Tuning::from_env() {
   t.dyn_min_pairs = env_int("PAS_K2_DYN_MIN_PAIRS", PAS_K2_DYN_MIN_PAIRS);
   t.dyn_min_steps = env_int("PAS_K2_DYN_MIN_STEPS", PAS_K2_DYN_MIN_STEPS);
   t.dyn_amb = env_int("PAS_K2_DYN_AMB", PAS_K2_DYN_AMB);
-  t.mcast = env_int("PAS_K2_MCAST", PAS_K2_MCAST) != 0;
   return t;
 }
 bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d,
                           const K2Tuning& tune, int* R_out, int* T_out, int* CS_out, int* MTg_out) {
   const int budget_mb = tune.dyn_mb;
-  if (budget_mb <= 0 || simtopk_uses_tmem_a(d) || simtopk_pair(N, d)) return false;
+  if (budget_mb <= 0 || simtopk_pair(N, d)) return false;
   const int64_t MT = (N + BM - 1) / BM;
   const int64_t NT = (M_local + BN - 1) / BN;
   if (MT <= 0 || NT <= 0) return false;
-  // schedule rows: prompt tiles, or pairs of them under the B multicast (one unit per CTA pair)
-  const bool mc = tune.mcast;
-  const int64_t rows = mc ? (MT + 1) / 2 : MT;
-  const int64_t workers = mc ? Tile<false>::NUM_WORKERS / 2 : Tile<false>::NUM_WORKERS;
+  const int64_t rows = MT;
+  const int64_t workers = Tile<false>::NUM_WORKERS;
   const int64_t want = (int64_t)tune.dyn_min_pairs * workers;
   // prompt-tile groups: every chunk step of a group re-reads all of its prompt tiles (A, kept in L2
   // with evict_last), so a group's A must leave L2 room for the chunks; each group streams the cache
-  // once.  Never split below `want` (range, prompt tile) pairs per group.  (Not with the multicast.)
+  // once.  Never split below `want` (range, prompt tile) pairs per group.
   const int64_t a_bytes = (int64_t)MT * BM * d * 2;
   const int64_t a_budget = (int64_t)std::max(tune.dyn_amb, 1) << 20;
-  int64_t groups = mc ? 1 : std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, rows), MTg, R;
-  const int64_t slots_per_range = mc ? 2 * rows : MT;   // parked-list slots
+  int64_t groups = std::min<int64_t>((a_bytes + a_budget - 1) / a_budget, rows), MTg, R;
+  const int64_t slots_per_range = MT;   // parked-list slots
   for (;; --groups) {   // fewer groups (more ranges per group) until the candidate buffers hold R ranges
     MTg = (rows + groups - 1) / groups;
     R = std::min<int64_t>((want + MTg - 1) / MTg, 128);   // the S-way merge takes S <= 128 sources
@@ -1047,17 +763,8 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   const int units = MT * a.R;
   const int workers = units < NUM_WORKERS ? units : NUM_WORKERS;
   const int grid = CTAS * workers;
-  if (simtopk_uses_tmem_a(a.d)) {
-    if (a.dump) return launch_ta<8, true>(a, MT, NT, grid, st);
-    if (a.k <= 8) return launch_ta<8, false>(a, MT, NT, grid, st);
-    return launch_ta<16, false>(a, MT, NT, grid, st);
-  }
   if (a.dyn.T > 0 && !pair && !a.dump) {
     const int g = NUM_WORKERS;   // every SM: units are handed out dynamically
-    if (a.dyn.mcast) {
-      if (a.k <= 8) return launch_variant<8, false, false, true, true>(a, MT, NT, g, 0, st);
-      return launch_variant<16, false, false, true, true>(a, MT, NT, g, 0, st);
-    }
     if (a.k <= 8) return launch_variant<8, false, false, true>(a, MT, NT, g, 0, st);
     return launch_variant<16, false, false, true>(a, MT, NT, g, 0, st);
   }

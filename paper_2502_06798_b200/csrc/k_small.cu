@@ -23,7 +23,7 @@ namespace {
 constexpr int SM_THREADS = 1024;
 
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __restrict__ in, int S,
-                                                               const uint8_t* __restrict__ pflags, const RouteParams P,
+                                                               const uint8_t* __restrict__ pflags, const __grid_constant__ RouteParams P,
                                                                SmallOut o) {
   pdl_entry();
   __shared__ uint8_t lvl_s[kSmallMax], cls_s[kSmallMax];
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
         int bs = -1;
         for (int s = 0; s < S; ++s) {
           if (pos[s] >= k) continue;
+          PAS_CHECK(p < stride, "small path candidate row");
           const Cand c = in[((int64_t)s * stride + p) * k + pos[s]];
           if (bs < 0 || cand_better(c, best)) {
             best = c;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
       inst = o.plan->inst_list[c][q1 % nj];
       sl = (q1 / nj) * b + t % b;
     }
+    PAS_CHECK(inst >= 0 && inst < P.W && sl >= 0, "small path instance / slot");
     o.instance[p] = inst;
     o.slot[p] = sl;
     atomicAdd(&icount_s[inst], 1);

@@ -119,6 +119,7 @@ struct pas_ctx {
   int k2_last_R = 0, k2_last_T = 0, k2_last_CS = 0;   // schedule of the last K2 launch (pas_plan_stats)
   K2Tuning k2_tune;                                    // experiment knobs, read at pas_create
   int small_max = kSmallMax;   // the one-CTA latency path serves N <= small_max (PAS_SMALL_MAX; 0: off)
+  bool k6_force_fallback = false;   // PAS_K6_FALLBACK=1: K6's exact histogram path for every batch (tests)
   // f1 forecast-driven mode (0 = exact per-batch plan)
   int fc_window = 0, fc_replan_every = 1;
   int64_t fc_tick = 0;
@@ -269,6 +270,7 @@ RouteParams make_params(const pas_ctx* ctx, int64_t N) {
   }
   for (int t = 0; t < kTTotal; ++t) p.c[t] = ctx->c[t];
   p.convex = ctx->c_convex ? 1 : 0;
+  p.k6_force_fallback = ctx->k6_force_fallback ? 1 : 0;
   for (int t = 0; t < kTTotal; ++t) p.cI[t] = ctx->cI[t];
   for (int w = 0; w < kMaxInst; ++w) p.inst_level[w] = ctx->inst_level[w];
   p.lru_stamp = ctx->stamps;
@@ -330,11 +332,9 @@ int k2_schedule(int64_t N, int64_t M_local, int d, int64_t cand_cap, const K2Tun
   int R = 1;
   if (!tune.force_static &&
       simtopk_plan_dynamic(N, M_local, cand_cap, k2_state_tiles(cand_cap), d, tune, &R, &dyn->T, &dyn->CS, &dyn->MTg)) {
-    dyn->mcast = tune.mcast;
     return R;
   }
   dyn->T = dyn->CS = dyn->MTg = 0;
-  dyn->mcast = false;
   R = simtopk_choose_ranges(N, M_local, cand_cap, d);
   if (tune.ranges >= 1 && (int64_t)tune.ranges * N <= cand_cap) R = tune.ranges;
   return R;
@@ -386,6 +386,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
       dyn.st_s = ctx->k2_st_s;
       dyn.st_g = ctx->k2_st_g;
       dyn.done = ctx->k2_done;
+      dyn.slots = (int)ctx->k2_state_tiles;
       dyn.sched = ctx->k2_sched;
     }
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
@@ -506,6 +507,7 @@ pas_status run_global_explicit(pas_ctx* ctx, const Cand* cand_all, int64_t N, co
 
 // a6 .. a8 (plan, redirection, route-and-batch) after the merge stage has written level / hist / plan.
 pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_route_out* out, cudaStream_t st) {
+  bool counts_ready = false;
   if (ctx->fc_window > 0) {
     // f1: plan from the forecast (held between rebuilds, R24), i.i.d. K' (R23), window update (R21)
     bool replan = !ctx->fc_planned || ctx->fc_tick % ctx->fc_replan_every == 0;
@@ -525,12 +527,16 @@ pas_status run_downstream(pas_ctx* ctx, RouteParams& p, int64_t N, const pas_rou
     CUDA_TRY(ctx, launch_plan(ctx->hist, p, ctx->plan, st));
     ctx->launches++;
     CUDA_TRY(ctx, rec_stage(ctx, 4, st));
-    CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, st, &ctx->launches));
+    CUDA_TRY(ctx, launch_redirect(ctx->level, p, ctx->plan, ctx->rw, out->K_prime, ctx->bw.blk_counts,
+                                  batch_tiles(N), p.mode == PAS_UNIFORM ? p.W : p.nK, st, &ctx->launches,
+                                  &counts_ready));
     ctx->fc_stats_valid = false;
   }
   CUDA_TRY(ctx, rec_stage(ctx, 5, st));
-  CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, ctx->bw, out->instance, out->slot,
-                                       out->bucket_offsets, out->bucket_prompts, st, &ctx->launches));
+  // K6's windowed pass wrote K7's tile counts (k_cls_count then only on its fallback)
+  CUDA_TRY(ctx, launch_route_and_batch(ctx->rw, p, ctx->plan, counts_ready ? &ctx->plan->k6_fallback : nullptr,
+                                       ctx->bw, out->instance, out->slot, out->bucket_offsets, out->bucket_prompts, st,
+                                       &ctx->launches));
   return finish_batch(ctx, N, st);
 }
 
@@ -542,7 +548,7 @@ pas_status finish_batch(pas_ctx* ctx, int64_t N, cudaStream_t st) {
   ctx->last_stream = st;
   ctx->last_N = N;
   ctx->batch_seq++;
-  if (ctx->ring_n > 0) {
+  if (ctx->ring_n > 0 && !ctx->capturing) {   // a capture records no stage events
     ctx->ring_pos++;
     ctx->ring_count = ctx->ring_count < ctx->ring_n ? ctx->ring_count + 1 : ctx->ring_n;
   }
@@ -646,6 +652,7 @@ pas_status pas_create(pas_ctx** out_ctx, const pas_config* cfg) {
   // K2 writes [R][N][k] with R * N <= cand_cap (simtopk_choose_ranges)
   ctx->cand_cap = k2_cand_cap(mb);
   ctx->k2_tune = K2Tuning::from_env();
+  ctx->k6_force_fallback = getenv("PAS_K6_FALLBACK") && atoi(getenv("PAS_K6_FALLBACK")) != 0;   // tests
   if (const char* v = getenv("PAS_SMALL_MAX")) {   // A/B and tests: force the multi-kernel chain
     const int m = atoi(v);
     ctx->small_max = m < 0 ? 0 : (m > kSmallMax ? kSmallMax : m);
@@ -1451,6 +1458,7 @@ pas_status pas_plan_stats(pas_ctx* ctx, pas_stats* out) {
   out->D_Q = p.D_Q;
   out->D_Q_LP = p.D_Q_LP;
   out->plan_solver_iters = p.solver_iters;
+  out->k6_fallback = p.k6_fallback;
   out->n_redirected = p.n_redirected;
   out->n_upgraded = p.n_upgraded;
   out->n_downgraded = p.n_downgraded;

@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include <utility>
@@ -51,6 +52,28 @@ constexpr int kMaxLevels = PAS_MAX_LEVELS;
 constexpr int kMaxInst = PAS_MAX_INSTANCES;
 constexpr int kTTotal = PAS_T_TOTAL;
 constexpr int kNumSMs = 148;
+
+// Checked build (python -m paper_2502_06798_b200.build -DPAS_CHECKED=1 --out=...): device-side bounds
+// and protocol checks on the indices the kernels compute (work units, parked-list slots, candidate,
+// list and batch-list positions); a failed check prints its site and traps.  The product build compiles
+// them out.  (compute-sanitizer is not available on this GPU pool.)
+#ifndef PAS_CHECKED
+#define PAS_CHECKED 0
+#endif
+#if PAS_CHECKED
+#define PAS_CHECK(cond, what)                                                                             \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("PAS_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                            \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define PAS_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
 
 // Candidate pair (score, global cache id); ordered by score desc, gid asc (R10).  Sentinel (-inf, -1).
 struct __align__(8) Cand {
@@ -110,6 +133,7 @@ struct RouteParams {
   double F[kMaxLevels];          // load fractions
   double c[kTTotal];             // degradation c(dK)
   int convex;                    // c convex: K5 takes the NW-corner closed form (R6, R7)
+  int k6_force_fallback;         // tests: K6 takes its exact histogram path
   int64_t cI[kTTotal];           // non-convex c: round-half-even(c * 2^24), K5's exact integer costs (R37)
   int inst_level[kMaxInst];      // level index of each serving instance
   uint32_t* lru_stamp;           // f2: [global slots] last-use ticks (K4 stamps each usable top-1)
@@ -122,6 +146,13 @@ struct RouteParams {
   DispState* dstate;
   DispPlan* dplan;
 };
+
+// K6 windows (k_redirect.cu): per class the distinct split ranks 0 < X < h of its plan row, each with
+// the kappa window [lo, hi) its order statistic lies in with probability 1 - 1e-15 (mean +- 8 sd of the
+// X-th of h uniforms); overlapping windows merged into zones.  At most nK - 1 splits exist (a basic
+// plan has <= 2 nK - 1 nonzeros); more, a list overflow or a split outside its zone sets k6_fallback
+// and the exact histogram path runs instead.
+constexpr int kMaxZones = 32;
 
 // Device-side plan + counters of one batch (K5 writes, pas_plan_stats reads).
 struct DevPlan {
@@ -138,6 +169,16 @@ struct DevPlan {
   int n_invalid, n_near_top1, n_near_threshold;
   int inst_count[kMaxInst];
   int solver_iters;                  // non-convex K5: min-cost-flow augmentations (+ lex-max cycles); -1: cap hit
+  // K6 windowed split search (written by K5, filled by the fused pass, resolved per zone)
+  int k6_nz, k6_fallback;
+  int cls_zone0[kMaxLevels], cls_nzone[kMaxLevels], cls_jtot[kMaxLevels], cls_slot0[kMaxLevels];
+  int z_cls[kMaxZones], z_first[kMaxZones], z_nsplit[kMaxZones], z_jbelow[kMaxZones], z_cap[kMaxZones],
+      z_base[kMaxZones], z_fill[kMaxZones];
+  uint64_t z_lo[kMaxZones], z_hi[kMaxZones];
+  int s_X[kMaxZones], s_mult[kMaxZones];
+  int gapcnt[kMaxLevels + kMaxZones];   // class prompts per (class, gap) slot: slot cls_slot0[i] + g
+  uint64_t s_thr_k[kMaxZones];          // each split's threshold entry (kappa, p): the prompt at rank X
+  int s_thr_p[kMaxZones];
 };
 constexpr int kDegShift = 24;        // R37: non-convex c held as integers on a 2^-24 grid
 
@@ -150,10 +191,10 @@ cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int 
                              cudaStream_t st, uint32_t* epoch_bump = nullptr);
 
 __device__ __forceinline__ uint64_t batch_seq_of(const RouteParams& P) {
-  return P.bc ? *reinterpret_cast<const volatile uint64_t*>(&P.bc->batch_seq) : P.batch_seq;
+  return P.bc ? P.bc->batch_seq : P.batch_seq;
 }
 __device__ __forceinline__ uint32_t lru_tick_of(const RouteParams& P) {
-  return P.bc ? *reinterpret_cast<const volatile uint32_t*>(&P.bc->lru_tick) : P.lru_tick;
+  return P.bc ? P.bc->lru_tick : P.lru_tick;
 }
 // The last kernel of a batch, one thread: the next batch's Philox sequence and LRU tick.
 __device__ __forceinline__ void advance_batch_counters(const RouteParams& P) {
@@ -169,13 +210,12 @@ __device__ __forceinline__ void advance_batch_counters(const RouteParams& P) {
 struct DynSched {
   int T = 0;                    // cache tiles per chunk
   int CS = 0;                   // chunk steps per range
-  int MTg = 0;                  // prompt tiles per group (each group streams the cache once); under
-                                // mcast: prompt-tile PAIRS per group
-  bool mcast = false;           // clusters of two CTAs sharing every B k-block by TMA multicast
+  int MTg = 0;                  // prompt tiles per group (each group streams the cache once)
   float* st_s = nullptr;        // [R*MT][2][KMAX][128] parked scores
   int32_t* st_g = nullptr;      // [R*MT][2][KMAX][128] parked local rows
   uint64_t* done = nullptr;     // [R*MT] epoch << 32 | chunks done
   uint32_t* sched = nullptr;    // [2] unit counter, workers finished (zero between launches)
+  int slots = 0;                // parked-list slots allocated (R * MT <= slots; checked builds)
 };
 
 // K2 schedule knobs for A/B experiments.  Read from the environment once per context at
@@ -189,7 +229,6 @@ struct K2Tuning {
   int dyn_min_pairs = 0;       // PAS_K2_DYN_MIN_PAIRS: (range, prompt tile) pairs per group, in units of 148
   int dyn_min_steps = 0;       // PAS_K2_DYN_MIN_STEPS: fewest chunk steps for the dynamic schedule
   int dyn_amb = 0;             // PAS_K2_DYN_AMB: L2 budget (MB) for one group's prompt tiles
-  bool mcast = false;          // PAS_K2_MCAST: B multicast across CTA pairs on the dynamic schedule
   static K2Tuning from_env();
 };
 
@@ -215,7 +254,6 @@ int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 // serves it (CTA-pair tile, too few units, or more parked lists than `state_tiles` prompt tiles).
 bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t state_tiles, int d,
                           const K2Tuning& tune, int* R, int* T, int* CS, int* MTg);
-bool simtopk_uses_tmem_a(int d);
 bool simtopk_pair(int64_t N, int d);   // the CTA-pair tile serves this batch size
 cudaError_t simtopk_init();
 int simtopk_prompt_rows();   // prompt rows per work unit (pair tile)
@@ -288,8 +326,11 @@ struct RedirectWs {
   uint8_t* cls7;          // [N] class for K7 (K' level in greedy, instance in uniform)
 };
 int redirect_kb(int64_t N);
-cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, const DevPlan* plan,
-                            const RedirectWs& w, int32_t* K_prime, cudaStream_t st, int* launches);
+// blk_counts / ntiles / nC: the K7 per-tile class counts, produced by the windowed pass (k_cls_count then
+// only runs on the fallback, gated on plan->k6_fallback).
+cudaError_t launch_redirect(const uint8_t* level, const RouteParams& p, DevPlan* plan,
+                            const RedirectWs& w, int32_t* K_prime, int32_t* blk_counts, int ntiles, int nC,
+                            cudaStream_t st, int* launches, bool* counts_ready);
 
 // f1 forecast-driven mode (R21-R24): predictor ring buffer + fixed-point Route-Plan.
 struct FcState {
@@ -341,7 +382,7 @@ int batch_tiles(int64_t N);
 cudaError_t batch_init();   // kernel attributes (once per device)
 // f3: events since the last batch, the pick tables, per-instance counts and the state after the batch
 cudaError_t launch_disp_prep(const RouteParams& p, int ntiles, int nC, const int32_t* scanned, cudaStream_t st);
-cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan,
+cudaError_t launch_route_and_batch(const RedirectWs& r, const RouteParams& p, DevPlan* plan, const int* count_gate,
                                    const BatchWs& w, int32_t* instance, int32_t* slot,
                                    int32_t* bucket_offsets, int32_t* bucket_prompts,
                                    cudaStream_t st, int* launches);

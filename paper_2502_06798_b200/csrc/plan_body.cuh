@@ -174,6 +174,79 @@ __device__ __forceinline__ int warp_sum(int v) {
 }
 
 
+// K6's windows (DevPlan comment in pas_internal.cuh): per class the distinct split ranks 0 < X < h_i of
+// the prefix row X_i (K' level of class rank r = #{j : X_i[j] <= r}), the window of the X-th smallest
+// of h_i uniform kappas (Beta(X + 1, h - X): mean +- 8 sd, +- 2 / h slack) in units of 2^-60, merged
+// into zones; list capacities (2x the expected entries + 1024, within N) and bases.  One thread.
+__device__ __noinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLevels], const RouteParams& P,
+                                      DevPlan* __restrict__ plan) {
+  const int nK = P.nK;
+  const double two60 = 1152921504606846976.0;   // 2^60
+  int nz = 0, ns = 0, slot = 0;
+  int64_t used = 0;
+  bool fallback = false;
+  for (int i = 0; i < nK; ++i) {
+    const int h = h_s[i];
+    plan->cls_zone0[i] = nz;
+    plan->cls_slot0[i] = slot;
+    int jb = 0, X = 0, lastX = -1, zc = -1;
+    for (int j = 0; j + 1 < nK; ++j) {
+      X += x[i][j];
+      if (X <= 0) {        // every class prompt has rank >= 0
+        ++jb;
+        continue;
+      }
+      if (X >= h) continue;  // no prompt of the class reaches it
+      if (X == lastX) {      // the same split rank again (x_ij == 0): one more level boundary there
+        ++plan->s_mult[ns - 1];
+        continue;
+      }
+      if (ns == kMaxZones) {
+        fallback = true;
+        continue;
+      }
+      const double mu = ((double)X + 1.0) / ((double)h + 1.0);
+      const double sd = sqrt(mu * (1.0 - mu) / ((double)h + 2.0));
+      const double lo = mu - 8.0 * sd - 2.0 / h, hi = mu + 8.0 * sd + 2.0 / h;
+      const uint64_t lo_k = lo <= 0.0 ? 0ull : (uint64_t)(lo * two60);
+      const uint64_t hi_k = hi >= 1.0 ? (1ull << 60) : (uint64_t)(hi * two60) + 1ull;
+      if (zc >= 0 && lo_k <= plan->z_hi[zc]) {   // overlaps the previous window of the class: merge
+        plan->z_hi[zc] = hi_k > plan->z_hi[zc] ? hi_k : plan->z_hi[zc];
+        ++plan->z_nsplit[zc];
+      } else {
+        zc = nz++;
+        plan->z_cls[zc] = i;
+        plan->z_lo[zc] = lo_k;
+        plan->z_hi[zc] = hi_k;
+        plan->z_first[zc] = ns;
+        plan->z_nsplit[zc] = 1;
+      }
+      plan->s_X[ns] = X;
+      plan->s_mult[ns] = 1;
+      ++ns;
+      lastX = X;
+    }
+    // K' level below each zone of the class (rank below all its splits) and above all of them
+    int j = jb;
+    for (int z = plan->cls_zone0[i]; z < nz; ++z) {
+      plan->z_jbelow[z] = j;
+      for (int t = 0; t < plan->z_nsplit[z]; ++t) j += plan->s_mult[plan->z_first[z] + t];
+      const double E = (double)(plan->z_hi[z] - plan->z_lo[z]) / two60 * h;
+      int64_t cap = (int64_t)(2.0 * E) + 1024;
+      if (cap > h) cap = h;
+      if (used + cap > P.N) cap = P.N - used;
+      plan->z_cap[z] = (int)cap;
+      plan->z_base[z] = (int)used;
+      used += cap;
+    }
+    plan->cls_jtot[i] = j;
+    plan->cls_nzone[i] = nz - plan->cls_zone0[i];
+    slot += plan->cls_nzone[i] + 1;   // gaps 0 .. nzone of the class
+  }
+  plan->k6_nz = nz;
+  if (fallback || P.k6_force_fallback) plan->k6_fallback = 1;
+}
+
 // One warp (lanes threadIdx.x & 31 of the calling warp); hist may point to shared or global memory.
 __device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan) {
   __shared__ int h_s[kMaxLevels], f_s[kMaxLevels], hc[kMaxLevels + 1], fc[kMaxLevels + 1];
@@ -278,6 +351,8 @@ __device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, De
     plan->n_upgraded = n_up;
     plan->n_downgraded = n_down;
   }
+  __syncwarp();
+  if (lane == 0) k6_zones(h_s, x_s, P, plan);
 }
 
 }  // namespace

@@ -55,7 +55,8 @@ class PasStats(C.Structure):
                 ("queue_len", C.c_int64 * PAS_MAX_INSTANCES), ("busy_until_us", C.c_int64 * PAS_MAX_INSTANCES),
                 ("fired_prompts", C.c_int64 * PAS_MAX_INSTANCES),
                 ("fired_batches", C.c_int64 * PAS_MAX_INSTANCES),
-                ("k2_ranges", C.c_int), ("k2_chunk_tiles", C.c_int), ("k2_chunk_steps", C.c_int)]
+                ("k2_ranges", C.c_int), ("k2_chunk_tiles", C.c_int), ("k2_chunk_steps", C.c_int),
+                ("k6_fallback", C.c_int)]
 
 
 class PasAssignment(C.Structure):
@@ -368,7 +369,7 @@ def pas_plan_stats(ctx) -> dict:
                 dispatcher=s.dispatcher, now_us=s.now_us, queue_len=list(s.queue_len[:W]),
                 busy_until_us=list(s.busy_until_us[:W]), fired_prompts=list(s.fired_prompts[:W]),
                 fired_batches=list(s.fired_batches[:W]), k2_ranges=s.k2_ranges,
-                k2_chunk_tiles=s.k2_chunk_tiles, k2_chunk_steps=s.k2_chunk_steps)
+                k2_chunk_tiles=s.k2_chunk_tiles, k2_chunk_steps=s.k2_chunk_steps, k6_fallback=s.k6_fallback)
 
 
 def pas_last_launch_count(ctx) -> int:

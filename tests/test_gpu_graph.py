@@ -41,8 +41,9 @@ def _run(pas, graph, cfg, N, M, steps, mode=None, bstar=None, topk=None):
     out = r.alloc_out(N)
     res = []
     for b, act in enumerate(steps):
-        if act == "fractions":
-            F = list(np.roll(cfg.F, 1))
+        if act == "fractions":   # half of the mass onto the first level that has an instance
+            F = [0.5 * f for f in cfg.F]
+            F[min(cfg.instance_level)] += 0.5
             r.set_fractions(F, cfg.instance_level, cfg.bstar if bstar is None else bstar,
                             cfg.mode if mode is None else mode)
         elif act == "insert":
@@ -110,3 +111,47 @@ def test_graph_latency_c1(pas):
         res[graph] = e0.elapsed_time(e1) / 500 * 1e3
     print(f"C1 per batch: eager {res[False]:.1f} us, graph {res[True]:.1f} us")
     r.close()
+
+
+@pytest.mark.parametrize("N,M,topk,mode,bstar,nonconvex,cold", [
+    (64, 1000, 8, 0, 4, False, False), (64, 1000, 8, 1, 1, False, False), (1, 1, 8, 0, 4, False, False),
+    (700, 20_000, 16, 0, 3, False, False), (1024, 150_000, 5, 0, 4, True, False), (333, 4000, 1, 1, 1, False, False),
+    (100, 0, 8, 0, 4, False, True)])
+def test_small_path_equals_multi_kernel_chain(pas, monkeypatch, N, M, topk, mode, bstar, nonconvex, cold):
+    """The one-CTA latency path (k_small.cu) vs the multi-kernel chain it replaces (PAS_SMALL_MAX=0),
+    byte for byte: outputs, plan stats, flags counters, LRU stamps -- incl. many cache ranges (S > 1),
+    k = 1 / 16, uniform mode, a non-convex table, invalid prompts and a cold cache."""
+    cfg = CONFIGS["C2"]
+    res = []
+    for small in (True, False):
+        if not small:
+            monkeypatch.setenv("PAS_SMALL_MAX", "0")
+        w = Workload(cfg, device=DEV, M=max(M, 1))
+        r = _router(pas, cfg, N, max(M, 1), mode, bstar, topk)
+        if nonconvex:
+            r.set_degradation(list(np.minimum(1.0, 0.09 * np.arange(50))))
+            r.set_fractions(cfg.F, cfg.instance_level, bstar, mode)
+        if not cold:
+            r.load_cache(w.cache_rows(0, M).contiguous())
+        P = w.prompts(N)
+        if N > 10:
+            P[7] = 0.0
+            P[9, 3] = float("nan")
+        out = r.route(P.contiguous())
+        torch.cuda.synchronize()
+        st = r.stats()
+        stamps = torch.empty(max(M, 1), dtype=torch.int32, device=DEV)
+        pas.pas_cache_stamps(r.ctx, stamps)
+        torch.cuda.synchronize()
+        res.append(({k: v.cpu().numpy() for k, v in out.items()}, st, stamps.cpu().numpy()))
+        r.close()
+    monkeypatch.delenv("PAS_SMALL_MAX")
+    (a, sa, ta), (b, sb, tb) = res
+    W = len(cfg.instance_level)
+    for key in a:
+        x, y = (a[key][:W + 1], b[key][:W + 1]) if key == "bucket_offsets" else (a[key], b[key])
+        assert np.array_equal(x, y), key
+    for key in ("h", "f", "x", "D_Q", "n_invalid", "n_near_top1", "n_near_threshold", "n_redirected",
+                "n_upgraded", "n_downgraded", "bucket_count"):
+        assert sa[key] == sb[key], key
+    assert np.array_equal(ta, tb)

@@ -583,21 +583,18 @@ def test_k2_dynamic_schedule_full_oracle_k16(pas, monkeypatch):
     print(rep.summary(), "R", st["k2_ranges"], "T", st["k2_chunk_tiles"], "CS", st["k2_chunk_steps"])
 
 
-@pytest.mark.parametrize("N,M,topk,amb,mcast", [(16384, 400_003, 8, None, None), (4097, 250_000, 3, None, None),
-                                                (16384, 400_003, 8, "8", None), (16384, 400_003, 8, None, "1"),
-                                                (4097, 250_000, 16, None, "1")])
-def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, mcast, monkeypatch):
+@pytest.mark.parametrize("N,M,topk,amb", [(16384, 400_003, 8, None), (4097, 250_000, 3, None),
+                                          (16384, 400_003, 8, "8"), (4097, 250_000, 16, None)])
+def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, monkeypatch):
     """Every output of the dynamic schedule byte-identical to the static one (same MMA sums, exact
     top-k with the same tie rule, whatever the split into groups, ranges and chunks), over three
     batches so the epoch-tagged chunk counters and the re-armed unit counter are exercised across
-    launches.  amb = "8": an 8 MB prompt-tile budget splits the 128 prompt tiles into 3 groups; mcast:
-    the B-multicast CTA pairs (k = 16 with 33 prompt tiles: the odd tile's peer computes padding rows)."""
+    launches (the epoch now bumped on the device by K1).  amb = "8": an 8 MB prompt-tile budget splits
+    the 128 prompt tiles into 3 groups."""
     cfg = CONFIGS["C3"]
     monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "2")
     if amb:
         monkeypatch.setenv("PAS_K2_DYN_AMB", amb)
-    if mcast:   # clusters of two CTAs sharing every B k-block by TMA multicast (odd MT: 33 prompt tiles)
-        monkeypatch.setenv("PAS_K2_MCAST", mcast)
     w = Workload(cfg, device=DEV, M=M)
     C_ = w.cache_rows(0, M).contiguous()
     res = {}
@@ -624,8 +621,8 @@ def test_k2_dynamic_schedule_matches_static(pas, N, M, topk, amb, mcast, monkeyp
 
 def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
     """Random shapes (d in {512, 768, 1024}) with the dynamic schedule forced into small chunks (T = 4 ..
-    16, as few as one chunk step, empty trailing chunks in the shorter ranges, odd prompt-tile counts for
-    the multicast pairs): every output byte-identical to the static schedule on the same inputs."""
+    16, as few as one chunk step, empty trailing chunks in the shorter ranges, odd prompt-tile counts):
+    every output byte-identical to the static schedule on the same inputs."""
     import dataclasses
     rng = np.random.default_rng(2502)
     for case in range(10):
@@ -641,7 +638,6 @@ def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
             monkeypatch.setenv("PAS_K2_SCHED", "static" if sched == "static" else "dynamic")
             monkeypatch.setenv("PAS_K2_DYN_MIN_STEPS", "1")
             monkeypatch.setenv("PAS_K2_DYN_MB", str(int(rng.choice([1, 4, 16]))))
-            monkeypatch.setenv("PAS_K2_MCAST", str(case % 2))
             r = _router(pas, cfg, N, M, topk=k)
             r.load_cache(C_)
             res[sched] = _host(r.route(P))
@@ -654,7 +650,7 @@ def test_k2_schedule_fuzz_dynamic_equals_static(pas, monkeypatch):
             if key == "bucket_offsets":
                 a, b = a[:W + 1], b[:W + 1]
             assert np.array_equal(a, b), (case, N, M, k, cfg.d, key, st["k2_chunk_tiles"], st["k2_chunk_steps"])
-    for v in ("PAS_K2_SCHED", "PAS_K2_DYN_MIN_STEPS", "PAS_K2_DYN_MB", "PAS_K2_MCAST"):
+    for v in ("PAS_K2_SCHED", "PAS_K2_DYN_MIN_STEPS", "PAS_K2_DYN_MB"):
         monkeypatch.delenv(v)
 
 

@@ -36,12 +36,20 @@ def _candidates(level_scores, k):
     return torch.stack([sc.contiguous().view(torch.int32), gid], dim=-1).contiguous()
 
 
+@pytest.mark.parametrize("fallback", [0, 1])
 @pytest.mark.parametrize("N,probs,F,mode", [
     (200_000, [0.6, 0.05, 0.05, 0.05, 0.05, 0.2], [0.05, 0.05, 0.1, 0.1, 0.2, 0.5], 0),
     (1 << 22, [0.02, 0.03, 0.15, 0.2, 0.25, 0.35], [0.5, 1e-5, 1e-5, 2e-5, 0.2, 0.29996], 0),
     (1 << 22, [0.0, 0.5, 0.0, 0.0, 0.0, 0.5], [0.25, 0.25, 0.0, 0.25, 0.0, 0.25], 1),
+    (3001, [0.3, 0.1, 0.1, 0.1, 0.1, 0.3], [0.1, 0.1, 0.2, 0.2, 0.2, 0.2], 0),
+    (300_007, [0.1, 0.2, 0.1, 0.2, 0.1, 0.3], [0.3, 0.1, 0.1, 0.1, 0.1, 0.3], 1),
 ])
-def test_k6_large_batches(pas, N, probs, F, mode):
+def test_k6_large_batches(pas, N, probs, F, mode, fallback, monkeypatch):
+    """fallback 0: the windowed split search (k6_fused + zone select / apply; N >= 2^18) or, below that,
+    the exact histogram path alone; 1: the exact path forced (PAS_K6_FALLBACK) -- all bit-exact vs the
+    oracle's full sort."""
+    if fallback:
+        monkeypatch.setenv("PAS_K6_FALLBACK", "1")
     cfg = CONFIGS["C4"]
     k = cfg.topk
     rng = np.random.default_rng(N + mode)
@@ -60,6 +68,7 @@ def test_k6_large_batches(pas, N, probs, F, mode):
         pas.pas_route_from_candidates(r.ctx, cand, 1, N, o)
         torch.cuda.synchronize()
         st = r.stats()
+        assert st["k6_fallback"] == fallback          # the windowed path decides every prompt itself
         K = o["K"].cpu().numpy()
         Kp = o["K_prime"].cpu().numpy()
         assert np.array_equal(np.searchsorted(np.asarray(cfg.grid), K), level)

@@ -23,9 +23,10 @@ def algorithmic_bytes(N, S, k, d, W, M):
     return {
         "k_normalize (cache insert, fp32 in)": M * d * (4 + 2),
         "k_merge_select_thr": N * (S * k * 8 + k * 8 + 4 + 1 + 1),
-        "k6_hist": N * (1 + 8 + 4),           # level byte, kappa written, one (class, bucket) count
-        "k6_assign": N * (1 + 8 + 4 + 1),     # level byte + kappa read; K' (int32) + K7 class byte written
-        "k_cls_count": N * 1,                  # class byte
+        "k6_fused": N * (1 + 4 + 1),           # level byte read; K' (int32) + K7 class byte written (+ K7's tile counts)
+        "k6_hist (fallback only)": N * (1 + 8 + 4),
+        "k6_assign (fallback only)": N * (1 + 8 + 4 + 1),
+        "k_cls_count (fallback only)": N * 1,
         "k_cls_rank": N * (1 + 4 + 4 + 4),     # class byte; instance, slot, bucket-list entry
     }
 
@@ -89,6 +90,7 @@ def main():
     out["stage_ms"] = dict(zip(["-", "-", "merge_optimalK", "plan", "redirect", "route_and_batch", "total"],
                                stage[:7]))
     out["h"] = st["h"]
+    out["k6_fallback"] = st["k6_fallback"]
     out["algorithmic_bytes"] = algorithmic_bytes(N, S, k, d, len(cfg.instance_level), M)
     out["merge_GBps"] = out["algorithmic_bytes"]["k_merge_select_thr"] / (stage[2] / 1e3) / 1e9
     rt.close()

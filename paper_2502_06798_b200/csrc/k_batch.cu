@@ -27,7 +27,11 @@
 // one ballot per class bit is slower still; the column scheme ranks slower than match.any (262 vs
 // 207 us); 16 consecutive prompts per thread with register-packed counters and a shuffle scan
 // ranks without votes but scatters the batch lists far worse (463 vs 305 us with the scatter); a
-// single-pass decoupled look-back is 60 % slower than count + scan + rank.
+// single-pass decoupled look-back is 60 % slower than count + scan + rank; (round 2) byte-packed class
+// counters with 4 prompts per lane and a 5-step warp scan of 4 packed registers per 128 prompts, int4
+// stores of instance and slot, executes MORE instructions per prompt (144 vs 97 warp instructions per 32
+// prompts: register selects for the packed fields, divergent per-prompt branches) and is slower at 64M
+// prompts (407 vs 260 us, profiles/r02_k7/): removed.
 // HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 4 B written.
 #include "dispatch.cuh"
 

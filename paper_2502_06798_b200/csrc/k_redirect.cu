@@ -288,101 +288,136 @@ constexpr int FT = 256;                 // k6_fused threads; 16 consecutive prom
 constexpr int FPER = 16;
 constexpr int kSlots = kMaxLevels + kMaxZones;   // (class, gap) slots
 
-// Private byte counter columns in shared memory (the column is the thread: no atomics, no conflicts).
+// Per prompt: Philox, then the (class, gap) slot.  A coarse table per class (256 buckets of the top 8
+// kappa bits) gives the gap of every bucket no zone touches (zones cover ~0.1 % of kappa space), so
+// almost every prompt resolves its slot with one shared load; the rest walk the class's zones.  Per
+// slot: K' and (greedy) the K7 class are table look-ups.  Counters: private byte columns in shared
+// memory (the column is the thread: no atomics, no conflicts); greedy class counts are the slot sums.
+constexpr int kCoarseBits = 8;
 template <int NCLS>
 __global__ void __launch_bounds__(FT) k6_fused(const uint8_t* __restrict__ level, const __grid_constant__ RouteParams P,
                                                DevPlan* __restrict__ plan, KeyEntry* __restrict__ cand,
                                                int32_t* __restrict__ K_prime, uint8_t* __restrict__ cls7,
                                                int32_t* __restrict__ blk_counts, int ntiles) {
+  constexpr bool UNIFORM = NCLS > kMaxLevels;
   pdl_entry();
   __shared__ uint64_t zlo[kMaxZones], zhi[kMaxZones];
-  __shared__ int zjb[kMaxZones], zcap[kMaxZones], zbase[kMaxZones];
-  __shared__ int cz0[kMaxLevels], cnz[kMaxLevels], cjt[kMaxLevels], cs0[kMaxLevels];
-  __shared__ int grid_s[kMaxLevels];
-  __shared__ uint8_t gcol[kSlots][FT];      // (class, gap) counts per thread (<= 16 each)
-  __shared__ uint8_t ccol[NCLS][FT];        // K7 class counts per thread
+  __shared__ int zcap[kMaxZones], zbase[kMaxZones];
+  __shared__ int cinfo[kMaxLevels];                    // zone0 | nzone << 8 | slot0 << 16
+  __shared__ int slotK[kSlots];                        // K' value of a prompt in the slot
+  __shared__ uint8_t slotJ[kSlots];                    // its K' level (the greedy K7 class)
+  __shared__ uint8_t coarse[kMaxLevels][1 << kCoarseBits];   // gap of a zone-free bucket, else 0xFF
+  __shared__ uint8_t gcol[kSlots][FT];                 // (class, gap) counts per thread (<= 16 each)
+  __shared__ uint8_t ccol[UNIFORM ? NCLS : 1][FT];     // uniform: K7 class (instance) counts per thread
+  __shared__ int csum[NCLS];
   const int t = threadIdx.x;
+  const int nK = P.nK;
   if (t < kMaxZones) {
     zlo[t] = plan->z_lo[t];
     zhi[t] = plan->z_hi[t];
-    zjb[t] = plan->z_jbelow[t];
     zcap[t] = plan->z_cap[t];
     zbase[t] = plan->z_base[t];
   }
-  if (t < kMaxLevels) {
-    cz0[t] = plan->cls_zone0[t];
-    cnz[t] = t < P.nK ? plan->cls_nzone[t] : 0;
-    cjt[t] = plan->cls_jtot[t];
-    cs0[t] = plan->cls_slot0[t];
-    grid_s[t] = P.grid[t];
+  if (t < nK) {
+    const int i = t, z0 = plan->cls_zone0[i], nz = plan->cls_nzone[i], s0 = plan->cls_slot0[i];
+    cinfo[i] = z0 | (nz << 8) | (s0 << 16);
+    for (int g = 0; g <= nz; ++g) {   // gap g: below zone g (or above all zones)
+      const int j = g < nz ? plan->z_jbelow[z0 + g] : plan->cls_jtot[i];
+      slotK[s0 + g] = P.grid[j];
+      slotJ[s0 + g] = (uint8_t)j;
+    }
   }
   for (int q = 0; q < kSlots; ++q) gcol[q][t] = 0;
-  for (int q = 0; q < NCLS; ++q) ccol[q][t] = 0;
+  if (UNIFORM)
+    for (int q = 0; q < NCLS; ++q) ccol[q][t] = 0;
+  if (t < NCLS) csum[t] = 0;
+  __syncthreads();
+  for (int e = t; e < nK << kCoarseBits; e += FT) {   // coarse buckets: gap, or 0xFF if a zone touches it
+    const int i = e >> kCoarseBits, b = e & ((1 << kCoarseBits) - 1);
+    const uint64_t blo = (uint64_t)b << (60 - kCoarseBits), bhi = blo + (1ull << (60 - kCoarseBits));
+    const int ci = cinfo[i], z0 = ci & 0xFF, nz = (ci >> 8) & 0xFF;
+    int g = 0;
+    bool touched = false;
+    for (int z = z0; z < z0 + nz; ++z) {
+      if (zhi[z] <= blo) ++g;
+      else if (zlo[z] < bhi) touched = true;
+    }
+    coarse[i][b] = touched ? 0xFF : (uint8_t)g;
+  }
   __syncthreads();
   const uint64_t bseq = batch_seq_of(P);
-  // the tile's prompts in warp-coalesced order: p = tile base + e * 256 + t (level loads, K' and class
-  // stores 32 consecutive per warp instruction); the counters are per thread, so the order is free
+  // the tile's prompts in warp-coalesced order: p = tile base + e * 256 + t
   const int64_t p0 = (int64_t)blockIdx.x * (FT * FPER) + t;
   bool overflow = false;
-#pragma unroll 4
-  for (int e = 0; e < FPER; ++e) {
-    const int64_t p = p0 + (int64_t)e * FT;
-    if (p >= P.N) break;
+  auto one = [&](int64_t p) {
     const int i = __ldg(level + p);
     const uint4 w = philox_stream(P.seed, bseq, (uint32_t)p, kStreamRedirect);
     const uint64_t kappa = (((uint64_t)w.y << 32) | w.x) >> 4;
-    const int z0 = cz0[i], nz = cnz[i];
-    int g = 0;
-    bool inside = false;
-    for (; g < nz; ++g) {
-      if (kappa < zlo[z0 + g]) break;
-      if (kappa < zhi[z0 + g]) {
-        inside = true;
-        break;
+    const int ci = cinfo[i];
+    int g = coarse[i][(int)(kappa >> (60 - kCoarseBits))];
+    if (g == 0xFF) {   // a bucket a zone touches: walk the class's zones
+      const int z0 = ci & 0xFF, nz = (ci >> 8) & 0xFF;
+      int z = -1;
+      for (g = 0; g < nz; ++g) {
+        if (kappa < zlo[z0 + g]) break;
+        if (kappa < zhi[z0 + g]) {
+          z = z0 + g;
+          break;
+        }
+      }
+      if (z >= 0) {
+        const int slot = atomicAdd(&plan->z_fill[z], 1);
+        PAS_CHECK(zbase[z] + zcap[z] <= P.N, "K6 zone list beyond N");
+        if (slot < zcap[z]) cand[zbase[z] + slot] = KeyEntry{kappa, (int32_t)p, 0};
+        else overflow = true;
+        return;
       }
     }
-    if (inside) {
-      const int z = z0 + g;
-      const int slot = atomicAdd(&plan->z_fill[z], 1);
-      PAS_CHECK(zbase[z] + zcap[z] <= P.N, "K6 zone list beyond N");
-      if (slot < zcap[z]) cand[zbase[z] + slot] = KeyEntry{kappa, (int32_t)p, 0};
-      else overflow = true;
-      continue;
-    }
-    PAS_CHECK(i < P.nK && cs0[i] + g < kSlots, "K6 gap slot");
-    ++gcol[cs0[i] + g][t];
-    const int j = g < nz ? zjb[z0 + g] : cjt[i];
-    PAS_CHECK(j < P.nK, "K6 K' level");
-    K_prime[p] = grid_s[j];
-    int c = j;
-    if (NCLS > kMaxLevels) {   // uniform: the instance I_j[(u n_j) >> 32]
+    const int slot = (ci >> 16) + g;
+    PAS_CHECK(i < nK && slot < kSlots, "K6 gap slot");
+    ++gcol[slot][t];
+    K_prime[p] = slotK[slot];
+    if (UNIFORM) {   // the instance I_j[(u n_j) >> 32]
+      const int j = slotJ[slot];
       const uint4 u = philox_stream(P.seed, bseq, (uint32_t)p, kStreamUniform);
-      c = plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)plan->n_inst[j]) >> 32)];
+      const int c = plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)plan->n_inst[j]) >> 32)];
+      cls7[p] = (uint8_t)c;
+      ++ccol[c][t];
+    } else {
+      cls7[p] = slotJ[slot];
     }
-    cls7[p] = (uint8_t)c;
-    ++ccol[c][t];
+  };
+  if ((int64_t)(blockIdx.x + 1) * (FT * FPER) <= P.N) {   // a full tile: no bounds checks
+#pragma unroll 4
+    for (int e = 0; e < FPER; ++e) one(p0 + (int64_t)e * FT);
+  } else {
+    for (int e = 0; e < FPER && p0 + (int64_t)e * FT < P.N; ++e) one(p0 + (int64_t)e * FT);
   }
   if (overflow) plan->k6_fallback = 1;
   __syncthreads();
-  // column sums: one warp per counter row
+  // column sums: one warp per counter row; (class, gap) totals to the plan, class totals to K7's tile
   const int lane = t & 31, wp = t >> 5;
-  const int nslots = cs0[P.nK - 1] + cnz[P.nK - 1] + 1;
-  const int nC = NCLS > kMaxLevels ? P.W : P.nK;
-  for (int q = wp; q < nslots + nC; q += FT / 32) {
-    const uint8_t* row = q < nslots ? gcol[q] : ccol[q - nslots];
+  const int nslots = (cinfo[nK - 1] >> 16) + ((cinfo[nK - 1] >> 8) & 0xFF) + 1;
+  const int nrows = nslots + (UNIFORM ? P.W : 0);
+  for (int q = wp; q < nrows; q += FT / 32) {
+    const uint8_t* row = q < nslots ? gcol[q] : ccol[UNIFORM ? q - nslots : 0];
     int sum = 0;
 #pragma unroll
     for (int r = 0; r < FT / 32; ++r) sum += row[lane + 32 * r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) {
+    if (lane == 0 && sum) {
       if (q < nslots) {
-        if (sum) atomicAdd(&plan->gapcnt[q], sum);
+        atomicAdd(&plan->gapcnt[q], sum);
+        if (!UNIFORM) atomicAdd(&csum[slotJ[q]], sum);
       } else {
-        blk_counts[(int64_t)(q - nslots) * ntiles + blockIdx.x] = sum;   // the zone entries are added later
+        csum[q - nslots] = sum;
       }
     }
   }
+  __syncthreads();
+  const int nC = UNIFORM ? P.W : nK;
+  if (t < nC) blk_counts[(int64_t)t * ntiles + blockIdx.x] = csum[t];   // the zone entries are added later
 }
 
 constexpr int ZT = 1024;          // k6_zone threads

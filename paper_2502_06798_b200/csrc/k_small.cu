@@ -21,6 +21,7 @@ namespace pas {
 namespace {
 
 constexpr int SM_THREADS = 1024;
+constexpr int kStageCands = 2048;   // candidate pairs staged in shared memory (16 KB) when they fit
 
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __restrict__ in, int S,
                                                                const uint8_t* __restrict__ pflags, const __grid_constant__ RouteParams P,
@@ -32,6 +33,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
   __shared__ int cnt_s[3];
   __shared__ int X_s[kMaxLevels][kMaxLevels];
   __shared__ int icount_s[kMaxInst], ioff_s[kMaxInst + 1];
+  __shared__ Cand cand_s[kStageCands];
   const int tid = threadIdx.x;
   const int N = (int)P.N, k = P.topk, nK = P.nK;
   const bool cold = P.M_total == 0;
@@ -45,6 +47,17 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
   __syncthreads();
   const uint32_t tick = lru_tick_of(P);
   const int64_t stride = P.cand_stride ? P.cand_stride : P.N;
+  // all S x N x k candidates in shared memory when they fit (one coalesced pass, every load in flight),
+  // else the merge reads them from L2
+  const bool staged = (int64_t)S * N * k <= kStageCands;
+  if (staged) {
+    const int per = N * k;
+    for (int e = tid; e < S * per; e += SM_THREADS) {
+      const int s = e / per, r = e - s * per;
+      cand_s[e] = in[(int64_t)s * stride * k + r];
+    }
+  }
+  __syncthreads();
   // ---- a4 + a5: merge, optimal-K, flags, stamps, H_K
   for (int p = tid; p < N; p += SM_THREADS) {
     const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
@@ -60,7 +73,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
         for (int s = 0; s < S; ++s) {
           if (pos[s] >= k) continue;
           PAS_CHECK(p < stride, "small path candidate row");
-          const Cand c = in[((int64_t)s * stride + p) * k + pos[s]];
+          const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
           if (bs < 0 || cand_better(c, best)) {
             best = c;
             bs = s;
@@ -101,7 +114,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
   }
   __syncthreads();
   // ---- a6: the plan, one warp (the same code as K5)
-  if (tid < 32) plan_body(hist_s, P, o.plan);
+  if (tid < 32) plan_body(hist_s, P, o.plan, false);   // no K6 windows: a7 ranks by counting
   __syncthreads();
   if (tid == 0) {
     o.plan->n_invalid = cnt_s[0];

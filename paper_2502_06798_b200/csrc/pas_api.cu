@@ -422,10 +422,6 @@ pas_status finish_batch(pas_ctx* ctx, int64_t N, cudaStream_t st);
 pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pas_route_out* out, cudaStream_t st) {
   ctx->lru_tick++;   // f2 clock: one tick per routed batch (R26)
   RouteParams p = make_params(ctx, N);
-  static_assert(sizeof(DevPlan) % 4 == 0, "DevPlan zeroed as int32 words");
-  CUDA_TRY(ctx, launch_zero(ctx->hist, kMaxLevels, reinterpret_cast<int32_t*>(ctx->plan), sizeof(DevPlan) / 4,
-                            nullptr, 0, st));
-  ctx->launches++;
   SelectOut so{out->K, out->topk_id, out->topk_score, out->flags, ctx->level, nullptr, ctx->hist, ctx->plan};
   // the validity flags of the pas_route_local / run_local that produced these candidates; consumed
   // here, so a later pas_route_from_candidates with the same N never reuses them (else: all valid)
@@ -443,6 +439,10 @@ pas_status run_global(pas_ctx* ctx, const Cand* cand, int S, int64_t N, const pa
     ctx->fc_stats_valid = false;
     return finish_batch(ctx, N, st);
   }
+  static_assert(sizeof(DevPlan) % 4 == 0, "DevPlan zeroed as int32 words");
+  CUDA_TRY(ctx, launch_zero(ctx->hist, kMaxLevels, reinterpret_cast<int32_t*>(ctx->plan), sizeof(DevPlan) / 4,
+                            nullptr, 0, st));
+  ctx->launches++;
   CUDA_TRY(ctx, launch_merge_select(cand, S, pflags, p, so, st));
   ctx->launches++;
   CUDA_TRY(ctx, rec_stage(ctx, 3, st));

@@ -248,7 +248,8 @@ __device__ __noinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLevels]
 }
 
 // One warp (lanes threadIdx.x & 31 of the calling warp); hist may point to shared or global memory.
-__device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan) {
+__device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan,
+                                       bool k6_windows = true) {
   __shared__ int h_s[kMaxLevels], f_s[kMaxLevels], hc[kMaxLevels + 1], fc[kMaxLevels + 1];
   __shared__ double frac_s[kMaxLevels];
   __shared__ int x_s[kMaxLevels][kMaxLevels];
@@ -352,7 +353,7 @@ __device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, De
     plan->n_downgraded = n_down;
   }
   __syncwarp();
-  if (lane == 0) k6_zones(h_s, x_s, P, plan);
+  if (lane == 0 && k6_windows) k6_zones(h_s, x_s, P, plan);
 }
 
 }  // namespace

@@ -37,10 +37,10 @@
 namespace pas {
 namespace {
 
-__global__ void __launch_bounds__(32) k_plan(const int* __restrict__ hist, const __grid_constant__ RouteParams P,
+__global__ void __launch_bounds__(32) k_plan(const int* __restrict__ hist, const RouteParams P,
                                              DevPlan* __restrict__ plan) {
   pdl_entry();
-  plan_body(hist, P, plan);
+  plan_body(hist, P, plan);   // inlined: the parameters are read with direct (indexed) constant loads
 }
 
 }  // namespace

@@ -24,21 +24,21 @@ constexpr int SM_THREADS = 1024;
 constexpr int kStageCands = 2048;   // candidate pairs staged in shared memory (16 KB) when they fit
 
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __restrict__ in, int S,
-                                                               const uint8_t* __restrict__ pflags, const __grid_constant__ RouteParams P,
-                                                               SmallOut o) {
+                                                               const uint8_t* __restrict__ pflags,
+                                                               const RouteParams P, SmallOut o) {
   pdl_entry();
   __shared__ uint8_t lvl_s[kSmallMax], cls_s[kSmallMax];
   __shared__ uint64_t kap_s[kSmallMax];
   __shared__ int hist_s[kMaxLevels];
   __shared__ int cnt_s[3];
-  __shared__ int X_s[kMaxLevels][kMaxLevels];
+  __shared__ DevPlan plan_s;          // the batch's plan lives in shared memory, copied out at the end
   __shared__ int icount_s[kMaxInst], ioff_s[kMaxInst + 1];
   __shared__ Cand cand_s[kStageCands];
   const int tid = threadIdx.x;
   const int N = (int)P.N, k = P.topk, nK = P.nK;
   const bool cold = P.M_total == 0;
   {   // zero the plan (as launch_zero does for the multi-kernel path) and the shared tallies
-    int32_t* w = reinterpret_cast<int32_t*>(o.plan);
+    int32_t* w = reinterpret_cast<int32_t*>(&plan_s);
     for (int i = tid; i < (int)(sizeof(DevPlan) / 4); i += SM_THREADS) w[i] = 0;
     if (tid < kMaxLevels) hist_s[tid] = 0;
     if (tid < 3) cnt_s[tid] = 0;
@@ -58,12 +58,31 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
     }
   }
   __syncthreads();
-  // ---- a4 + a5: merge, optimal-K, flags, stamps, H_K
+  // ---- a4 + a5: merge (a thread per prompt; cursors in registers for S <= 8), optimal-K, flags,
+  // stamps, H_K.  (A warp per prompt with shuffle reductions measured 3x slower here: 64 prompts.)
   for (int p = tid; p < N; p += SM_THREADS) {
     const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
     Cand res[PAS_MAX_TOPK];
     if (invalid || cold) {
       for (int i = 0; i < k; ++i) res[i] = Cand{-INFINITY, -1};
+    } else if (S <= 8) {
+      int pos[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int i = 0; i < k; ++i) {
+        Cand best{-INFINITY, -1};
+        int bs = -1;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          if (s >= S || pos[s] >= k) continue;
+          const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
+          if (bs < 0 || cand_better(c, best)) {
+            best = c;
+            bs = s;
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) pos[s] += s == bs ? 1 : 0;
+        res[i] = bs >= 0 ? best : Cand{-INFINITY, -1};
+      }
     } else {
       uint8_t pos[128];
       for (int s = 0; s < S; ++s) pos[s] = 0;
@@ -114,51 +133,63 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
   }
   __syncthreads();
   // ---- a6: the plan, one warp (the same code as K5)
-  if (tid < 32) plan_body(hist_s, P, o.plan, false);   // no K6 windows: a7 ranks by counting
-  __syncthreads();
+  if (tid < 32) plan_body(hist_s, P, &plan_s, false);   // no K6 windows: a7 ranks by counting
   if (tid == 0) {
-    o.plan->n_invalid = cnt_s[0];
-    o.plan->n_near_top1 = cnt_s[1];
-    o.plan->n_near_threshold = cnt_s[2];
+    plan_s.n_invalid = cnt_s[0];
+    plan_s.n_near_top1 = cnt_s[1];
+    plan_s.n_near_threshold = cnt_s[2];
   }
-  for (int e = tid; e < nK * kMaxLevels; e += SM_THREADS) X_s[e / kMaxLevels][e % kMaxLevels] = o.plan->X[e / kMaxLevels][e % kMaxLevels];
   const uint64_t bseq = batch_seq_of(P);
   for (int p = tid; p < N; p += SM_THREADS) {
     const uint4 w = philox_stream(P.seed, bseq, (uint32_t)p, kStreamRedirect);
     kap_s[p] = (((uint64_t)w.y << 32) | w.x) >> 4;
   }
   __syncthreads();
-  // ---- a7: class rank of (kappa, p), K' from the row prefix of the plan
-  for (int p = tid; p < N; p += SM_THREADS) {
-    const int i = lvl_s[p];
-    const uint64_t kp = kap_s[p];
+  // ---- a7: class rank of (kappa, p), K' from the row prefix of the plan.  G threads per prompt
+  // (G = 1024 / N rounded down to a power of two, <= 32) split the count and reduce by shuffles.
+  int G = 1;
+  while (G < 32 && G * 2 * N <= SM_THREADS) G *= 2;
+  const int sub = tid & (G - 1);
+  for (int base = 0; base < N * G; base += SM_THREADS) {
+    const int p = (base + tid) / G;
+    const bool act = p < N;
+    const int i = act ? lvl_s[p] : 0;
+    const uint64_t kp = act ? kap_s[p] : 0;
     int r = 0;
-    for (int q = 0; q < N; ++q)
-      r += (lvl_s[q] == i && (kap_s[q] < kp || (kap_s[q] == kp && q < p))) ? 1 : 0;
+    if (act)
+      for (int q = sub; q < N; q += G)
+        r += (lvl_s[q] == i && (kap_s[q] < kp || (kap_s[q] == kp && q < p))) ? 1 : 0;
+    for (int off = G >> 1; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+    if (!act || sub != 0) continue;
     int j = 0;
-    while (j + 1 < nK && X_s[i][j] <= r) ++j;
+    while (j + 1 < nK && plan_s.X[i][j] <= r) ++j;
     o.K_prime[p] = P.grid[j];
     int c = j;
     if (P.mode == PAS_UNIFORM) {
       const uint4 u = philox_stream(P.seed, bseq, (uint32_t)p, kStreamUniform);
-      c = o.plan->inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)o.plan->n_inst[j]) >> 32)];
+      c = plan_s.inst_list[j][(uint32_t)(((uint64_t)u.x * (uint32_t)plan_s.n_inst[j]) >> 32)];
     }
     cls_s[p] = (uint8_t)c;
   }
   __syncthreads();
   // ---- a8: instance and slot (FIFO rank within the class), then the batch lists
-  for (int p = tid; p < N; p += SM_THREADS) {
-    const int c = cls_s[p];
+  for (int base = 0; base < N * G; base += SM_THREADS) {
+    const int p = (base + tid) / G;
+    const bool act = p < N;
+    const int c = act ? cls_s[p] : 0;
     int t = 0;
-    for (int q = 0; q < p; ++q) t += cls_s[q] == c ? 1 : 0;
+    if (act)
+      for (int q = sub; q < p; q += G) t += cls_s[q] == c ? 1 : 0;
+    for (int off = G >> 1; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (!act || sub != 0) continue;
     int inst, sl;
     if (P.mode == PAS_UNIFORM) {
       inst = c;
       sl = t;
     } else {
-      const int b = P.bstar, nj = o.plan->n_inst[c];
+      const int b = P.bstar, nj = plan_s.n_inst[c];
       const int q1 = t / b;
-      inst = o.plan->inst_list[c][q1 % nj];
+      inst = plan_s.inst_list[c][q1 % nj];
       sl = (q1 / nj) * b + t % b;
     }
     PAS_CHECK(inst >= 0 && inst < P.W && sl >= 0, "small path instance / slot");
@@ -172,7 +203,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
     for (int w = 0; w < P.W; ++w) {
       ioff_s[w] = acc;
       acc += icount_s[w];
-      o.plan->inst_count[w] = icount_s[w];
+      plan_s.inst_count[w] = icount_s[w];
     }
     ioff_s[P.W] = acc;
   }
@@ -180,6 +211,11 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
   if (o.bucket_offsets && tid <= P.W) o.bucket_offsets[tid] = ioff_s[tid];
   if (o.bucket_prompts)
     for (int p = tid; p < N; p += SM_THREADS) o.bucket_prompts[ioff_s[o.instance[p]] + o.slot[p]] = p;
+  {   // the plan and counters for pas_plan_stats
+    const int32_t* src = reinterpret_cast<const int32_t*>(&plan_s);
+    int32_t* dst = reinterpret_cast<int32_t*>(o.plan);
+    for (int i = tid; i < (int)(sizeof(DevPlan) / 4); i += SM_THREADS) dst[i] = src[i];
+  }
   __syncthreads();
   advance_batch_counters(P);   // after every read of the counters in this batch
 }

@@ -24,7 +24,7 @@ constexpr long long kInfD = (long long)1 << 62;
 // unit cost of cell (i, j) = (cI[K_j - K_i] if K_j > K_i else 0, (K_j - K_i)^2); then the
 // lexicographically greatest optimal x in row-major order.  One thread; x in shared memory.  Returns
 // the number of augmentations, or -1 if the iteration cap was hit (x is then feasible, not canonical).
-__device__ int mcf_plan(const int* h, const int* f, const RouteParams& P, int (*x)[kMaxLevels]) {
+__device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteParams& P, int (*x)[kMaxLevels]) {
   const int nK = P.nK;
   const int V = 2 * nK + 2, S = 0, T = 2 * nK + 1;   // S, rows 1..nK, cols nK+1..2nK, T
   // working arrays in shared memory (one thread runs the solver; no per-thread stack frame)
@@ -178,7 +178,7 @@ __device__ __forceinline__ int warp_sum(int v) {
 // the prefix row X_i (K' level of class rank r = #{j : X_i[j] <= r}), the window of the X-th smallest
 // of h_i uniform kappas (Beta(X + 1, h - X): mean +- 8 sd, +- 2 / h slack) in units of 2^-60, merged
 // into zones; list capacities (2x the expected entries + 1024, within N) and bases.  One thread.
-__device__ __noinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLevels], const RouteParams& P,
+__device__ __forceinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLevels], const RouteParams& P,
                                       DevPlan* __restrict__ plan) {
   const int nK = P.nK;
   const double two60 = 1152921504606846976.0;   // 2^60
@@ -248,7 +248,10 @@ __device__ __noinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLevels]
 }
 
 // One warp (lanes threadIdx.x & 31 of the calling warp); hist may point to shared or global memory.
-__device__ __noinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan,
+// Inlined (with mcf_plan and k6_zones) so that P, a kernel parameter, is read with direct indexed
+// constant loads: a reference escaping into a called function would make the compiler copy the whole
+// parameter block to local memory per thread.
+__device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P, DevPlan* __restrict__ plan,
                                        bool k6_windows = true) {
   __shared__ int h_s[kMaxLevels], f_s[kMaxLevels], hc[kMaxLevels + 1], fc[kMaxLevels + 1];
   __shared__ double frac_s[kMaxLevels];

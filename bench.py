@@ -325,7 +325,8 @@ def main():
 
     # per-step events on the routing stream and the library's stage-timing ring: nothing in the timed
     # loop waits on the device (no stats() / host sync between steps)
-    pas.pas_stage_ring(router.ctx, args.steps)
+    ring = min(args.steps, 4096)                 # PAS_MAX_RING: stage times of the last <= 4,096 steps
+    pas.pas_stage_ring(router.ctx, ring)
     clocks = ClockSampler(local)
     clocks.start()
     clocks.begin()
@@ -347,7 +348,7 @@ def main():
     barrier()
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in zip(s0, s1)]
-    stages = pas.pas_stage_ring_read(router.ctx, args.steps)
+    stages = pas.pas_stage_ring_read(router.ctx, ring)
     pas.pas_stage_ring(router.ctx, 0)
     stage_sum = [sum(r[i] for r in stages) for i in range(7)]
     n_st = max(1, len(stages))        # 0 in graph mode: a replayed batch is timed as a whole

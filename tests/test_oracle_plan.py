@@ -256,3 +256,25 @@ def test_r37_never_worse_than_nw_and_often_better():
         assert D(x) <= D(nw)
         better += D(x) < D(nw)
     assert better >= 20
+
+
+def test_dq_continuous_pins():
+    """D_Q_LP (pas_plan_stats; the Eq. 1 optimum on unrounded masses): the S:237 fractional example
+    {0, 25}, H = (.5, .5), F = (.25, .75) -> 0.0375; H = F -> 0; all mass upgraded (F below H) -> 0;
+    and for linear D it equals the cut closed form divided by N on masses that are multiples of 1/N."""
+    c = O.default_degradation()
+    assert abs(O.dq_continuous([0.5, 0.5], [0.25, 0.75], [0, 25], c) - 0.0375) < 1e-12
+    assert abs(O.dq_continuous([0.2, 0.3, 0.5], [0.2, 0.3, 0.5], [0, 10, 25], c)) < 1e-12
+    assert abs(O.dq_continuous([0.0, 0.0, 1.0], [0.5, 0.5, 0.0], [0, 10, 25], c)) < 1e-12
+    h, f, N = [3, 5, 2], [1, 2, 7], 10
+    ref = O.dq_linear_closed_form(h, f, [0, 10, 25], 0.006, N)
+    assert abs(O.dq_continuous([v / N for v in h], [v / N for v in f], [0, 10, 25], c) - ref) < 1e-12
+
+
+def test_is_convex_pins():
+    assert O.is_convex(O.default_degradation())                          # linear
+    assert O.is_convex(np.concatenate([[0.0], np.cumsum(np.linspace(0.001, 0.02, 49))]))   # increasing steps
+    assert not O.is_convex(np.minimum(1.0, 0.09 * np.arange(50)))       # concave cap
+    c = np.zeros(50)
+    c[1:] = 0.5                                                          # a jump: non-convex
+    assert not O.is_convex(c)

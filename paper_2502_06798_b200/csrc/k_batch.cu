@@ -31,7 +31,16 @@
 // counters with 4 prompts per lane and a 5-step warp scan of 4 packed registers per 128 prompts, int4
 // stores of instance and slot, executes MORE instructions per prompt (144 vs 97 warp instructions per 32
 // prompts: register selects for the packed fields, divergent per-prompt branches) and is slower at 64M
-// prompts (407 vs 260 us, profiles/r02_k7/): removed.
+// prompts (407 vs 260 us, profiles/r02_k7/): removed.  Round 2 rework of the rank kernel (profiles/r02_k7b/):
+// the per-instance counts in closed form from K5's inst_pos (no W-step loop per instance, no 64-bit
+// division), a past-the-end dump class so the rank loop has no range tests and the group leader writes
+// its count without a reload, the emit specialised on a full chunk and on the scatter with the scalars
+// hoisted, and {instance, list offset} in one 8-byte table entry: 176M -> 102M warp instructions,
+// 255 -> 224 us at 64M prompts.  Now latency-bound (issue 40 %, short-scoreboard and barrier stalls),
+// not write-bound (a write-only fill reaches 7.1 TB/s here): measured and not kept -- one block barrier
+// instead of three (230 us), the batch-list scatter staged through shared memory in (class, t) order
+// and written coalesced (231 us; the direct scatter's partial sectors merge in L2: DRAM writes equal
+// the algorithmic bytes), 4 or 6 resident CTAs instead of 5 (226 / 265 us).
 // HBM per prompt: class 1 B read twice, instance + slot 8 B written, bucket list 4 B written.
 #include "dispatch.cuh"
 
@@ -59,13 +68,20 @@ __device__ __forceinline__ void load_cls(const uint8_t* __restrict__ src, int64_
   }
 }
 
-// Row j of this warp's chunk for k_cls_rank: prompt base + 32 j + lane (-1 past the end).
+// Row j of this warp's chunk for k_cls_rank: prompt base + 32 j + lane (NCLS past the end: a dump class
+// with its own counter, so the rank loop needs no range test).
 __device__ __forceinline__ void load_rows(const uint8_t* __restrict__ src, int64_t base, int64_t N, int (&v)[ROWS]) {
   const int lane = threadIdx.x & 31;
+  if (base + 32 * ROWS <= N) {   // the whole chunk in range: one base address, immediate offsets
+    const uint8_t* __restrict__ q = src + base + lane;
+#pragma unroll
+    for (int j = 0; j < ROWS; ++j) v[j] = (int)__ldg(q + 32 * j);
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < ROWS; ++j) {
     const int64_t p = base + 32 * j + lane;
-    v[j] = p < N ? (int)__ldg(src + p) : -1;
+    v[j] = p < N ? (int)__ldg(src + p) : NCLS;
   }
 }
 
@@ -109,8 +125,43 @@ __global__ void __launch_bounds__(THREADS) k_cls_count(const uint8_t* __restrict
 }
 
 #ifndef PAS_K7_MINB
-#define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers, no spills
+#define PAS_K7_MINB 5     // resident CTAs per SM the rank kernel is compiled for: 48 registers (a few once-per-warp spills)
 #endif
+
+// The stateless per-row emit of k_cls_rank: t = wb[class] + in-warp rank; greedy (MODE 0/1): q1 = t div b*,
+// q2 = q1 div n_j (exact multiply-high, t < 2^26, n_j <= 64), instance I_j[q1 mod n_j], slot
+// q2 * b* + t mod b*; uniform (MODE 2): instance = class, slot = t.  SCATTER: also write the batch lists;
+// FULL: all 16 rows of the warp's chunk are in range (no per-row end test).
+template <int MODE, bool SCATTER, bool FULL>
+__device__ __forceinline__ void emit_rows(const int (&c)[ROWS], const int32_t* __restrict__ wb, const uint4* cinfo_s,
+                                          const int2* flat_s, const int32_t* ioff,
+                                          int32_t* __restrict__ inst_w, int32_t* __restrict__ slot_w,
+                                          int32_t* __restrict__ prompts, int32_t p_w, uint32_t b, uint32_t sh, int W) {
+#pragma unroll
+  for (int j = 0; j < ROWS; ++j) {
+    const int cj = c[j] & 0xFF, rj = c[j] >> 8;
+    if (!FULL && cj == NCLS) continue;
+    const int t = wb[cj] + rj;
+    int inst, sl, off;
+    if (MODE == 2) {
+      inst = cj;
+      sl = t;
+      off = ioff[cj];
+    } else {
+      const uint32_t q1 = MODE == 0 ? ((uint32_t)t >> sh) : (uint32_t)t / b;
+      const uint4 ci = cinfo_s[cj];
+      const uint32_t q2 = ci.x ? __umulhi(q1, ci.x) : q1;
+      const int2 e = flat_s[ci.z + (q1 - q2 * ci.y)];   // I_j[q1 mod n_j] and its list offset
+      inst = e.x;
+      off = e.y;
+      sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
+    }
+    PAS_CHECK(inst >= 0 && inst < W && sl >= 0 && off == ioff[inst] && off + sl < ioff[inst + 1], "K7 batch-list position");
+    inst_w[32 * j] = inst;
+    slot_w[32 * j] = sl;
+    if (SCATTER) prompts[off + sl] = p_w + 32 * j;   // the batch lists (counting-sort scatter)
+  }
+}
 
 // DISP: the f3 stateful dispatcher picks (a separate instantiation keeps R13 lean).  MODE (the stateless
 // path; compile-time so the per-row loop carries no mode branches or parameter reloads): 0 greedy with
@@ -123,35 +174,42 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
                                                       int32_t* __restrict__ user_off) {
   pdl_entry();
   advance_batch_counters(P);   // the batch's last kernel: every reader of the counters has finished
-  __shared__ int32_t wcnt[WARPS][NCLS];    // per-warp running class counts, then exclusive prefix over warps
+  __shared__ int32_t wcnt[WARPS][NCLS + 1];   // per-warp class counts of this tile (+ the past-the-end dump)
+  __shared__ int32_t wbase[WARPS][NCLS];   // per warp and class: t of the warp's first prompt of the class
   __shared__ int32_t tile_off[NCLS];
-  __shared__ int32_t icount[kMaxInst], ioff[kMaxInst + 1];   // per-instance counts, batch-list offsets
-  // per K' level: {32-bit reciprocal of n_j (0 for n_j = 1), n_j} -- one 8-byte shared load per prompt
-  __shared__ uint2 cinfo_s[kMaxLevels];
-  __shared__ int32_t ilist_s[kMaxLevels][kMaxInst];
+  __shared__ int32_t icount[kMaxInst], fpos[kMaxInst], ioff[kMaxInst + 1];   // per instance: count, flat_s slot, list offset
+  // per K' level j: {32-bit reciprocal of n_j (0 for n_j = 1), n_j, first entry of I_j in flat_s, -}
+  __shared__ uint4 cinfo_s[kMaxLevels];
+  // {instance, batch-list offset} of I_0[0..n_0), I_1[0..n_1), ...: W <= 64 entries (each instance sits
+  // at exactly one level), so the per-prompt instance pick and its list offset are one 8-byte load
+  __shared__ int2 flat_s[kMaxInst];
+  __shared__ __align__(16) int32_t ilist_s[DISP ? kMaxLevels : 1][kMaxInst];   // f3 only: I_j per level
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int64_t base = (int64_t)tile * TILE + w * 32 * ROWS;
   const bool uniform = DISP ? P.mode == PAS_UNIFORM : MODE == 2;
   int c[ROWS];
   load_rows(cls, base, P.N, c);
-  for (int i = threadIdx.x; i < WARPS * NCLS; i += THREADS) (&wcnt[0][0])[i] = 0;
-  if (!uniform) {   // the instance lists of the K' levels, staged once per block
-    if (threadIdx.x < nC) {
-      // q div n_j for q < 2^26 and n_j <= 64 as umulhi(q, ceil(2^32 / n_j)): exact since the
-      // reciprocal's error (< n_j) times q stays below 2^32 (n_j = 1: q itself)
-      const uint32_t nj = (uint32_t)plan->n_inst[threadIdx.x];
-      cinfo_s[threadIdx.x] = make_uint2(nj > 1 ? (uint32_t)((0x100000000ull + nj - 1) / nj) : 0u, nj);
+  for (int i = threadIdx.x; i < WARPS * (NCLS + 1); i += THREADS) (&wcnt[0][0])[i] = 0;
+  if (!uniform) {
+    // K5 wrote n_j's reciprocal (q div n_j = umulhi(q, ceil(2^32 / n_j)), exact for q < 2^26 and
+    // n_j <= 64) and I_j's start in the level-ordered instance list
+    if (threadIdx.x < nC)
+      cinfo_s[threadIdx.x] = make_uint4(plan->n_inst_recip[threadIdx.x], (uint32_t)plan->n_inst[threadIdx.x],
+                                        (uint32_t)plan->inst_base[threadIdx.x], 0u);
+    if (DISP) {   // the instance lists of the K' levels (the f3 picks walk them)
+#pragma unroll 1
+      for (int i = threadIdx.x; i < nC * (kMaxInst / 4); i += THREADS)   // 16-byte copies
+        reinterpret_cast<int4*>(&ilist_s[0][0])[i] = reinterpret_cast<const int4*>(&plan->inst_list[0][0])[i];
     }
-    for (int i = threadIdx.x; i < nC * kMaxInst; i += THREADS)
-      ilist_s[i / kMaxInst][i % kMaxInst] = plan->inst_list[i / kMaxInst][i % kMaxInst];
   }
   if (threadIdx.x < nC) {
     const int64_t row = (int64_t)threadIdx.x * ntiles;
     tile_off[threadIdx.x] = scanned[row + tile] - scanned[row];
   }
   if (threadIdx.x < P.W) {
-    // class totals (from the scanned counts) -> this instance's count (closed form, R13 / R14)
+    // class totals (from the scanned counts) -> this instance's count (closed form, R13 / R14): instance
+    // i is I_j[m] (m = its position among the n_j instances of its level j, from K5)
     const int i = threadIdx.x;
     const int cc = uniform ? i : P.inst_level[i];
     const int64_t start = scanned[(int64_t)cc * ntiles];
@@ -161,15 +219,27 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
     if (DISP) {
       cnt = P.dplan->cnt[i];   // f3: counted by k_disp_prep from the same class totals
     } else if (!uniform) {
-      int m = 0, nj = 0;   // position of i among the instances of its level, their number
-      for (int q = 0; q < P.W; ++q) {
-        m += (P.inst_level[q] == cc && q < i) ? 1 : 0;
-        nj += (P.inst_level[q] == cc) ? 1 : 0;
-      }
-      const int b = P.bstar, full = total / (b * nj), rem = total % (b * nj), extra = rem - m * b;
+      const int m = plan->inst_pos[i], nj = plan->n_inst[cc];
+      const int b = P.bstar, full = total / (b * nj), rem = total - full * (b * nj), extra = rem - m * b;
       cnt = full * b + (extra < 0 ? 0 : (extra > b ? b : extra));
+      fpos[i] = plan->inst_base[cc] + m;
     }
     icount[i] = cnt;
+  }
+  // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count per
+  // class (advanced by the group's lowest lane, whose rank is the count itself) carries the earlier
+  // rows.  The rank is packed above the class byte (c[j] = rank << 8 | class): one register per row.
+  __syncthreads();   // wcnt zeroed
+  const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+  for (int j = 0; j < ROWS; ++j) {
+    const unsigned m = __match_any_sync(0xffffffffu, c[j]);
+    const unsigned below = m & lt;
+    const int r = wcnt[w][c[j]] + __popc(below);
+    __syncwarp();
+    if (below == 0) wcnt[w][c[j]] = r + __popc(m);
+    __syncwarp();
+    c[j] = (r << 8) | c[j];
   }
   __syncthreads();
   if (w == 0) {   // batch-list offsets: exclusive scan of the W <= 64 instance counts, two per lane
@@ -186,6 +256,10 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
     if (i0 < P.W) ioff[i0] = ex;
     if (i1 < P.W) ioff[i1] = ex + a;
     if (lane == 31) ioff[P.W] = incl;   // the total
+    if (!uniform) {
+      if (i0 < P.W) flat_s[fpos[i0]] = make_int2(i0, ex);
+      if (i1 < P.W) flat_s[fpos[i1]] = make_int2(i1, ex + a);
+    }
     if (tile == 0) {
       if (user_off) {
         if (i0 < P.W) user_off[i0] = ex;
@@ -196,28 +270,15 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
       if (i1 < P.W) plan->inst_count[i1] = b;
     }
   }
-  // in-warp rank, row by row: match.any groups the lanes of one class; a per-warp running count
-  // per class (bumped by the lowest lane of each group) carries the earlier rows
-  // the rank is packed above the class byte (c[j] = rank << 8 | class, class 0xFF past the end): one
-  // register per row instead of two
-  const unsigned lt = (1u << lane) - 1;
+  if (threadIdx.x < nC) {   // per class: the tile's offset plus the exclusive prefix over the warps
+    int x[WARPS];
 #pragma unroll
-  for (int j = 0; j < ROWS; ++j) {
-    const unsigned m = __match_any_sync(0xffffffffu, c[j]);
-    const bool lead = lane == __ffs(m) - 1;
-    const int r = c[j] >= 0 ? wcnt[w][c[j]] + __popc(m & lt) : 0;
-    __syncwarp();
-    if (lead && c[j] >= 0) wcnt[w][c[j]] += __popc(m);
-    __syncwarp();
-    c[j] = (r << 8) | (c[j] & 0xFF);
-  }
-  __syncthreads();
-  if (threadIdx.x < nC) {   // per class: the tile's offset plus the exclusive prefix over warps
+    for (int v = 0; v < WARPS; ++v) x[v] = wcnt[v][threadIdx.x];   // independent loads, then a short add chain
     int run = tile_off[threadIdx.x];
-    for (int v2 = 0; v2 < WARPS; ++v2) {
-      const int x = wcnt[v2][threadIdx.x];
-      wcnt[v2][threadIdx.x] = run;
-      run += x;
+#pragma unroll
+    for (int v = 0; v < WARPS; ++v) {
+      wbase[v][threadIdx.x] = run;
+      run += x[v];
     }
   }
   __syncthreads();
@@ -225,36 +286,32 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   int32_t* const inst_w = instance + base + lane;
   int32_t* const slot_w = slot + base + lane;
   const int32_t p_w = (int32_t)(base + lane);   // prompt ids fit int32 (N <= max_batch < 2^31)
-#pragma unroll
-  for (int j = 0; j < ROWS; ++j) {
-    const int cj = c[j] & 0xFF, rj = c[j] >> 8;
-    if (cj == 0xFF) continue;
-    const int t = wcnt[w][cj] + rj;
-    int inst, sl, pos;
-    if (DISP) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
-      int64_t sl64;
-      if (uniform) {
-        inst = cj;
-        sl64 = P.dplan->Q0[inst] + t;
-      } else {
-        disp_pick_greedy(P.dplan, ilist_s[cj], (int)cinfo_s[cj].y, cj, t, P.bstar, inst, sl64);
-      }
-      sl = (int)sl64;
-      pos = (int)(sl64 - P.dplan->Q0[inst]);
-    } else if (uniform) {
-      inst = cj;
-      sl = t;
+  if (!DISP) {   // stateless: the per-row emit specialised on the batch-list scatter and a full chunk
+    const bool full = base + 32 * ROWS <= P.N;
+    const uint32_t bs = (uint32_t)P.bstar, sh = (uint32_t)P.bstar_shift;
+    if (prompts) {
+      if (full) emit_rows<MODE, true, true>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
+      else emit_rows<MODE, true, false>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
     } else {
-      // q1 = t div b*, q2 = q1 div n_j (exact multiply-high, t < 2^26, n_j <= 64):
-      // instance I_j[q1 mod n_j], slot q2 * b* + t mod b*
-      const uint32_t b = (uint32_t)P.bstar;
-      const uint32_t q1 = MODE == 0 ? ((uint32_t)t >> P.bstar_shift) : (uint32_t)t / b;
-      const uint2 ci = cinfo_s[cj];
-      const uint32_t q2 = ci.x ? __umulhi(q1, ci.x) : q1;
-      inst = ilist_s[cj][q1 - q2 * ci.y];
-      sl = (int)(q2 * b + ((uint32_t)t - q1 * b));
+      if (full) emit_rows<MODE, false, true>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
+      else emit_rows<MODE, false, false>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
     }
-    if (!DISP) pos = sl;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < ROWS; ++j) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
+    const int cj = c[j] & 0xFF, rj = c[j] >> 8;
+    if (cj == NCLS) continue;
+    const int t = wbase[w][cj] + rj;
+    int inst;
+    int64_t sl64;
+    if (uniform) {
+      inst = cj;
+      sl64 = P.dplan->Q0[inst] + t;
+    } else {
+      disp_pick_greedy(P.dplan, ilist_s[DISP ? cj : 0], (int)cinfo_s[cj].y, cj, t, P.bstar, inst, sl64);
+    }
+    const int sl = (int)sl64, pos = (int)(sl64 - P.dplan->Q0[inst]);
     PAS_CHECK(inst >= 0 && inst < P.W && pos >= 0 && ioff[inst] + pos < ioff[inst + 1], "K7 batch-list position");
     inst_w[32 * j] = inst;
     slot_w[32 * j] = sl;

@@ -25,12 +25,17 @@ constexpr uint64_t kOne = 1ull << 32;
 
 __device__ void fill_instance_lists(const RouteParams& P, DevPlan* plan, int lane) {
   if (lane < P.nK) {
-    int n = 0;
-    for (int w = 0; w < P.W; ++w)
-      if (P.inst_level[w] == lane) plan->inst_list[lane][n++] = w;
+    int n = 0, nb = 0;
+    for (int w = 0; w < P.W; ++w) {
+      nb += P.inst_level[w] < lane ? 1 : 0;
+      if (P.inst_level[w] == lane) {
+        plan->inst_pos[w] = n;
+        plan->inst_list[lane][n++] = w;
+      }
+    }
+    plan->inst_base[lane] = nb;
     plan->n_inst[lane] = n;
-    const uint64_t d = n > 0 ? (uint64_t)n : 1;
-    plan->n_inst_magic[lane] = ((1ull << 32) + d - 1) / d;
+    plan->n_inst_recip[lane] = n > 1 ? 0xFFFFFFFFu / (uint32_t)n + 1u : 0u;   // = ceil(2^32 / n)
   }
 }
 

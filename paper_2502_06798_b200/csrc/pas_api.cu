@@ -2,6 +2,7 @@
 // pipeline K1..K7 on the caller's stream, the cache store, and the NCCL all-gather for world > 1.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: a no-op unless a tool (nsys) injects itself
 
 #include <cmath>
 #include <cstdarg>
@@ -168,6 +169,7 @@ struct pas_ctx {
   uint8_t *x_level = nullptr, *x_flags = nullptr;
   // timing
   cudaEvent_t ev[8]{};
+  nvtxRangeId_t nvtx_range = 0;   // the open NVTX range of the stage being enqueued (0: none)
   cudaEvent_t ev_aux = nullptr;   // end event of pas_solve_assignment's timing
   // stage-timing ring (pas_stage_ring): the 7 stage boundaries of each of the last ring_n batches
   std::vector<cudaEvent_t> ring;
@@ -230,8 +232,18 @@ int64_t local_rows_below(int64_t total, int G, int rank) {
   return total > rank ? (total - rank + G - 1) / G : 0;
 }
 
-// Record stage boundary i (0..6) of the current batch: ev[i], and its slot of the timing ring.
+// NVTX range names of the stages between boundaries i and i + 1 (tracing row).
+constexpr const char* kStageNvtx[6] = {"pas K1 normalise",      "pas K2 similarity + top-k",
+                                       "pas K3/K4 merge + optimal-K", "pas K5 plan",
+                                       "pas K6 redirect",       "pas K7 route-and-batch"};
+
+// Record stage boundary i (0..6) of the current batch: ev[i], and its slot of the timing ring.  The
+// host-side enqueue of each stage is also an NVTX range (process-wide start/end ranges, so a batch
+// enqueued from several threads stays well-formed; a range left open by an error closes at the next
+// boundary), which nsys correlates with the stage's kernels.
 cudaError_t rec_stage(pas_ctx* ctx, int i, cudaStream_t st) {
+  if (ctx->nvtx_range) nvtxRangeEnd(ctx->nvtx_range);
+  ctx->nvtx_range = i < 6 ? nvtxRangeStartA(kStageNvtx[i]) : 0;
   if (ctx->capturing) return cudaSuccess;   // a replayed graph is timed as a whole (pas_route_batch)
   cudaError_t e = cudaEventRecord(ctx->ev[i], st);
   if (e == cudaSuccess && ctx->ring_n > 0) e = cudaEventRecord(ctx->ring[(ctx->ring_pos % ctx->ring_n) * 7 + i], st);

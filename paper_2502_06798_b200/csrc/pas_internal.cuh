@@ -162,8 +162,11 @@ struct DevPlan {
   int X[kMaxLevels][kMaxLevels];     // inclusive prefix sums of the rows of x
   int class_start[kMaxLevels + 1];   // exclusive prefix of h
   int n_inst[kMaxLevels];
-  uint64_t n_inst_magic[kMaxLevels];   // ceil(2^32 / n_j): x / n_j == (x * magic) >> 32 for x < 2^26
-  int inst_list[kMaxLevels][kMaxInst];
+  uint32_t n_inst_recip[kMaxLevels];   // ceil(2^32 / n_j) for n_j > 1, 0 for n_j <= 1: q div n_j ==
+                                       // umulhi(q, recip) for q < 2^26 (the error < n_j times q stays < 2^32)
+  alignas(16) int inst_list[kMaxLevels][kMaxInst];   // 16-byte aligned: K7 stages it with int4 copies
+  int inst_pos[kMaxInst];              // position of instance i in inst_list[its level] (K7's closed form)
+  int inst_base[kMaxLevels];           // #instances at levels < j: I_j's first entry in a level-ordered list
   double D_Q, D_Q_LP;
   int n_redirected, n_upgraded, n_downgraded;
   int n_invalid, n_near_top1, n_near_threshold;

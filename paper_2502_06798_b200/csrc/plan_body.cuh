@@ -339,12 +339,17 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
       plan->X[i][j] = acc;
     }
     // I_j: ascending instance ids at level j, and the multiply-high constant for div n_j
-    int n = 0;
-    for (int w = 0; w < P.W; ++w)
-      if (P.inst_level[w] == i) plan->inst_list[i][n++] = w;
+    int n = 0, nb = 0;
+    for (int w = 0; w < P.W; ++w) {
+      nb += P.inst_level[w] < i ? 1 : 0;
+      if (P.inst_level[w] == i) {
+        plan->inst_pos[w] = n;
+        plan->inst_list[i][n++] = w;
+      }
+    }
+    plan->inst_base[i] = nb;
     plan->n_inst[i] = n;
-    const uint64_t d = n > 0 ? (uint64_t)n : 1;
-    plan->n_inst_magic[i] = ((1ull << 32) + d - 1) / d;
+    plan->n_inst_recip[i] = n > 1 ? 0xFFFFFFFFu / (uint32_t)n + 1u : 0u;   // = ceil(2^32 / n)
   }
   if (lane == 0) {
     plan->class_start[nK] = hc[nK];

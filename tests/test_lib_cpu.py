@@ -87,3 +87,17 @@ def test_binding_rejects_bad_embedding_layouts(lib):
         assert lib._rows(fake, torch.zeros(4, 768), device=False).value is not None
     finally:
         lib._CTX_D.pop(fake.value)
+
+
+def test_nvtx_stage_ranges_built_in(lib, tmp_path):
+    """The six stage range names are in the library (SURVEY 5 tracing row; exercised on the GPU by
+    tests/test_gpu_nvtx.py) and the test-only injection probe builds and exports its entry point."""
+    data = open(lib.LIB_PATH, "rb").read()
+    for name in ("K1 normalise", "K2 similarity + top-k", "K3/K4 merge + optimal-K", "K5 plan", "K6 redirect",
+                 "K7 route-and-batch"):
+        assert b"pas " + name.encode() + b"\0" in data, name
+    probe = str(tmp_path / "probe.so")
+    subprocess.run(["gcc", "-shared", "-fPIC", "-O2", "-o", probe, os.path.join(ROOT, "tests", "native", "nvtx_probe.c")],
+                   check=True)
+    out = subprocess.run(["nm", "-D", "--defined-only", probe], capture_output=True, text=True).stdout
+    assert re.search(r"\bT InitializeInjectionNvtx2\b", out)

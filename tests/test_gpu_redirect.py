@@ -64,6 +64,8 @@ def test_k6_large_batches(pas, N, probs, F, mode, fallback, monkeypatch):
     r.set_fractions(F, inst, bstar, mode)
     r.load_cache(torch.ones(1, cfg.d, device=DEV))      # a warm cache: K comes from the candidates
     o = r.alloc_out(N, optional=False)
+    o["bucket_offsets"] = torch.empty(pas.PAS_MAX_INSTANCES + 1, dtype=torch.int32, device=DEV)
+    o["bucket_prompts"] = torch.empty(N, dtype=torch.int32, device=DEV)
     for b in range(2):
         pas.pas_route_from_candidates(r.ctx, cand, 1, N, o)
         torch.cuda.synchronize()
@@ -85,4 +87,12 @@ def test_k6_large_batches(pas, N, probs, F, mode, fallback, monkeypatch):
             pick = ((u * nj) >> np.uint64(32)).astype(np.int64)
             want = np.array([I[j][q] if len(I[j]) else -1 for j, q in zip(kp, pick)])
             assert np.array_equal(o["instance"].cpu().numpy(), want)
+        # K7 on every prompt (the rank kernel's tiles, its persistent walk over > 740 tiles at 2^22,
+        # ragged tails): instance, slot and the batch lists vs the oracle
+        wi, ws = O.route_and_batch(kp, inst, bstar, mode, cfg.route_seed, b)
+        assert np.array_equal(o["instance"].cpu().numpy(), wi), f"batch {b}: instance differs"
+        assert np.array_equal(o["slot"].cpu().numpy(), ws), f"batch {b}: slot differs"
+        off, pr = O.buckets(wi, ws, len(inst))
+        assert np.array_equal(o["bucket_offsets"][:len(inst) + 1].cpu().numpy(), off)
+        assert np.array_equal(o["bucket_prompts"].cpu().numpy(), pr)
     r.close()

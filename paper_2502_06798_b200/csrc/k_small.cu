@@ -2,8 +2,9 @@
 // latency).  For N <= kSmallMax prompts the multi-kernel downstream (merge +
 // optimal-K, plan, 6 redirect kernels, count / scan / rank) is a chain of ~11 launches of a few
 // microseconds each; here ONE CTA of 1024 threads runs all of it from the K2 candidates:
-//   a4/a5  thread per prompt: S-way merge of the sorted candidate lists (score desc, gid asc, ties to
-//          the lower source, R10), optimal-K level #{m : s1 >= t_m}, flags, LRU stamp of the top-1
+//   a4/a5  S-way merge of the sorted candidate lists (score desc, gid asc, ties to the lower source,
+//          R10) -- eight lanes per prompt with a shuffle tournament per output when S, k <= 8, else a
+//          thread per prompt --, optimal-K level #{m : s1 >= t_m}, flags, LRU stamp of the top-1
 //          (R26), H_K and the flag counters in shared memory;
 //   a6     warp 0: the Eq. 1 plan (plan_body: the same code as K5);
 //   a7     kappa_p = Philox(p) (stream 1), the class rank of (kappa, p) by counting (O(N) per prompt over
@@ -58,56 +59,9 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
     }
   }
   __syncthreads();
-  // ---- a4 + a5: merge (a thread per prompt; cursors in registers for S <= 8), optimal-K, flags,
-  // stamps, H_K.  (A warp per prompt with shuffle reductions measured 3x slower here: 64 prompts.)
-  for (int p = tid; p < N; p += SM_THREADS) {
-    const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
-    Cand res[PAS_MAX_TOPK];
-    if (invalid || cold) {
-      for (int i = 0; i < k; ++i) res[i] = Cand{-INFINITY, -1};
-    } else if (S <= 8) {
-      int pos[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int i = 0; i < k; ++i) {
-        Cand best{-INFINITY, -1};
-        int bs = -1;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          if (s >= S || pos[s] >= k) continue;
-          const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
-          if (bs < 0 || cand_better(c, best)) {
-            best = c;
-            bs = s;
-          }
-        }
-#pragma unroll
-        for (int s = 0; s < 8; ++s) pos[s] += s == bs ? 1 : 0;
-        res[i] = bs >= 0 ? best : Cand{-INFINITY, -1};
-      }
-    } else {
-      uint8_t pos[128];
-      for (int s = 0; s < S; ++s) pos[s] = 0;
-      for (int i = 0; i < k; ++i) {
-        Cand best{-INFINITY, -1};
-        int bs = -1;
-        for (int s = 0; s < S; ++s) {
-          if (pos[s] >= k) continue;
-          PAS_CHECK(p < stride, "small path candidate row");
-          const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
-          if (bs < 0 || cand_better(c, best)) {
-            best = c;
-            bs = s;
-          }
-        }
-        if (bs >= 0) pos[bs]++;
-        res[i] = bs >= 0 ? best : Cand{-INFINITY, -1};
-      }
-    }
-    for (int i = 0; i < k; ++i) {
-      if (o.topk_id) o.topk_id[(int64_t)p * k + i] = res[i].g;
-      if (o.topk_score) o.topk_score[(int64_t)p * k + i] = res[i].s;
-    }
-    // select_one of k_merge.cu
-    const float s1 = res[0].s, s2 = k > 1 ? res[1].s : -INFINITY;
+  // ---- a4 + a5: merge, optimal-K, flags, stamps, H_K
+  // select_one of k_merge.cu for prompt p with its merged s1, s2 (-inf for k = 1) and top-1 id
+  auto finish = [&](int p, bool invalid, float s1, float s2, int32_t g1) {
     int lv = 0;
     uint8_t fl = 0;
     if (invalid) fl |= PAS_FLAG_INVALID;
@@ -120,7 +74,6 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
       if ((lv > 0 && s1 - P.thr[lv - 1] < 2e-2f) || (lv < nK - 1 && P.thr[lv] - s1 < 2e-2f))
         fl |= PAS_FLAG_NEAR_THRESHOLD;
     }
-    const int32_t g1 = res[0].g;
     if (P.lru_stamp && !invalid && !cold && g1 >= 0 && g1 < P.M_total) P.lru_stamp[g1] = tick;
     lvl_s[p] = (uint8_t)lv;
     o.level[p] = (uint8_t)lv;
@@ -130,6 +83,118 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_route(const Cand* __res
     if (fl & PAS_FLAG_INVALID) atomicAdd(&cnt_s[0], 1);
     if (fl & PAS_FLAG_NEAR_TOP1) atomicAdd(&cnt_s[1], 1);
     if (fl & PAS_FLAG_NEAR_THRESHOLD) atomicAdd(&cnt_s[2], 1);
+  };
+  if (S <= 8 && k <= 8) {
+    // eight lanes per prompt, lane g holding source list g in registers; each round a width-8
+    // shuffle tournament takes the best head (score desc, gid asc, then the lower source, R10) and its
+    // lane advances -- k rounds of three shuffle steps instead of k * S dependent shared loads on one
+    // thread (64 prompts: all of them at once on 512 threads)
+    const int g = tid & 7;
+    for (int base = 0; base < N * 8; base += SM_THREADS) {
+      const int p = (base + tid) >> 3;
+      const bool act = p < N;   // group-uniform; whole warps shuffle (inactive groups carry padding)
+      const bool invalid = act && pflags && (pflags[p] & PAS_FLAG_INVALID);
+      const bool live = act && !invalid && !cold && g < S;
+      Cand L[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        L[i] = (live && i < k) ? (staged ? cand_s[(g * N + p) * k + i] : in[((int64_t)g * stride + p) * k + i])
+                               : Cand{-INFINITY, -1};
+      float s1 = -INFINITY, s2 = -INFINITY;
+      int32_t g1 = -1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i >= k) break;
+        float bs = L[0].s;
+        int32_t bg = L[0].g;
+        int bsrc = g;
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) {
+          const float os = __shfl_xor_sync(0xffffffffu, bs, off, 8);
+          const int32_t og = __shfl_xor_sync(0xffffffffu, bg, off, 8);
+          const int osrc = __shfl_xor_sync(0xffffffffu, bsrc, off, 8);
+          if (os > bs || (os == bs && ((unsigned)og < (unsigned)bg || (og == bg && osrc < bsrc)))) {
+            bs = os;
+            bg = og;
+            bsrc = osrc;
+          }
+        }
+        if (bsrc == g) {   // this lane's head was taken: advance
+#pragma unroll
+          for (int j = 0; j < 7; ++j) L[j] = L[j + 1];
+          L[7] = Cand{-INFINITY, -1};
+        }
+        if (act && g == (i & 7)) {
+          if (o.topk_id) o.topk_id[(int64_t)p * k + i] = bg;
+          if (o.topk_score) o.topk_score[(int64_t)p * k + i] = bs;
+        }
+        if (i == 0) {
+          s1 = bs;
+          g1 = bg;
+        } else if (i == 1) {
+          s2 = bs;
+        }
+      }
+      if (act && g == 0) finish(p, invalid, s1, s2, g1);
+    }
+  } else {   // a thread per prompt
+    for (int p = tid; p < N; p += SM_THREADS) {
+      const bool invalid = pflags && (pflags[p] & PAS_FLAG_INVALID);
+      // each merged entry goes straight to the outputs; s1, s2 and the top-1 id stay in registers
+      // (a per-thread result array would live in local memory)
+      float s1 = -INFINITY, s2 = -INFINITY;
+      int32_t g1 = -1;
+      auto emit = [&](int i, const Cand& c) {
+        if (o.topk_id) o.topk_id[(int64_t)p * k + i] = c.g;
+        if (o.topk_score) o.topk_score[(int64_t)p * k + i] = c.s;
+        if (i == 0) {
+          s1 = c.s;
+          g1 = c.g;
+        } else if (i == 1) {
+          s2 = c.s;
+        }
+      };
+      if (invalid || cold) {
+        for (int i = 0; i < k; ++i) emit(i, Cand{-INFINITY, -1});
+      } else if (S <= 8) {
+        int pos[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < k; ++i) {
+          Cand best{-INFINITY, -1};
+          int bs = -1;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            if (s >= S || pos[s] >= k) continue;
+            const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
+            if (bs < 0 || cand_better(c, best)) {
+              best = c;
+              bs = s;
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < 8; ++s) pos[s] += s == bs ? 1 : 0;
+          emit(i, bs >= 0 ? best : Cand{-INFINITY, -1});
+        }
+      } else {
+        uint8_t pos[128];
+        for (int s = 0; s < S; ++s) pos[s] = 0;
+        for (int i = 0; i < k; ++i) {
+          Cand best{-INFINITY, -1};
+          int bs = -1;
+          for (int s = 0; s < S; ++s) {
+            if (pos[s] >= k) continue;
+            PAS_CHECK(p < stride, "small path candidate row");
+            const Cand c = staged ? cand_s[(s * N + p) * k + pos[s]] : in[((int64_t)s * stride + p) * k + pos[s]];
+            if (bs < 0 || cand_better(c, best)) {
+              best = c;
+              bs = s;
+            }
+          }
+          if (bs >= 0) pos[bs]++;
+          emit(i, bs >= 0 ? best : Cand{-INFINITY, -1});
+        }
+      }
+      finish(p, invalid, s1, s2, g1);
+    }
   }
   __syncthreads();
   // ---- a6: the plan, one warp (the same code as K5)

@@ -29,13 +29,16 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
   const int V = 2 * nK + 2, S = 0, T = 2 * nK + 1;   // S, rows 1..nK, cols nK+1..2nK, T
   // working arrays in shared memory (one thread runs the solver; no per-thread stack frame)
   __shared__ Cost2 C[kMaxLevels][kMaxLevels];
+#pragma unroll 1
   for (int i = 0; i < nK; ++i)
+#pragma unroll 1
     for (int j = 0; j < nK; ++j) {
       const int dk = P.grid[j] - P.grid[i];
       C[i][j] = {dk > 0 ? P.cI[dk] : 0, (long long)dk * dk};
       x[i][j] = 0;
     }
   __shared__ int rs[kMaxLevels], rd[kMaxLevels];
+#pragma unroll 1
   for (int i = 0; i < nK; ++i) {
     rs[i] = h[i];
     rd[i] = f[i];
@@ -43,10 +46,12 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
   __shared__ Cost2 pot[2 * kMaxLevels + 2], dist[2 * kMaxLevels + 2];
   __shared__ int prev[2 * kMaxLevels + 2];
   __shared__ bool done[2 * kMaxLevels + 2];
+#pragma unroll 1
   for (int v = 0; v < V; ++v) pot[v] = {0, 0};
   int iters = 0;
   const int cap = 64 * nK * nK + 64;
   int left = 0;
+#pragma unroll 1
   for (int i = 0; i < nK; ++i) left += rs[i];
   // residual capacity of edge u -> v (0 = absent); cost of u -> v
   auto rcap = [&](int u, int v) -> long long {
@@ -65,18 +70,22 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
   };
   while (left > 0) {
     if (++iters > cap) return -1;
+#pragma unroll 1
     for (int v = 0; v < V; ++v) {
       dist[v] = {kInfD, 0};
       done[v] = false;
       prev[v] = -1;
     }
     dist[S] = {0, 0};
+#pragma unroll 1
     for (int it = 0; it < V; ++it) {   // dense Dijkstra on reduced costs (all >= 0)
       int u = -1;
+#pragma unroll 1
       for (int v = 0; v < V; ++v)
         if (!done[v] && dist[v].d < kInfD && (u < 0 || lt(dist[v], dist[u]))) u = v;
       if (u < 0) break;
       done[u] = true;
+#pragma unroll 1
       for (int v = 0; v < V; ++v) {
         if (done[v] || rcap(u, v) <= 0) continue;
         const Cost2 nd = add(dist[u], sub(add(cost(u, v), pot[u]), pot[v]));
@@ -87,12 +96,15 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
       }
     }
     if (dist[T].d >= kInfD) return -1;   // cannot happen: every cell is open
+#pragma unroll 1
     for (int v = 0; v < V; ++v) pot[v] = add(pot[v], (dist[v].d < kInfD && lt(dist[v], dist[T])) ? dist[v] : dist[T]);
     long long b = kInfD;
+#pragma unroll 1
     for (int v = T; v != S; v = prev[v]) {
       const long long c = rcap(prev[v], v);
       b = c < b ? c : b;
     }
+#pragma unroll 1
     for (int v = T; v != S; v = prev[v]) {
       const int u = prev[v];
       if (u == S) rs[v - 1] -= (int)b;
@@ -104,17 +116,22 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
   }
   // optimal face: cells with zero reduced cost under the final potentials (optimal duals)
   __shared__ bool tight[kMaxLevels][kMaxLevels];
+#pragma unroll 1
   for (int i = 0; i < nK; ++i)
+#pragma unroll 1
     for (int j = 0; j < nK; ++j) tight[i][j] = is_zero(sub(add(C[i][j], pot[1 + i]), pot[1 + nK + j]));
   // lexicographically greatest x in row-major order on the face: raise x_ij along cycles
   // row i -> col j -> row r (lower a later cell (r, j)) -> col c (raise a later tight (r, c)) -> ... -> row i
   __shared__ int q[2 * kMaxLevels], from[2 * kMaxLevels];
+#pragma unroll 1
   for (int e = 0; e < nK * nK; ++e) {
     const int i = e / nK, j = e % nK;
     if (!tight[i][j]) continue;
+#pragma unroll 1
     for (;;) {
       if (++iters > cap) return -1;
       // BFS over nodes: rows 0..nK-1, cols nK..2nK-1; start at col j, target row i
+#pragma unroll 1
       for (int v = 0; v < 2 * nK; ++v) from[v] = -2;
       int qh = 0, qt = 0;
       q[qt++] = nK + j;
@@ -124,6 +141,7 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
         const int u = q[qh++];
         if (u >= nK) {   // col c: lower a later cell (r, c) with x > 0
           const int c = u - nK;
+#pragma unroll 1
           for (int r = 0; r < nK; ++r)
             if (from[r] == -2 && r * nK + c > e && x[r][c] > 0) {
               from[r] = u;
@@ -135,6 +153,7 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
             }
         } else {         // row r: raise a later tight cell (r, c)
           const int r = u;
+#pragma unroll 1
           for (int c = 0; c < nK; ++c)
             if (from[nK + c] == -2 && r * nK + c > e && tight[r][c]) {
               from[nK + c] = u;
@@ -144,6 +163,7 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
       }
       if (!found) break;
       long long b = kInfD;
+#pragma unroll 1
       for (int v = i; from[v] != -1; v = from[v]) {
         const int u = from[v];
         if (u >= nK) {   // col u -> row v: lowered cell (v, u - nK)
@@ -151,6 +171,7 @@ __device__ __forceinline__ int mcf_plan(const int* h, const int* f, const RouteP
           b = c < b ? c : b;
         }
       }
+#pragma unroll 1
       for (int v = i; from[v] != -1; v = from[v]) {
         const int u = from[v];
         if (u >= nK) x[v][u - nK] -= (int)b;   // lowered
@@ -185,11 +206,13 @@ __device__ __forceinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLeve
   int nz = 0, ns = 0, slot = 0;
   int64_t used = 0;
   bool fallback = false;
+#pragma unroll 1
   for (int i = 0; i < nK; ++i) {
     const int h = h_s[i];
     plan->cls_zone0[i] = nz;
     plan->cls_slot0[i] = slot;
     int jb = 0, X = 0, lastX = -1, zc = -1;
+#pragma unroll 1
     for (int j = 0; j + 1 < nK; ++j) {
       X += x[i][j];
       if (X <= 0) {        // every class prompt has rank >= 0
@@ -228,8 +251,10 @@ __device__ __forceinline__ void k6_zones(const int* h_s, const int (*x)[kMaxLeve
     }
     // K' level below each zone of the class (rank below all its splits) and above all of them
     int j = jb;
+#pragma unroll 1
     for (int z = plan->cls_zone0[i]; z < nz; ++z) {
       plan->z_jbelow[z] = j;
+#pragma unroll 1
       for (int t = 0; t < plan->z_nsplit[z]; ++t) j += plan->s_mult[plan->z_first[z] + t];
       const double E = (double)(plan->z_hi[z] - plan->z_lo[z]) / two60 * h;
       int64_t cap = (int64_t)(2.0 * E) + 1024;
@@ -275,6 +300,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
   __syncwarp();
   if (lane < nK) {
     int rank = 0;
+#pragma unroll 1
     for (int j = 0; j < nK; ++j) rank += (frac_s[j] > frac || (frac_s[j] == frac && j < lane)) ? 1 : 0;
     f_s[lane] = fl + (rank < R ? 1 : 0);
   }
@@ -282,6 +308,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
   if (lane == 0) {   // cumulative sums (<= 16 terms)
     hc[0] = 0;
     fc[0] = 0;
+#pragma unroll 1
     for (int i = 0; i < nK; ++i) {
       hc[i + 1] = hc[i] + h_s[i];
       fc[i + 1] = fc[i] + f_s[i];
@@ -290,6 +317,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
   __syncwarp();
   // ---- O6 plan: NW-corner coupling in closed form (convex c), else the exact min-cost solver (R37)
   if (P.convex) {
+#pragma unroll 1
     for (int e = lane; e < nK * nK; e += 32) {
       const int i = e / nK, j = e % nK;
       const int lo = max(hc[i], fc[j]), hi = min(hc[i + 1], fc[j + 1]);
@@ -304,6 +332,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
   double dq = 0.0, lp = 0.0;
   int n_red = 0, n_up = 0, n_down = 0;
   const double invN = N > 0 ? __ddiv_rn(1.0, (double)N) : 0.0;
+#pragma unroll 1
   for (int e = lane; e < nK * nK; e += 32) {
     const int i = e / nK, j = e % nK;
     const int x = x_s[i][j];
@@ -317,6 +346,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
     // D_Q_LP: the same monotone coupling on the unrounded masses (h/N, F), context only
     double hlo = __dmul_rn((double)hc[i], invN), hhi = __dmul_rn((double)hc[i + 1], invN);
     double flo = 0.0, fhi = 0.0;
+#pragma unroll 1
     for (int jj = 0; jj < j; ++jj) flo = __dadd_rn(flo, P.F[jj]);
     fhi = __dadd_rn(flo, P.F[j]);
     const double ov = fmin(hhi, fhi) - fmax(hlo, flo);
@@ -334,12 +364,14 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
     plan->f[i] = f_s[i];
     plan->class_start[i] = hc[i];
     int acc = 0;
+#pragma unroll 1
     for (int j = 0; j < nK; ++j) {
       acc += x_s[i][j];
       plan->X[i][j] = acc;
     }
     // I_j: ascending instance ids at level j, and the multiply-high constant for div n_j
     int n = 0, nb = 0;
+#pragma unroll 1
     for (int w = 0; w < P.W; ++w) {
       nb += P.inst_level[w] < i ? 1 : 0;
       if (P.inst_level[w] == i) {

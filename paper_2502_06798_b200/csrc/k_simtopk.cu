@@ -470,6 +470,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         t1 = (int)((int64_t)(r + 1) * NT / R);
       }
       const int64_t prompt = (int64_t)m * UNIT_ROWS + (PAIR ? crank * BM : 0) + row;
+      // a warp whose 32 rows are all past the batch (the padding of the last prompt tile) has no lists
+      // to keep: it skips the epilogue work (those Q_hat rows are whatever the buffer holds, and a
+      // list fed garbage scores inserts on most chunks -- C1: 5.5 us of K2's 18.5)
+      const bool warp_live = __any_sync(0xffffffffu, prompt < N);
       float s[KMAX];
       int32_t gl[KMAX];
 #pragma unroll
@@ -492,7 +496,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tc_fence_after();
         const int col_base = t * BN + half * (BN / 2);
         const uint32_t taddr = lane_addr + acc * BN;
-        if (DUMP) {
+        if (!warp_live) {
+          // nothing to rank (the accumulator is released below like any other)
+        } else if (DUMP) {
 #pragma unroll 1
           for (int c = 0; c < BN / 64; ++c) {
             uint32_t v[32];

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
   int32_t* const inst_w = instance + base + lane;
   int32_t* const slot_w = slot + base + lane;
   const int32_t p_w = (int32_t)(base + lane);   // prompt ids fit int32 (N <= max_batch < 2^31)
-  if (!DISP) {   // stateless: the per-row emit specialised on the batch-list scatter and a full chunk
+  if constexpr (!DISP) {   // stateless: the per-row emit specialised on the batch-list scatter and a full chunk
     const bool full = base + 32 * ROWS <= P.N;
     const uint32_t bs = (uint32_t)P.bstar, sh = (uint32_t)P.bstar_shift;
     if (prompts) {
@@ -297,26 +297,26 @@ __global__ void __launch_bounds__(THREADS, DISP ? 1 : PAS_K7_MINB) k_cls_rank(co
       if (full) emit_rows<MODE, false, true>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
       else emit_rows<MODE, false, false>(c, wbase[w], cinfo_s, flat_s, ioff, inst_w, slot_w, prompts, p_w, bs, sh, P.W);
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int j = 0; j < ROWS; ++j) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
-    const int cj = c[j] & 0xFF, rj = c[j] >> 8;
-    if (cj == NCLS) continue;
-    const int t = wbase[w][cj] + rj;
-    int inst;
-    int64_t sl64;
-    if (uniform) {
-      inst = cj;
-      sl64 = P.dplan->Q0[inst] + t;
-    } else {
-      disp_pick_greedy(P.dplan, ilist_s[DISP ? cj : 0], (int)cinfo_s[cj].y, cj, t, P.bstar, inst, sl64);
+    for (int j = 0; j < ROWS; ++j) {   // f3 stateful dispatcher: slot = position in the instance's queue (R29, R31)
+      const int cj = c[j] & 0xFF, rj = c[j] >> 8;
+      if (cj == NCLS) continue;
+      const int t = wbase[w][cj] + rj;
+      int inst;
+      int64_t sl64;
+      if (uniform) {
+        inst = cj;
+        sl64 = P.dplan->Q0[inst] + t;
+      } else {
+        disp_pick_greedy(P.dplan, ilist_s[cj], (int)cinfo_s[cj].y, cj, t, P.bstar, inst, sl64);
+      }
+      const int sl = (int)sl64, pos = (int)(sl64 - P.dplan->Q0[inst]);
+      PAS_CHECK(inst >= 0 && inst < P.W && pos >= 0 && ioff[inst] + pos < ioff[inst + 1], "K7 batch-list position");
+      inst_w[32 * j] = inst;
+      slot_w[32 * j] = sl;
+      if (prompts) prompts[ioff[inst] + pos] = p_w + 32 * j;   // the batch lists (counting-sort scatter)
     }
-    const int sl = (int)sl64, pos = (int)(sl64 - P.dplan->Q0[inst]);
-    PAS_CHECK(inst >= 0 && inst < P.W && pos >= 0 && ioff[inst] + pos < ioff[inst + 1], "K7 batch-list position");
-    inst_w[32 * j] = inst;
-    slot_w[32 * j] = sl;
-    if (prompts) prompts[ioff[inst] + pos] = p_w + 32 * j;   // the batch lists (counting-sort scatter)
   }
 }
 

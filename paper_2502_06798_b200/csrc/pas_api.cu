@@ -74,11 +74,6 @@ EncodeTiledFn get_encode_fn() {
 thread_local std::string g_global_err;
 
 
-int ceil_log2(int64_t v) {
-  int b = 0;
-  while (((int64_t)1 << b) < v) ++b;
-  return b;
-}
 }  // namespace
 
 // ----------------------------------------------------------------------------------------------

@@ -351,6 +351,22 @@ pas_status pas_set_graph(pas_ctx* ctx, int on);
 pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
                                 const pas_route_out* out_host, pas_stream stream);
 
+/* Pipelined form of pas_route_batch_host for a stream of batches: enqueues the host→device copy of
+ * emb_host on the context's H2D copy stream, the batch on `stream` (after that copy), and the copies of
+ * every non-NULL array of out_host on the context's D2H copy stream (after the batch), and returns
+ * without waiting, so the copies of one batch overlap the routing of its neighbours.  Two staging slots
+ * (inputs and outputs on the device): a call blocks the host only until the batch issued two calls
+ * earlier has delivered its outputs.  emb_host and out_host must stay valid (pinned for speed) until
+ * that batch is done; the outputs are complete once `stream` has passed pas_route_host_end.
+ * pas_route_host_begin(ctx, stream): the copy streams wait for all work enqueued on `stream` so far (a
+ * timing or ordering fence before a pipelined run).  pas_route_host_end(ctx, stream): `stream` waits
+ * for every batch issued so far, outputs included (does not block the host).  Same arguments and
+ * errors as pas_route_batch_host; graph mode re-captures for each slot's buffers. */
+pas_status pas_route_batch_host_async(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
+                                      const pas_route_out* out_host, pas_stream stream);
+pas_status pas_route_host_begin(pas_ctx* ctx, pas_stream stream);
+pas_status pas_route_host_end(pas_ctx* ctx, pas_stream stream);
+
 /* Split form of pas_route_batch for callers with their own transport (and for single-GPU tests of
  * the sharded path).  pas_route_local runs a1+a3+the intra-GPU part of a4 on this rank's shard and
  * writes cand_dev: device [N x topk] pairs {float score; int32 gid} (8 bytes each, score desc, gid asc,

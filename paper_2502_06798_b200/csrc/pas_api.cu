@@ -154,6 +154,20 @@ struct pas_ctx {
           *s_boff = nullptr, *s_bpr = nullptr;
   float* s_tsc = nullptr;
   uint8_t* s_flags = nullptr;
+  // pipelined host API (pas_route_batch_host_async): two staging slots (input + every output), an H2D
+  // and a D2H copy stream, per slot: input copied / batch routed / outputs copied
+  struct HostSlot {
+    void* emb = nullptr;
+    int32_t *K = nullptr, *Kp = nullptr, *inst = nullptr, *slot = nullptr, *tid = nullptr, *boff = nullptr,
+            *bpr = nullptr;
+    float* tsc = nullptr;
+    uint8_t* flags = nullptr;
+    cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+    bool used = false;
+  } hs[2];
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t h_join = nullptr;
+  int64_t hseq = 0;
   // tensor maps
   CUtensorMap tm_q{}, tm_c{}, tm_c2{};
   // comm
@@ -613,6 +627,16 @@ pas_status pas_destroy(pas_ctx* ctx) {
                   ctx->s_flags, ctx->x_cand, ctx->x_K, ctx->x_level, ctx->x_flags};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& h : ctx->hs) {
+    void* hp[] = {h.emb, h.K, h.Kp, h.inst, h.slot, h.tid, h.boff, h.bpr, h.tsc, h.flags};
+    for (void* p : hp)
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : {h.h2d, h.done, h.d2h})
+      if (e) cudaEventDestroy(e);
+  }
+  if (ctx->h_join) cudaEventDestroy(ctx->h_join);
+  if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_aux) cudaEventDestroy(ctx->ev_aux);
@@ -1391,6 +1415,27 @@ pas_status pas_route_batch(pas_ctx* ctx, const void* emb, pas_dtype dtype, int64
   return route_enqueue(ctx, emb, dtype, N, out, st);
 }
 
+namespace {
+// The device→host copies of one routed batch (every non-NULL array of oh) on stream st.
+pas_status copy_out(pas_ctx* ctx, const pas_route_out& od, const pas_route_out* oh, int64_t N, cudaStream_t st) {
+  const int64_t k = ctx->cfg.topk;
+  const int W = ctx->W;
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K, od.K, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K_prime, od.K_prime, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->instance, od.instance, N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(oh->slot, od.slot, N * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->topk_id) CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_id, od.topk_id, N * k * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->topk_score)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_score, od.topk_score, N * k * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->flags) CUDA_TRY(ctx, cudaMemcpyAsync(oh->flags, od.flags, N, cudaMemcpyDeviceToHost, st));
+  if (oh->bucket_offsets)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_offsets, od.bucket_offsets, (W + 1) * 4, cudaMemcpyDeviceToHost, st));
+  if (oh->bucket_prompts)
+    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_prompts, od.bucket_prompts, N * 4, cudaMemcpyDeviceToHost, st));
+  return PAS_OK;
+}
+}  // namespace
+
 pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
                                 const pas_route_out* oh, pas_stream stream) {
   pas_status s = check_live(ctx);
@@ -1427,20 +1472,86 @@ pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dt
                    oh->bucket_offsets ? ctx->s_boff : nullptr,
                    oh->bucket_prompts ? ctx->s_bpr : nullptr};
   if ((s = pas_route_batch(ctx, ctx->stage_emb, dtype, N, &od, stream))) return s;
-  const int W = ctx->W;
-  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K, od.K, N * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(ctx, cudaMemcpyAsync(oh->K_prime, od.K_prime, N * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(ctx, cudaMemcpyAsync(oh->instance, od.instance, N * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(ctx, cudaMemcpyAsync(oh->slot, od.slot, N * 4, cudaMemcpyDeviceToHost, st));
-  if (oh->topk_id) CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_id, od.topk_id, N * k * 4, cudaMemcpyDeviceToHost, st));
-  if (oh->topk_score)
-    CUDA_TRY(ctx, cudaMemcpyAsync(oh->topk_score, od.topk_score, N * k * 4, cudaMemcpyDeviceToHost, st));
-  if (oh->flags) CUDA_TRY(ctx, cudaMemcpyAsync(oh->flags, od.flags, N, cudaMemcpyDeviceToHost, st));
-  if (oh->bucket_offsets)
-    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_offsets, od.bucket_offsets, (W + 1) * 4, cudaMemcpyDeviceToHost, st));
-  if (oh->bucket_prompts)
-    CUDA_TRY(ctx, cudaMemcpyAsync(oh->bucket_prompts, od.bucket_prompts, N * 4, cudaMemcpyDeviceToHost, st));
+  if ((s = copy_out(ctx, od, oh, N, st))) return s;
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return PAS_OK;
+}
+
+
+pas_status pas_route_batch_host_async(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
+                                      const pas_route_out* oh, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if ((s = ready(ctx, N))) return s;
+  if (dtype != PAS_F32 && dtype != PAS_BF16) return fail(ctx, PAS_ERR_ARG, "bad dtype");
+  if (N == 0) return PAS_OK;
+  if ((s = validate_out(ctx, oh, false))) return s;
+  if (!emb_host) return fail(ctx, PAS_ERR_ARG, "emb_host is NULL");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk;
+  if (!ctx->h2d_stream) {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->h_join, cudaEventDisableTiming));
+  }
+  pas_ctx::HostSlot& S = ctx->hs[ctx->hseq & 1];
+  if (!S.emb) {
+    cudaError_t e = cudaMalloc(&S.emb, (size_t)mb * ctx->cfg.d * 4);
+    if (!e) e = dmalloc(&S.K, mb);
+    if (!e) e = dmalloc(&S.Kp, mb);
+    if (!e) e = dmalloc(&S.inst, mb);
+    if (!e) e = dmalloc(&S.slot, mb);
+    if (!e) e = dmalloc(&S.tid, mb * k);
+    if (!e) e = dmalloc(&S.tsc, mb * k);
+    if (!e) e = dmalloc(&S.flags, mb);
+    if (!e) e = dmalloc(&S.boff, kMaxInst + 1);
+    if (!e) e = dmalloc(&S.bpr, mb);
+    for (cudaEvent_t* ev : {&S.h2d, &S.done, &S.d2h})
+      if (!e) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    CUDA_TRY(ctx, e);
+  }
+  // at most two batches in flight: this slot's previous batch must have delivered its outputs (its
+  // input buffer was consumed before those copies started)
+  if (S.used) CUDA_TRY(ctx, cudaEventSynchronize(S.d2h));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t esz = dtype == PAS_F32 ? 4 : 2;
+  CUDA_TRY(ctx, cudaMemcpyAsync(S.emb, emb_host, (size_t)N * ctx->cfg.d * esz, cudaMemcpyHostToDevice, ctx->h2d_stream));
+  CUDA_TRY(ctx, cudaEventRecord(S.h2d, ctx->h2d_stream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, S.h2d, 0));
+  pas_route_out od{S.K, S.Kp, S.inst, S.slot,
+                   oh->topk_id ? S.tid : nullptr,
+                   oh->topk_score ? S.tsc : nullptr,
+                   oh->flags ? S.flags : nullptr,
+                   oh->bucket_offsets ? S.boff : nullptr,
+                   oh->bucket_prompts ? S.bpr : nullptr};
+  if ((s = pas_route_batch(ctx, S.emb, dtype, N, &od, stream))) return s;
+  CUDA_TRY(ctx, cudaEventRecord(S.done, st));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, S.done, 0));
+  if ((s = copy_out(ctx, od, oh, N, ctx->d2h_stream))) return s;
+  CUDA_TRY(ctx, cudaEventRecord(S.d2h, ctx->d2h_stream));
+  S.used = true;
+  ctx->hseq++;
+  return PAS_OK;
+}
+
+pas_status pas_route_host_begin(pas_ctx* ctx, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  if (!ctx->h2d_stream) return PAS_OK;   // no pipelined batch yet: the first call creates the streams,
+                                         // whose first copy is enqueued after this point anyway
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  CUDA_TRY(ctx, cudaEventRecord(ctx->h_join, (cudaStream_t)stream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->h2d_stream, ctx->h_join, 0));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->h_join, 0));
+  return PAS_OK;
+}
+
+pas_status pas_route_host_end(pas_ctx* ctx, pas_stream stream) {
+  pas_status s = check_live(ctx);
+  if (s) return s;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  for (auto& S : ctx->hs)
+    if (S.used) CUDA_TRY(ctx, cudaStreamWaitEvent((cudaStream_t)stream, S.d2h, 0));
   return PAS_OK;
 }
 

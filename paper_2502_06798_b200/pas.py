@@ -108,6 +108,9 @@ _SIG = {
                                        C.c_int, C.POINTER(PasAssignment)]),
     "pas_route_batch": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_route_batch_host": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
+    "pas_route_batch_host_async": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
+    "pas_route_host_begin": (C.c_int, [_P, _P]),
+    "pas_route_host_end": (C.c_int, [_P, _P]),
     "pas_route_local": (C.c_int, [_P, _P, C.c_int, C.c_int64, _P, _P]),
     "pas_route_from_candidates": (C.c_int, [_P, _P, C.c_int, C.c_int64, C.POINTER(PasRouteOut), _P]),
     "pas_plan_stats": (C.c_int, [_P, C.POINTER(PasStats)]),
@@ -339,6 +342,22 @@ def pas_route_batch_host(ctx, emb, out: dict, stream=None):
     o = make_out(**out)
     _check(ctx, lib.pas_route_batch_host(ctx, _rows(ctx, emb, device=False), _dtype_code(emb), emb.shape[0],
                                          C.byref(o), _stream(stream)))
+
+
+def pas_route_batch_host_async(ctx, emb, out: dict, stream=None):
+    """Pipelined host-buffer routing (include/pas.h): returns before the batch is done; emb and the
+    out tensors (CPU, pinned) must stay alive and untouched until pas_route_host_end + a stream sync."""
+    o = make_out(**out)
+    _check(ctx, lib.pas_route_batch_host_async(ctx, _rows(ctx, emb, device=False), _dtype_code(emb), emb.shape[0],
+                                               C.byref(o), _stream(stream)))
+
+
+def pas_route_host_begin(ctx, stream=None):
+    _check(ctx, lib.pas_route_host_begin(ctx, _stream(stream)))
+
+
+def pas_route_host_end(ctx, stream=None):
+    _check(ctx, lib.pas_route_host_end(ctx, _stream(stream)))
 
 
 def pas_route_local(ctx, emb, cand, stream=None):

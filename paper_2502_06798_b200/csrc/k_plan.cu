@@ -40,7 +40,9 @@ namespace {
 __global__ void __launch_bounds__(32) k_plan(const int* __restrict__ hist, const RouteParams P,
                                              DevPlan* __restrict__ plan) {
   pdl_entry();
-  plan_body(hist, P, plan);   // inlined: the parameters are read with direct (indexed) constant loads
+  // inlined: the parameters are read with direct (indexed) constant loads; K6's windows only for the
+  // batches that take the windowed path
+  plan_body(hist, P, plan, P.N >= kWindowMinN);
 }
 
 }  // namespace

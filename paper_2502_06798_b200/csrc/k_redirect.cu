@@ -50,7 +50,6 @@ constexpr int RT = 256;
 constexpr int kSmemList = 2048;   // k6_resolve: entries staged in shared memory (else read from L2)
 // The windowed split search serves N >= kWindowMinN; below, its fixed launch cost (fused pass, zone
 // kernels, gated fallback launches) exceeds what it saves, and the exact histogram path runs alone.
-constexpr int64_t kWindowMinN = 1 << 18;
 
 __device__ __forceinline__ bool entry_less(uint64_t ka, int32_t pa, uint64_t kb, int32_t pb) {
   return ka < kb || (ka == kb && pa < pb);

@@ -153,6 +153,9 @@ struct RouteParams {
 // plan has <= 2 nK - 1 nonzeros); more, a list overflow or a split outside its zone sets k6_fallback
 // and the exact histogram path runs instead.
 constexpr int kMaxZones = 32;
+// K6's windowed split search serves batches of at least this many prompts (k_redirect.cu); below, the
+// exact histogram path runs alone and K5 skips the windows.
+constexpr int64_t kWindowMinN = 1 << 18;
 
 // Device-side plan + counters of one batch (K5 writes, pas_plan_stats reads).
 struct DevPlan {

@@ -394,6 +394,7 @@ __device__ __forceinline__ void plan_body(const int* hist, const RouteParams& P,
   }
   __syncwarp();
   if (lane == 0 && k6_windows) k6_zones(h_s, x_s, P, plan);
+  if (lane == 0 && !k6_windows && P.k6_force_fallback) plan->k6_fallback = 1;   // (reported as forced)
 }
 
 }  // namespace

@@ -1478,6 +1478,17 @@ pas_status pas_route_batch_host(pas_ctx* ctx, const void* emb_host, pas_dtype dt
 }
 
 
+namespace {
+// The pipelined host API's copy streams and fence event (created on first use).
+pas_status ensure_host_streams(pas_ctx* ctx) {
+  if (ctx->h2d_stream) return PAS_OK;
+  CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+  CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+  CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->h_join, cudaEventDisableTiming));
+  return PAS_OK;
+}
+}  // namespace
+
 pas_status pas_route_batch_host_async(pas_ctx* ctx, const void* emb_host, pas_dtype dtype, int64_t N,
                                       const pas_route_out* oh, pas_stream stream) {
   pas_status s = check_live(ctx);
@@ -1489,11 +1500,7 @@ pas_status pas_route_batch_host_async(pas_ctx* ctx, const void* emb_host, pas_dt
   if (!emb_host) return fail(ctx, PAS_ERR_ARG, "emb_host is NULL");
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
   const int64_t mb = ctx->cfg.max_batch, k = ctx->cfg.topk;
-  if (!ctx->h2d_stream) {
-    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
-    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->h_join, cudaEventDisableTiming));
-  }
+  if ((s = ensure_host_streams(ctx))) return s;
   pas_ctx::HostSlot& S = ctx->hs[ctx->hseq & 1];
   if (!S.emb) {
     cudaError_t e = cudaMalloc(&S.emb, (size_t)mb * ctx->cfg.d * 4);
@@ -1537,9 +1544,8 @@ pas_status pas_route_batch_host_async(pas_ctx* ctx, const void* emb_host, pas_dt
 pas_status pas_route_host_begin(pas_ctx* ctx, pas_stream stream) {
   pas_status s = check_live(ctx);
   if (s) return s;
-  if (!ctx->h2d_stream) return PAS_OK;   // no pipelined batch yet: the first call creates the streams,
-                                         // whose first copy is enqueued after this point anyway
   CUDA_TRY(ctx, cudaSetDevice(ctx->cfg.device));
+  if ((s = ensure_host_streams(ctx))) return s;
   CUDA_TRY(ctx, cudaEventRecord(ctx->h_join, (cudaStream_t)stream));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->h2d_stream, ctx->h_join, 0));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, ctx->h_join, 0));

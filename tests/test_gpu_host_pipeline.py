@@ -59,3 +59,22 @@ def test_pipelined_host_routing_equals_sync(pas, name, N, M, sizes):
             assert np.array_equal(a, c), f"batch {b} ({sizes[b]} prompts): {k} differs"
     sync_r.close()
     pipe_r.close()
+
+
+def test_pipelined_host_routing_errors(pas):
+    """The pipelined call validates like the synchronous one (no batch enqueued on an error)."""
+    cfg = CONFIGS["C1"]
+    w = Workload(cfg, device=DEV, M=1000)
+    r = _router(pas, cfg, 64, 1000, w)
+    big = torch.zeros(65, cfg.d).pin_memory()
+    o = {k: v.pin_memory() for k, v in r.alloc_out(65, device="cpu").items()}
+    with pytest.raises(pas.PasError):
+        pas.pas_route_batch_host_async(r.ctx, big, o)          # N > max_batch
+    x = w.prompts(64).cpu().pin_memory()
+    o = {k: v.pin_memory() for k, v in r.alloc_out(64, device="cpu").items()}
+    pas.pas_route_host_begin(r.ctx)
+    pas.pas_route_batch_host_async(r.ctx, x, o)                # the context still routes
+    pas.pas_route_host_end(r.ctx)
+    torch.cuda.synchronize()
+    assert o["K"].numpy().min() >= 0
+    r.close()

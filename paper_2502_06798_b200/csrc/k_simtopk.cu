@@ -45,7 +45,8 @@
 #include "pas_internal.cuh"
 #include "ptx_sm100.cuh"
 
-// Shape-dispatched tile: the CTA pair (cta_group::2) for N <= PAS_K2_PAIR_MAX_TILES x 128 prompts,
+// Shape-dispatched tile: the CTA pair (cta_group::2) for N <= PAS_K2_PAIR_MAX_TILES x 128 prompts in an
+// even number of 128-row tiles,
 // the single-CTA tile above that (A/B in DESIGN.md 8: the pair is faster where K2 is latency- and
 // L2-bound, the single CTA where it is power-bound).  0 disables the pair; a huge value forces it.
 #ifndef PAS_K2_PAIR_MAX_TILES
@@ -604,7 +605,11 @@ bool simtopk_pair(int64_t N, int d) {
     return v ? atoi(v) : PAS_K2_PAIR_MAX_TILES;
   }();
   (void)d;
-  return (N + BM - 1) / BM <= max_tiles;
+  // the pair covers 256 prompt rows per unit: with an odd number of 128-row tiles one CTA of a pair
+  // computes only padding (C5, 50M rows: N = 128 8.0k vs 10.8k prompts/s single-CTA, N = 384 11.1k vs
+  // 14.1k; N = 256 14.3k vs 12.9k), so the pair serves only whole pairs of tiles
+  const int64_t tiles = (N + BM - 1) / BM;
+  return tiles <= max_tiles && tiles % 2 == 0;
 }
 int simtopk_prompt_rows() { return Tile<true>::UNIT_ROWS; }   // prompt buffers are padded to whole pair tiles
 int simtopk_box_q() { return BM; }

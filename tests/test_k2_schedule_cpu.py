@@ -25,7 +25,7 @@ def test_schedule_invariants(pas, N, M):
     MT, NT, R, T, CS = s["MT"], s["NT"], s["R"], s["T"], s["CS"]
     assert MT == math.ceil(N / 128) and NT == math.ceil(M / 256)
     assert 1 <= R <= min(128, max(NT, 1)) and R * N <= s["cand_cap"]      # S-way merge, candidate buffer
-    assert s["pair"] == (MT <= 4)                                          # CTA pair only for N <= 512
+    assert s["pair"] == (MT <= 4 and MT % 2 == 0)                          # CTA pair: whole tile pairs, N <= 512
     if T:
         L = math.ceil(NT / R)                                              # tiles of the longest range
         assert not s["pair"] and 4 <= T <= 128
@@ -48,7 +48,8 @@ def test_bench_configs(pas):
     c2 = pas.pas_debug_k2_schedule(4096, 100_000)                          # C2: 40-tile ranges, 6 chunks
     assert (c2["R"], c2["T"], c2["CS"]) == (10, 7, 6)
     c1 = pas.pas_debug_k2_schedule(64, 1000)
-    assert c1["pair"] == 1 and c1["T"] == 0
+    assert c1["pair"] == 0 and c1["T"] == 0                                # one 128-row tile: a single CTA
+    assert pas.pas_debug_k2_schedule(256, 50_000_000)["pair"] == 1         # C5 at N = 256: the pair
 
 
 def test_static_override(pas, monkeypatch):

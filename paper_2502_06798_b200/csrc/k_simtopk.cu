@@ -8,9 +8,9 @@
 //
 // Two tile organisations share one source (template parameter), dispatched by batch size
 // (simtopk_pair; DESIGN.md section 8 records the A/B on one B200):
-//   single CTA (N > 512)  tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
+//   single CTA (else)     tcgen05.mma.cta_group::1, 128 prompt rows x 256 cache rows x K=16 per
 //                         instruction; per stage A 128x64 + B 256x64 bf16 (48 KB), 4 stages.
-//   CTA pair (N <= 512)   tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
+//   CTA pair (N = 129..256, 385..512)   tcgen05.mma.cta_group::2, 256 x 256 x 16: prompt rows 0..127 in CTA 0,
 //                         128..255 in CTA 1; the 256 cache rows of B split 128/128 between the two
 //                         CTAs' smem (32 KB / stage, 6 stages); TMA bytes of both CTAs land on the
 //                         leader's mbarrier; commits multicast to both CTAs.

@@ -1,5 +1,5 @@
 # Last-commit check: smoke, the whole -m gpu suite, the C4 / C2 / C1 bench lines (gpurun_out/check/)
-O=gpurun_out/check
+O=${O:-gpurun_out/check}
 mkdir -p $O
 python -m paper_2502_06798_b200.build > /dev/null
 timeout 300 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log

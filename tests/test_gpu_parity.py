@@ -539,6 +539,15 @@ def test_many_ranges_warp_merge(pas):
     assert st["stage_ms"][1] > 0
 
 
+@pytest.mark.parametrize("N,M", [(128, 2_000_000), (384, 1_000_003)])
+def test_odd_tile_batches_many_ranges(pas, N, M):
+    """An odd number of 128-row prompt tiles takes the single-CTA tile (not the CTA pair); against a
+    large cache K2 then cuts it into up to 128 ranges, so the merge takes S ~ 128 sources (the latency
+    path's thread-per-prompt merge at N <= 1,024): full oracle parity."""
+    rep, st = _full_parity(pas, CONFIGS["C2"], N=N, M=M)
+    assert st["k2_ranges"] >= 64, st["k2_ranges"]
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 def test_many_instances(pas, mode):
     """W = 40 serving instances (several per level; in uniform mode > 32 classes for K7)."""

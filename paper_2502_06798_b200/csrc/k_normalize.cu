@@ -47,7 +47,9 @@ __device__ __forceinline__ float div_rn(float v, double norm, double inv) {
   return __double2float_rn(q);
 }
 
-__device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[4], double norm, bool valid) {
+// dup != nullptr: the same four values are also stored there (K2's duplicated-row small batches)
+__device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[4], double norm, bool valid,
+                                           __nv_bfloat16* dup = nullptr) {
   __nv_bfloat162 lo, hi;
   if (valid) {
     const double inv = 1.0 / norm;
@@ -61,6 +63,7 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
   pk.x = *reinterpret_cast<uint32_t*>(&lo);
   pk.y = *reinterpret_cast<uint32_t*>(&hi);
   *reinterpret_cast<uint2*>(dst) = pk;
+  if (dup) *reinterpret_cast<uint2*>(dup) = pk;
 }
 
 // One warp per row.  VEC = d / 128 float4 (or 4 x bf16) per lane: all of a row's loads are in flight
@@ -84,7 +87,7 @@ template <typename T, int VEC>
 __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count,
-                                                   uint32_t* epoch_bump) {
+                                                   uint32_t* epoch_bump, int64_t dup_rows) {
   pdl_entry();
   if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) {   // the epoch of the K2 launch that follows
     const uint32_t e = *epoch_bump + 1;
@@ -136,11 +139,13 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       for (int c = 0; c < VEC; ++c) {
         float w[4];
         load4(src + c * 128 + lane * 4, w);
-        store_row4(dst + c * 128 + lane * 4, w, norm, valid);
+        store_row4(dst + c * 128 + lane * 4, w, norm, valid, dup_rows ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
       }
 #else
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) store_row4(dst + c * 128 + lane * 4, v[c], norm, valid);
+      for (int c = 0; c < VEC; ++c) {
+        store_row4(dst + c * 128 + lane * 4, v[c], norm, valid, dup_rows ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
+      }
 #endif
       if (lane == 0) {
         if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       for (int c = lane * 4; c < d; c += 128) {
         float v[4];
         load4(src + c, v);
-        store_row4(dst + c, v, norm, valid);
+        store_row4(dst + c, v, norm, valid, dup_rows ? dst + dup_rows * d + c : nullptr);
       }
       if (lane == 0) {
         if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
 
 template <typename T>
 cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8_t* flags, int64_t first_gid, int G,
-                     int rank, int* invalid_count, cudaStream_t st, uint32_t* eb) {
+                     int rank, int* invalid_count, cudaStream_t st, uint32_t* eb, int64_t dup) {
   const int threads = 256;
   const int vec = d % 128 == 0 && d <= 1024 ? d / 128 : 0;
   // one warp per row, one CTA per 8 rows (PAS_K1_GRIDCAP 1: capped at the resident CTAs, grid-stride)
@@ -189,15 +194,15 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
   if (PAS_K1_GRIDCAP && blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
   switch (vec) {
-    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb); break;
-    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb);
+    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
+    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup);
   }
   return cudaGetLastError();
 }
@@ -206,13 +211,13 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
 
 cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
-                             cudaStream_t st, uint32_t* epoch_bump) {
+                             cudaStream_t st, uint32_t* epoch_bump, int64_t dup_rows) {
   if (rows <= 0) return cudaSuccess;
   if (dtype == PAS_F32)
     return launch_t(static_cast<const float*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st,
-                    epoch_bump);
+                    epoch_bump, dup_rows);
   return launch_t(static_cast<const __nv_bfloat16*>(in), rows, d, out, flags, first_gid, G, rank, invalid_count, st,
-                  epoch_bump);
+                  epoch_bump, dup_rows);
 }
 
 }  // namespace pas

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch_arg,
-              const uint32_t* __restrict__ epoch_dev, uint32_t slack, const DynSched dyn) {
+              const uint32_t* __restrict__ epoch_dev, uint32_t slack, const DynSched dyn, int dup_arg) {
   static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
   using TL = Tile<PAIR>;
   constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
@@ -445,7 +445,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t q = warp & 3;              // TMEM lane quarter this warp may access
     const int half = (int)(warp - 2) >> 2;    // 0: columns 0..127 of each tile, 1: 128..255
     const int row = (int)(q * 32 + lane);
-    const uint32_t lane_addr = tmem_base + ((q * 32u) << 16) + half * (BN / 2);
+    // Small batches (dup, N <= 64): K1 wrote every prompt row again 64 rows down, so the MMA computes
+    // each prompt's scores in lane quarters q and q + 2 -- which belong to different SM
+    // sub-partitions.  The four (quarter pair, half) combinations then take a quarter of the columns
+    // each: the epilogue runs on all four schedulers instead of the two the real rows would occupy.
+    const bool dup = !PAIR && !DYN && !DUMP && dup_arg;
+    const int cpart = dup ? (int)(q >> 1) * 2 + half : half;   // column part of the tile this warp ranks
+    const int PCOLS = dup ? BN / 4 : BN / 2;
+    const int prow = dup ? (row & 63) : row;                   // the prompt row this lane ranks
+    const uint32_t lane_addr = tmem_base + ((q * 32u) << 16) + cpart * PCOLS;
     const int Ml = (int)M_local;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         t0 = (int)((int64_t)r * NT / R);
         t1 = (int)((int64_t)(r + 1) * NT / R);
       }
-      const int64_t prompt = (int64_t)m * UNIT_ROWS + (PAIR ? crank * BM : 0) + row;
+      const int64_t prompt = (int64_t)m * UNIT_ROWS + (PAIR ? crank * BM : 0) + prow;
       // a warp whose 32 rows are all past the batch (the padding of the last prompt tile) has no lists
       // to keep: it skips the epilogue work (those Q_hat rows are whatever the buffer holds, and a
       // list fed garbage scores inserts on most chunks -- C1: 5.5 us of K2's 18.5)
@@ -495,7 +503,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t0; t < t1; ++t) {
         ptx::mbar_wait(&bars->tfull[acc], acc_phase);
         ptx::tc_fence_after();
-        const int col_base = t * BN + half * (BN / 2);
+        const int col_base = t * BN + cpart * PCOLS;
         const uint32_t taddr = lane_addr + acc * BN;
         if (!warp_live) {
           // nothing to rank (the accumulator is released below like any other)
@@ -511,6 +519,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 32; ++j)
                 if (col0 + j < M_local) dump[prompt * M_local + col0 + j] = __uint_as_float(v[j]);
           }
+        } else if (dup) {
+          if (col_base + BN / 4 > Ml) epi_tile<KMAX, true, BN / 128>(taddr, col_base, Ml, s, gl);
+          else epi_tile<KMAX, false, BN / 128>(taddr, col_base, Ml, s, gl);
         } else if (col_base + BN / 2 > Ml) {
           epi_tile<KMAX, true>(taddr, col_base, Ml, s, gl);
         } else {
@@ -548,8 +559,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         epi_barrier();
-        if (half == 0) {
-          merge_lists<KMAX>(s, gl, list_s + row * KMAX, list_g + row * KMAX);
+        if (half == 0) merge_lists<KMAX>(s, gl, list_s + row * KMAX, list_g + row * KMAX);
+        if (dup) {   // second round: rows 64..127 (the copies) hand their merged lists to rows 0..63
+          if (half == 0 && row >= 64) {
+#pragma unroll
+            for (int i = 0; i < KMAX; ++i) {
+              list_s[row * KMAX + i] = s[i];
+              list_g[row * KMAX + i] = gl[i];
+            }
+          }
+          epi_barrier();
+          if (half == 0 && row < 64) merge_lists<KMAX>(s, gl, list_s + (row + 64) * KMAX, list_g + (row + 64) * KMAX);
+        }
+        if (half == 0 && (!dup || row < 64)) {
           if (prompt < N) {
             Cand* dst = out + ((int64_t)r * N + prompt) * k;
 #pragma unroll
@@ -594,7 +616,8 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   // the CTA pair and the B multicast read the cache through the 128-row box map
   return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN>, *a.tmap_q,
                             PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
-                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, a.epoch_dev, slack, a.dyn);
+                            a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, a.epoch_dev, slack, a.dyn,
+                            a.dup ? 1 : 0);
 }
 
 }  // namespace
@@ -610,6 +633,10 @@ bool simtopk_pair(int64_t N, int d) {
   // 14.1k; N = 256 14.3k vs 12.9k), so the pair serves only whole pairs of tiles
   const int64_t tiles = (N + BM - 1) / BM;
   return tiles <= max_tiles && tiles % 2 == 0;
+}
+int64_t simtopk_dup_rows(int64_t N, int d) {
+  static const bool off = getenv("PAS_K2_NO_DUP") != nullptr;   // A/B experiments
+  return !off && N <= 64 && !simtopk_pair(N, d) ? 64 : 0;
 }
 int simtopk_prompt_rows() { return Tile<true>::UNIT_ROWS; }   // prompt buffers are padded to whole pair tiles
 int simtopk_box_q() { return BM; }

@@ -395,8 +395,9 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
                      int* S, Cand* merged) {
   const int k = ctx->cfg.topk;
   if (pas_status s = ensure_prompt_ws(ctx)) return s;
+  const int64_t dup = simtopk_dup_rows(N, (int)ctx->cfg.d);
   CUDA_TRY(ctx, launch_normalize(emb, dt, N, ctx->cfg.d, ctx->qhat, ctx->pflags, 0, 1, 0, nullptr, st,
-                                 &ctx->bc->k2_epoch));
+                                 &ctx->bc->k2_epoch, dup));
   ctx->launches++;
   CUDA_TRY(ctx, rec_stage(ctx, 1, st));
   int R = 1;
@@ -413,6 +414,7 @@ pas_status run_local(pas_ctx* ctx, const void* emb, pas_dtype dt, int64_t N, cud
     SimTopkArgs a{&ctx->tm_q, &ctx->tm_c, &ctx->tm_c2, N, ctx->M_local, ctx->cfg.d, k, ctx->cfg.world, ctx->cfg.rank, R,
                   ctx->qhat, ctx->cand_local, nullptr, ctx->k2_tune.no_leash ? nullptr : ctx->k2_progress,
                   0, &ctx->bc->k2_epoch, dyn};
+    a.dup = dup > 0;
     CUDA_TRY(ctx, launch_simtopk(a, st));
     ctx->k2_last_R = R;
     ctx->k2_last_T = dyn.T;

@@ -194,7 +194,9 @@ constexpr int kDegShift = 24;        // R37: non-convex c held as integers on a 
 // K1: normalise + quantise rows; shard filter (first_gid + i) % G == rank -> local row (first_gid+i)/G
 cudaError_t launch_normalize(const void* in, pas_dtype dtype, int64_t rows, int d, __nv_bfloat16* out,
                              uint8_t* flags, int64_t first_gid, int G, int rank, int* invalid_count,
-                             cudaStream_t st, uint32_t* epoch_bump = nullptr);
+                             cudaStream_t st, uint32_t* epoch_bump = nullptr, int64_t dup_rows = 0);
+// dup_rows > 0: each row is also written dup_rows rows further down (K2's duplicated-row small-batch
+// epilogue, SimTopkArgs::dup)
 
 __device__ __forceinline__ uint64_t batch_seq_of(const RouteParams& P) {
   return P.bc ? P.bc->batch_seq : P.batch_seq;
@@ -253,7 +255,13 @@ struct SimTopkArgs {
   uint32_t epoch;                 // this launch's epoch (never 0: zeroed words read as "not started")
   const uint32_t* epoch_dev;      // or, if set, read from here after the PDL wait (bumped by K1)
   DynSched dyn;                   // T > 0: the dynamic schedule (simtopk_plan_dynamic)
+  int dup = 0;                    // 1: N <= 64 on the single-CTA static tile and K1 wrote every prompt
+                                  // row again at row + 64, so the epilogue splits each row's columns
+                                  // over all four TMEM lane quarters (simtopk_dup_rows)
 };
+// Batches of at most this many prompts take K2's duplicated-row epilogue (K1 writes row p also at
+// p + 64); 0 for other shapes.
+int64_t simtopk_dup_rows(int64_t N, int d);
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 // The dynamic schedule's ranges R and chunk T for this batch, or false when the static schedule

@@ -45,6 +45,27 @@ __device__ __forceinline__ Head warp_best(Head h) {
 // are used for the heads).  Returns nothing; writes out[0..k) via lane 0.
 __device__ __forceinline__ void merge_prompt(const Cand* __restrict__ in, int S, int64_t N, int k, int64_t p,
                                              Cand* res /*[k] in shared or global*/, int lane) {
+  if (S <= 32 && k <= 8) {
+    // one source per lane, its whole list loaded up front (eight independent loads instead of one
+    // dependent load per round), then k rounds of the warp tournament; the winner's lane shifts
+    Cand L[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      L[i] = (lane < S && i < k) ? in[((int64_t)lane * N + p) * k + i] : Cand{-INFINITY, -1};
+    for (int i = 0; i < k; ++i) {
+      Head h;
+      h.src = lane < S ? lane : -1;
+      h.c = L[0];
+      const Head b = warp_best(h);
+      if (b.src == lane) {
+#pragma unroll
+        for (int j = 0; j < 7; ++j) L[j] = L[j + 1];
+        L[7] = Cand{-INFINITY, -1};
+      }
+      if (lane == 0) res[i] = (b.src >= 0) ? b.c : Cand{-INFINITY, -1};
+    }
+    return;
+  }
   // per-lane cursor over its sources: sources lane, lane+32, ...; keep pos per source in a small array
   constexpr int MAXSRC_PER_LANE = 4;   // S <= 128
   int pos[MAXSRC_PER_LANE];

@@ -15,14 +15,15 @@ def main(reps=int(os.environ.get("REPS", "400"))):
     from paper_2502_06798_b200 import pas
     from synth import CONFIGS, Workload
     cfg = CONFIGS["C1"]
+    N = int(os.environ.get("C1_N", cfg.N))   # batch size override (tiny low-load batches)
     dev = torch.device("cuda", 0)
     w = Workload(cfg, device=dev)
-    r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=cfg.N, max_rows_per_rank=cfg.M, device=0, seed=cfg.route_seed)
+    r = pas.Router(d=cfg.d, topk=cfg.topk, max_batch=N, max_rows_per_rank=cfg.M, device=0, seed=cfg.route_seed)
     r.set_bands(cfg.grid, cfg.thresholds)
     r.set_fractions(cfg.F, cfg.instance_level, cfg.bstar, cfg.mode)
     r.load_cache(w.cache_rows(0, cfg.M).contiguous())
-    emb = w.prompts(cfg.N).contiguous()
-    out = r.alloc_out(cfg.N)
+    emb = w.prompts(N).contiguous()
+    out = r.alloc_out(N)
     res = {}
     for graph in (False, True):
         pas.pas_set_graph(r.ctx, graph)

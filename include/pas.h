@@ -416,10 +416,11 @@ pas_status pas_debug_qhat(pas_ctx* ctx, void* out_dev, int64_t N, pas_stream str
 pas_status pas_debug_store_rows(pas_ctx* ctx, int64_t first_local_row, int64_t n, void* out_dev, pas_stream stream);
 
 /* The K2 work schedule a batch of N prompts against M_local rows of width d would get in a context of
- * max_batch prompts (host logic only, no device; DESIGN.md 8 "K2 schedule").  out[8] receives:
+ * max_batch prompts (host logic only, no device; DESIGN.md 8 "K2 schedule").  out[9] receives:
  * R (cache ranges per prompt tile = sources of the merge), T (cache tiles per chunk; 0 = static
  * schedule), CS (chunk steps per range), MTg (prompt tiles per group), pair (1 = CTA-pair tile),
- * MT (prompt tiles of 128), NT (cache tiles of 256), cand_cap (candidate rows: R * N <= cand_cap).
+ * MT (prompt tiles of 128), NT (cache tiles), cand_cap (candidate rows: R * N <= cand_cap), and the
+ * cache tile's rows (256, or 128 for the small-problem tile).
  * The PAS_K2_* experiment variables are read at each call here; a context reads them
  * once, at pas_create.  Errors: PAS_ERR_ARG. */
 pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_batch, int* out);

@@ -66,11 +66,12 @@ constexpr int TMEM_COLS = 512;
 constexpr int LIST_BYTES = BM * 16 * 8;             // hand-over of the upper half's lists (KMAX <= 16)
 constexpr int WARMUP_TILES = 24;
 
-template <bool P>
+// BNT: cache rows per tile (MMA N): 256, or 128 for the small-problem tile (simtopk_small)
+template <bool P, int BNT = BN>
 struct Tile {
   static constexpr int CTAS = P ? 2 : 1;
-  static constexpr int BN_CTA = BN / CTAS;           // cache rows staged per CTA
-  static constexpr int STAGES = P ? 6 : 4;
+  static constexpr int BN_CTA = BNT / CTAS;          // cache rows staged per CTA
+  static constexpr int STAGES = (P || BNT < BN) ? 6 : 4;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // per CTA
@@ -250,14 +251,15 @@ __device__ __forceinline__ void epi_barrier() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
 }
 
-template <int KMAX, bool DUMP, bool PAIR, bool DYN>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN, int BNT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_simtopk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmC, int64_t N,
               int64_t M_local, int kblocks, int k, int G, int rank, int R, int MT, int NT, Cand* __restrict__ out,
               float* __restrict__ dump, uint64_t* __restrict__ progress, uint32_t epoch_arg,
               const uint32_t* __restrict__ epoch_dev, uint32_t slack, const DynSched dyn, int dup_arg) {
   static_assert(!DYN || (!PAIR && !DUMP), "the dynamic schedule serves the single-CTA top-k tile");
-  using TL = Tile<PAIR>;
+  static_assert(BNT == BN || (!PAIR && !DYN && !DUMP), "the small tile serves the static single-CTA path");
+  using TL = Tile<PAIR, BNT>;
   constexpr int CTAS = TL::CTAS, BN_CTA = TL::BN_CTA, STAGES = TL::STAGES, A_BYTES = TL::A_BYTES,
                 B_BYTES = TL::B_BYTES, STAGE_BYTES = TL::STAGE_BYTES, UNIT_ROWS = TL::UNIT_ROWS;
   extern __shared__ uint8_t smem_raw[];
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
               ptx::mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
               ptx::tma_load_2d(&tmQ, sA + stage * A_BYTES, &bars->full[stage], kb * BK, qrow, ptx::kEvictLast);
-              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BN,
+              ptx::tma_load_2d(&tmC, sB + stage * B_BYTES, &bars->full[stage], kb * BK, t * BNT,
                                ptx::kEvictNormal);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (leader) leash_wait(progress, worker, nworkers, epoch, issued, slack);
             __syncwarp();
           }
-          const int crow = t * BN + (int)crank * BN_CTA;
+          const int crow = t * BNT + (int)crank * BN_CTA;
           if (lane == 0)
           for (int kb = 0; kb < kblocks; ++kb) {
             ptx::mbar_wait(&bars->empty[stage], phase ^ 1);
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------- MMA issuer ---------------------------------
     // (CTA pair: the leader issues for both CTAs; the single-CTA tile its own)
     if ((!PAIR || leader) && ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(UNIT_ROWS, BN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(UNIT_ROWS, BNT);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int t = t0; t < t1; ++t) {
           ptx::mbar_wait(&bars->tempty[acc], acc_phase ^ 1);
           ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + acc * BN;
+          const uint32_t d_tmem = tmem_base + acc * BNT;
           for (int kb = 0; kb < kblocks; ++kb) {
             ptx::mbar_wait(&bars->full[stage], phase);
             ptx::tc_fence_after();
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // each: the epilogue runs on all four schedulers instead of the two the real rows would occupy.
     const bool dup = !PAIR && !DYN && !DUMP && dup_arg;
     const int cpart = dup ? (int)(q >> 1) * 2 + half : half;   // column part of the tile this warp ranks
-    const int PCOLS = dup ? BN / 4 : BN / 2;
+    const int PCOLS = dup ? BNT / 4 : BNT / 2;
     const int prow = dup ? (row & 63) : row;                   // the prompt row this lane ranks
     const uint32_t lane_addr = tmem_base + ((q * 32u) << 16) + cpart * PCOLS;
     const int Ml = (int)M_local;
@@ -503,13 +505,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = t0; t < t1; ++t) {
         ptx::mbar_wait(&bars->tfull[acc], acc_phase);
         ptx::tc_fence_after();
-        const int col_base = t * BN + cpart * PCOLS;
-        const uint32_t taddr = lane_addr + acc * BN;
+        const int col_base = t * BNT + cpart * PCOLS;
+        const uint32_t taddr = lane_addr + acc * BNT;
         if (!warp_live) {
           // nothing to rank (the accumulator is released below like any other)
         } else if (DUMP) {
 #pragma unroll 1
-          for (int c = 0; c < BN / 64; ++c) {
+          for (int c = 0; c < BNT / 64; ++c) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(taddr + c * 32, v);
             ptx::tmem_wait_ld();
@@ -520,12 +522,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (col0 + j < M_local) dump[prompt * M_local + col0 + j] = __uint_as_float(v[j]);
           }
         } else if (dup) {
-          if (col_base + BN / 4 > Ml) epi_tile<KMAX, true, BN / 128>(taddr, col_base, Ml, s, gl);
-          else epi_tile<KMAX, false, BN / 128>(taddr, col_base, Ml, s, gl);
-        } else if (col_base + BN / 2 > Ml) {
-          epi_tile<KMAX, true>(taddr, col_base, Ml, s, gl);
+          if (col_base + BNT / 4 > Ml) epi_tile<KMAX, true, BNT / 128>(taddr, col_base, Ml, s, gl);
+          else epi_tile<KMAX, false, BNT / 128>(taddr, col_base, Ml, s, gl);
+        } else if (col_base + BNT / 2 > Ml) {
+          epi_tile<KMAX, true, BNT / 64>(taddr, col_base, Ml, s, gl);
         } else {
-          epi_tile<KMAX, false>(taddr, col_base, Ml, s, gl);
+          epi_tile<KMAX, false, BNT / 64>(taddr, col_base, Ml, s, gl);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -595,9 +597,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int KMAX, bool DUMP, bool PAIR, bool DYN = false>
+template <int KMAX, bool DUMP, bool PAIR, bool DYN = false, int BNT = BN>
 cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint32_t slack, cudaStream_t st) {
-  using TL = Tile<PAIR>;
+  using TL = Tile<PAIR, BNT>;
+  static_assert(TL::NUM_WORKERS > 0 && TL::SMEM_BYTES <= 232448, "tile configuration");
   constexpr int CTAS = PAIR ? 2 : 1;   // cluster size
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -614,8 +617,8 @@ cudaError_t launch_variant(const SimTopkArgs& a, int MT, int NT, int grid, uint3
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 2 : 1;
   // the CTA pair and the B multicast read the cache through the 128-row box map
-  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN>, *a.tmap_q,
-                            PAIR ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
+  return cudaLaunchKernelEx(&cfg, k_simtopk<KMAX, DUMP, PAIR, DYN, BNT>, *a.tmap_q,
+                            (PAIR || BNT < BN) ? *a.tmap_c_pair : *a.tmap_c, a.N, a.M_local, a.d / BK, a.k, a.G,
                             a.rank, a.R, MT, NT, a.out, a.dump, a.progress, a.epoch, a.epoch_dev, slack, a.dyn,
                             a.dup ? 1 : 0);
 }
@@ -634,6 +637,16 @@ bool simtopk_pair(int64_t N, int d) {
   const int64_t tiles = (N + BM - 1) / BM;
   return tiles <= max_tiles && tiles % 2 == 0;
 }
+// Small problems (one prompt tile, at most 128 cache tiles of 128 rows): the 128-row cache tile, one per
+// CTA -- twice the CTAs of the 256-row tile, each pulling half the bytes through its TMA and running half
+// the MMA and epilogue (C1: 8 CTAs instead of 4).  Large caches keep 256-row tiles (the prompt tile is
+// re-read from L2 once per cache tile).
+bool simtopk_small(int64_t N, int64_t M_local, int d) {
+  static const bool off = getenv("PAS_K2_NO_SMALL") != nullptr;   // A/B experiments
+  return !off && N > 0 && N <= BM && !simtopk_pair(N, d) && M_local > 0 && (M_local + 127) / 128 <= 128;
+}
+int simtopk_tile_rows(int64_t N, int64_t M_local, int d) { return simtopk_small(N, M_local, d) ? 128 : BN; }
+
 int64_t simtopk_dup_rows(int64_t N, int d) {
   static const bool off = getenv("PAS_K2_NO_DUP") != nullptr;   // A/B experiments
   return !off && N <= 64 && !simtopk_pair(N, d) ? 64 : 0;
@@ -647,14 +660,16 @@ static int tile_rows(int d) { return (void)d, BN; }
 // Opt the kernel variants into > 48 KB dynamic shared memory on the current device.
 cudaError_t simtopk_init() {
   cudaError_t e;
-  const int ss = Tile<false>::SMEM_BYTES, pr = Tile<true>::SMEM_BYTES;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
-  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
-  return cudaFuncSetAttribute(k_simtopk<16, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
+  const int ss = Tile<false>::SMEM_BYTES, pr = Tile<true>::SMEM_BYTES, sm = Tile<false, 128>::SMEM_BYTES;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, false, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<16, false, false, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, true, false, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, ss))) return e;
+  if ((e = cudaFuncSetAttribute(k_simtopk<8, false, true, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr))) return e;
+  return cudaFuncSetAttribute(k_simtopk<16, false, true, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pr);
 }
 
 // Dynamic schedule.  Static units (prompt tile, whole range) let the 148 CTAs drift apart over a range
@@ -749,6 +764,11 @@ bool simtopk_plan_dynamic(int64_t N, int64_t M_local, int64_t cand_rows, int64_t
 // nearly every 32-column chunk of some lane takes the insert path (P(insert) ~ 32 k / columns seen),
 // which makes the first ~8k columns of a unit epilogue-bound rather than MMA-bound.
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d) {
+  if (simtopk_small(N, M_local, d)) {   // one 128-row tile per CTA (as many as the candidate buffer holds)
+    int64_t R = (M_local + 127) / 128;
+    while (R > 1 && R * N > cand_rows) --R;
+    return (int)R;
+  }
   const bool pair = simtopk_pair(N, d);
   const int UNIT_ROWS = pair ? Tile<true>::UNIT_ROWS : Tile<false>::UNIT_ROWS;
   const int NUM_WORKERS = pair ? Tile<true>::NUM_WORKERS : Tile<false>::NUM_WORKERS;
@@ -796,7 +816,9 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   const int NUM_WORKERS = pair ? Tile<true>::NUM_WORKERS : Tile<false>::NUM_WORKERS;
   const int CTAS = pair ? 2 : 1;
   const int MT = (int)((a.N + UNIT_ROWS - 1) / UNIT_ROWS);
-  const int NT = (int)((a.M_local + tile_rows(a.d) - 1) / tile_rows(a.d));
+  const bool small = !a.dump && a.dyn.T == 0 && simtopk_small(a.N, a.M_local, a.d);
+  const int tr = small ? 128 : tile_rows(a.d);
+  const int NT = (int)((a.M_local + tr - 1) / tr);
   if (MT == 0 || NT == 0) return cudaSuccess;
   const int units = MT * a.R;
   const int workers = units < NUM_WORKERS ? units : NUM_WORKERS;
@@ -811,6 +833,10 @@ cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st) {
   if (pair) {
     if (a.k <= 8) return launch_variant<8, false, true>(a, MT, NT, grid, slack, st);
     return launch_variant<16, false, true>(a, MT, NT, grid, slack, st);
+  }
+  if (small) {
+    if (a.k <= 8) return launch_variant<8, false, false, false, 128>(a, MT, NT, grid, 0, st);
+    return launch_variant<16, false, false, false, 128>(a, MT, NT, grid, 0, st);
   }
   if (a.k <= 8) return launch_variant<8, false, false>(a, MT, NT, grid, slack, st);
   return launch_variant<16, false, false>(a, MT, NT, grid, slack, st);

@@ -1664,8 +1664,10 @@ pas_status pas_debug_k2_schedule(int64_t N, int64_t M_local, int d, int64_t max_
   out[3] = dyn.MTg;
   out[4] = simtopk_pair(N, d) ? 1 : 0;
   out[5] = (int)((N + simtopk_box_q() - 1) / simtopk_box_q());
-  out[6] = (int)((M_local + 255) / 256);
+  const int tr = simtopk_tile_rows(N, M_local, d);
+  out[6] = (int)((M_local + tr - 1) / tr);
   out[7] = (int)(cap > INT32_MAX ? INT32_MAX : cap);
+  out[8] = tr;
   return PAS_OK;
 }
 

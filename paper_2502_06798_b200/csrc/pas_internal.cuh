@@ -262,6 +262,9 @@ struct SimTopkArgs {
 // Batches of at most this many prompts take K2's duplicated-row epilogue (K1 writes row p also at
 // p + 64); 0 for other shapes.
 int64_t simtopk_dup_rows(int64_t N, int d);
+// Small problems take a 128-row cache tile (simtopk_small); simtopk_tile_rows: 128 or 256.
+bool simtopk_small(int64_t N, int64_t M_local, int d);
+int simtopk_tile_rows(int64_t N, int64_t M_local, int d);
 cudaError_t launch_simtopk(const SimTopkArgs& a, cudaStream_t st);
 int simtopk_choose_ranges(int64_t N, int64_t M_local, int64_t cand_rows, int d);
 // The dynamic schedule's ranges R and chunk T for this batch, or false when the static schedule

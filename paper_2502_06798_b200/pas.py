@@ -397,11 +397,11 @@ def pas_last_launch_count(ctx) -> int:
 
 def pas_debug_k2_schedule(N, M_local, d=768, max_batch=None) -> dict:
     """K2's schedule for a batch (host logic, no device): R, T (0 = static), CS, MTg, pair, MT, NT."""
-    out = (C.c_int * 8)()
+    out = (C.c_int * 9)()
     st = lib.pas_debug_k2_schedule(N, M_local, d, N if max_batch is None else max_batch, out)
     if st != PAS_OK:
         raise PasError(st, "pas_debug_k2_schedule: bad arguments")
-    return dict(zip(("R", "T", "CS", "MTg", "pair", "MT", "NT", "cand_cap"), list(out)))
+    return dict(zip(("R", "T", "CS", "MTg", "pair", "MT", "NT", "cand_cap", "tile_rows"), list(out)))
 
 
 def pas_debug_qhat(ctx, out, stream=None):

@@ -23,7 +23,11 @@ CASES = [(N, M) for N in (1, 64, 256, 512, 513, 2048, 2200, 4096, 4097, 16384, 6
 def test_schedule_invariants(pas, N, M):
     s = pas.pas_debug_k2_schedule(N, M)
     MT, NT, R, T, CS = s["MT"], s["NT"], s["R"], s["T"], s["CS"]
-    assert MT == math.ceil(N / 128) and NT == math.ceil(M / 256)
+    small = N <= 128 and MT % 2 == 1 and math.ceil(M / 128) <= 128          # the 128-row cache tile
+    assert s["tile_rows"] == (128 if small else 256)
+    assert MT == math.ceil(N / 128) and NT == math.ceil(M / s["tile_rows"])
+    if small:
+        assert T == 0 and R == max(1, min(NT, s["cand_cap"] // max(N, 1)))   # one cache tile per CTA
     assert 1 <= R <= min(128, max(NT, 1)) and R * N <= s["cand_cap"]      # S-way merge, candidate buffer
     assert s["pair"] == (MT <= 4 and MT % 2 == 0)                          # CTA pair: whole tile pairs, N <= 512
     if T:
@@ -49,6 +53,7 @@ def test_bench_configs(pas):
     assert (c2["R"], c2["T"], c2["CS"]) == (10, 7, 6)
     c1 = pas.pas_debug_k2_schedule(64, 1000)
     assert c1["pair"] == 0 and c1["T"] == 0                                # one 128-row tile: a single CTA
+    assert c1["tile_rows"] == 128 and c1["R"] == 8                         # 8 CTAs of 128 cache rows
     assert pas.pas_debug_k2_schedule(256, 50_000_000)["pair"] == 1         # C5 at N = 256: the pair
 
 

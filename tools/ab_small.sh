@@ -1,12 +1,17 @@
-# C5 small batches (N = 256..2048 vs 50M): CTA-pair tile with the static schedule (default) vs the
-# single-CTA tile with the dynamic schedule (PAS_K2_PAIR_MAX_TILES=0); C3 K2 DRAM bytes (ncu).
-# Results: gpurun_out/small/
-set -u
-O=gpurun_out/small
+# K2's 128-row small-problem tile (simtopk_small) on vs off (PAS_K2_NO_SMALL), same box, alternating
+O=gpurun_out/ab_small
 mkdir -p $O
-PAS_K2_PAIR_MAX_TILES=0 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -s -k "c1_parity or ragged or fewer or topk_widths or k2_dyn" > $O/tests.log 2>&1; echo "rc=$?" >> $O/tests.log
-for v in 16 0; do
-  PAS_K2_PAIR_MAX_TILES=$v timeout 900 python tools/sweep.py --kind load --ns 256,512,1024,2048,4096 --steps 4 --warmup 2 > $O/c5_pair$v.jsonl 2> $O/c5_pair$v.err
+python -m paper_2502_06798_b200.build > /dev/null
+for rep in 1 2; do
+  for v in small nosmall; do
+    if [ $v = nosmall ]; then export PAS_K2_NO_SMALL=1; else unset PAS_K2_NO_SMALL; fi
+    for n in 1 64; do
+      C1_N=$n timeout 300 python tools/c1_latency.py > $O/c1_${v}_n${n}_$rep.json 2>&1
+      echo "$v n=$n $rep $(cat $O/c1_${v}_n${n}_$rep.json)"
+    done
+  done
 done
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct
-timeout 600 ncu --metrics $M --clock-control none -k regex:k_simtopk -c 1 --csv --log-file $O/ncu_c3.csv python bench.py --no-cpu-baseline --no-e2e --config C3 --steps 1 --warmup 1 > /dev/null 2>&1
+unset PAS_K2_NO_SMALL
+REPS=20 timeout 600 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file $O/c1_launches_small.csv python tools/c1_latency.py > /dev/null 2>&1
+PAS_K2_NO_SMALL=1 REPS=20 timeout 600 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file $O/c1_launches_nosmall.csv python tools/c1_latency.py > /dev/null 2>&1
+timeout 1500 python -m pytest tests/test_gpu_graph.py tests/test_gpu_parity.py tests/test_gpu_cache.py tests/test_gpu_nvtx.py tests/test_gpu_host_pipeline.py tests/test_gpu_dispatch.py -m gpu -q -x -k "not c4 and not c5" > $O/tests.log 2>&1; echo "tests rc=$?" >> $O/tests.log; tail -2 $O/tests.log

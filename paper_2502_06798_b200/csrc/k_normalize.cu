@@ -83,7 +83,9 @@ __device__ __forceinline__ void store_row4(__nv_bfloat16* dst, const float (&v)[
 #define PAS_K1_ACC 1      // independent fp64 partial sums per lane (shorter DFMA dependency chain)
 #endif
 
-template <typename T, int VEC>
+// DUP: every row is also written dup_rows rows further down (K2's duplicated-row small batches); a
+// compile-time switch so the common path carries no extra live state (40 registers, no spills).
+template <typename T, int VEC, bool DUP>
 __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restrict__ in, int64_t rows, int d,
                                                    __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ flags,
                                                    int64_t first_gid, int G, int rank, int* invalid_count,
@@ -139,12 +141,12 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       for (int c = 0; c < VEC; ++c) {
         float w[4];
         load4(src + c * 128 + lane * 4, w);
-        store_row4(dst + c * 128 + lane * 4, w, norm, valid, dup_rows ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
+        store_row4(dst + c * 128 + lane * 4, w, norm, valid, DUP ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
       }
 #else
 #pragma unroll
       for (int c = 0; c < VEC; ++c) {
-        store_row4(dst + c * 128 + lane * 4, v[c], norm, valid, dup_rows ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
+        store_row4(dst + c * 128 + lane * 4, v[c], norm, valid, DUP ? dst + dup_rows * d + c * 128 + lane * 4 : nullptr);
       }
 #endif
       if (lane == 0) {
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(256, PAS_K1_MINB) k_normalize(const T* __restr
       for (int c = lane * 4; c < d; c += 128) {
         float v[4];
         load4(src + c, v);
-        store_row4(dst + c, v, norm, valid, dup_rows ? dst + dup_rows * d + c : nullptr);
+        store_row4(dst + c, v, norm, valid, DUP ? dst + dup_rows * d + c : nullptr);
       }
       if (lane == 0) {
         if (flags) flags[orow] = valid ? 0 : PAS_FLAG_INVALID;
@@ -193,16 +195,19 @@ cudaError_t launch_t(const T* in, int64_t rows, int d, __nv_bfloat16* out, uint8
   const int64_t cap = (int64_t)kNumSMs * PAS_K1_MINB;
   if (PAS_K1_GRIDCAP && blocks > cap) blocks = cap;
   const unsigned g = (unsigned)blocks;
+  auto go = [&](auto kern) {
+    launch_pdl(kern, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup);
+  };
   switch (vec) {
-    case 1: launch_pdl(k_normalize<T, 1>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 2: launch_pdl(k_normalize<T, 2>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 3: launch_pdl(k_normalize<T, 3>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 4: launch_pdl(k_normalize<T, 4>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 5: launch_pdl(k_normalize<T, 5>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 6: launch_pdl(k_normalize<T, 6>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 7: launch_pdl(k_normalize<T, 7>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    case 8: launch_pdl(k_normalize<T, 8>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup); break;
-    default: launch_pdl(k_normalize<T, 0>, g, threads, 0, st, in, rows, d, out, flags, first_gid, G, rank, invalid_count, eb, dup);
+    case 1: dup ? go(k_normalize<T, 1, true>) : go(k_normalize<T, 1, false>); break;
+    case 2: dup ? go(k_normalize<T, 2, true>) : go(k_normalize<T, 2, false>); break;
+    case 3: dup ? go(k_normalize<T, 3, true>) : go(k_normalize<T, 3, false>); break;
+    case 4: dup ? go(k_normalize<T, 4, true>) : go(k_normalize<T, 4, false>); break;
+    case 5: dup ? go(k_normalize<T, 5, true>) : go(k_normalize<T, 5, false>); break;
+    case 6: dup ? go(k_normalize<T, 6, true>) : go(k_normalize<T, 6, false>); break;
+    case 7: dup ? go(k_normalize<T, 7, true>) : go(k_normalize<T, 7, false>); break;
+    case 8: dup ? go(k_normalize<T, 8, true>) : go(k_normalize<T, 8, false>); break;
+    default: dup ? go(k_normalize<T, 0, true>) : go(k_normalize<T, 0, false>);
   }
   return cudaGetLastError();
 }

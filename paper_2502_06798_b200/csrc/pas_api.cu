@@ -591,7 +591,7 @@ pas_status finish_batch(pas_ctx* ctx, int64_t N, cudaStream_t st) {
 extern "C" {
 
 const char* pas_version(void) {
-  return "libpas 0.5 (sm_100a; K2 tcgen05 cta_group::1 128x256 on a dynamic chunked schedule, cta_group::2 256x256 for N <= 512)";
+  return "libpas 0.6 (sm_100a; K2 tcgen05 cta_group::1 128x256 on a dynamic chunked schedule, cta_group::2 256x256 for even tile counts <= 4, 128x128 for one prompt tile vs small caches)";
 }
 
 const char* pas_last_error(const pas_ctx* ctx) { return ctx ? ctx->err.c_str() : g_global_err.c_str(); }
